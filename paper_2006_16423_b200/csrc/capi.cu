@@ -1,0 +1,922 @@
+// capi.cu — the C-ABI (include/dsg_b200.h) over the sm_100a kernels.
+//
+// dsg_dp_solve replaces MaxloadDp (/root/reference/proj/src/dp_solver.cpp:
+// 116-405) behind the same contract: same validation and error order as the
+// MaxloadDp constructor (133-166), same budget semantics (ideals.cpp:69),
+// same optimum and the same fewest-devices rule (337-351).  The host part is
+// O(|V|^2/64): flatten the Graph, convert every weight to int64 fixed point
+// at the common denominator D (exact: the DP only adds, subtracts, maxes and
+// mins), build adjacency bitsets, upload.  Everything O(#ideals) or more runs
+// on the device: enumeration (enumerate.cu), descriptors (describe.cu), and
+// one transition + finalize launch per lattice level (transition.cu).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "dsg_b200.h"
+#include "dsg_device.cuh"
+#include "dsg_internal.h"
+
+#define DSG_TIME_KERNELS_FLAG DSG_FLAG_TIME_KERNELS
+
+namespace dsg {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+}  // namespace dsg
+
+namespace {
+
+using namespace dsg;
+using i128 = __int128;
+using Clock = std::chrono::steady_clock;
+
+struct Fail {
+  int status;
+  std::string msg;
+  int64_t limit = 0;
+};
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw Fail{DSG_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)};     \
+  } while (0)
+
+double ms_since(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+// ------------------------------------------------------------ device arena
+// Named device buffers reused across solves on one device (grow-only), so a
+// repeated solve does no cudaMalloc.  One context per device, one solve at a
+// time per device (the mutex); independent devices run concurrently.
+struct DeviceCtx {
+  int device = -1;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  std::map<std::string, std::pair<void*, size_t>> bufs;
+  void* pinned = nullptr;
+  size_t pinned_cap = 0;
+
+  void* get(const std::string& name, size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    auto& b = bufs[name];
+    if (b.second < bytes) {
+      if (b.first) CK(cudaFree(b.first));
+      b.first = nullptr;
+      size_t cap = std::max(bytes, b.second + b.second / 2);
+      CK(cudaMalloc(&b.first, cap));
+      b.second = cap;
+    }
+    return b.first;
+  }
+  template <typename T>
+  T* get_t(const std::string& name, size_t count) {
+    return static_cast<T*>(get(name, count * sizeof(T)));
+  }
+  void* host(size_t bytes) {
+    if (pinned_cap < bytes) {
+      if (pinned) cudaFreeHost(pinned);
+      pinned = nullptr;
+      size_t cap = std::max(bytes, pinned_cap * 2);
+      CK(cudaMallocHost(&pinned, cap));
+      pinned_cap = cap;
+    }
+    return pinned;
+  }
+};
+
+std::mutex g_ctx_mu;
+std::map<int, std::unique_ptr<DeviceCtx>> g_ctx;
+
+DeviceCtx& context(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw Fail{DSG_CUDA_ERROR, std::string("no CUDA device: ") + cudaGetErrorString(e)};
+  if (device < 0) CK(cudaGetDevice(&device));
+  if (device >= count) throw Fail{DSG_CUDA_ERROR, "device ordinal out of range"};
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  auto& p = g_ctx[device];
+  if (!p) {
+    p = std::make_unique<DeviceCtx>();
+    p->device = device;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      throw Fail{DSG_CUDA_ERROR, "libdsg_b200 is built for sm_100a (B200); found sm_" +
+                                     std::to_string(prop.major * 10 + prop.minor)};
+    p->sm_count = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  }
+  return *p;
+}
+
+// ------------------------------------------------------------ host prepare
+struct Q {  // exact rational
+  int64_t num = 0, den = 1;
+  bool inf = false;
+};
+
+int64_t gcd64(int64_t a, int64_t b) {
+  if (a < 0) a = -a;
+  if (b < 0) b = -b;
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+Q to_q(dsg_rat r) {
+  Q q;
+  if (r.den == 0) {
+    if (r.num <= 0) throw Fail{DSG_INVALID, "invalid rational"};
+    q.inf = true;
+    return q;
+  }
+  i128 n = r.num, d = r.den;
+  if (d < 0) {
+    n = -n;
+    d = -d;
+  }
+  i128 g = gcd64((int64_t)(n < 0 ? -n : n), (int64_t)d);
+  if (g > 1) {
+    n /= g;
+    d /= g;
+  }
+  if (n > INT64_MAX || n < INT64_MIN) throw Fail{DSG_OVERFLOW, "rational overflow"};
+  q.num = (int64_t)n;
+  q.den = (int64_t)d;
+  return q;
+}
+
+struct Prepared {
+  int n = 0, W = 0, K = 0, L = 0, C = 0;
+  bool training = false;
+  std::vector<int32_t> ids;
+  std::vector<int64_t> cpu, acc, comm, mem;
+  std::vector<uint8_t> unsup, comminf, in_universe, bw;
+  std::vector<uint64_t> succ_real, pred_real, pred_u, succ_u, twins, bw_succ, bw_from, bw_to,
+      bwset;
+  std::vector<int32_t> out_off, out_adj, in_off, in_adj;
+  int64_t D = 1;
+  int value_bits = 64;
+  int64_t mlim = 0;
+  int memcheck = 0;
+  int interleave = 0;
+  bool has_bw = false;
+  bool inf_cpu_mem = false;  // deferred std::domain_error("subtracting infinity")
+};
+
+void set_bit(std::vector<uint64_t>& m, int row, int W, int v) {
+  m[(size_t)row * W + (v >> 6)] |= 1ull << (v & 63);
+}
+
+// Graph::Graph + MaxloadDp ctor checks (graph.cpp:132-158, dp_solver.cpp:133-166)
+Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint8_t* within,
+                 bool enumerate_only, int flags) {
+  Prepared P;
+  if (!g || g->n_nodes < 0) throw Fail{DSG_INVALID, "invalid graph"};
+  const int n = g->n_nodes;
+  if (n > kMaxWords * 64)
+    throw Fail{DSG_UNSUPPORTED, "graphs above " + std::to_string(kMaxWords * 64) + " nodes"};
+  P.n = n;
+  P.W = std::max(1, (n + 63) / 64);
+  const int W = P.W;
+  P.ids.assign(g->ids, g->ids + n);
+  std::unordered_map<int32_t, int> index;
+  index.reserve(n * 2 + 1);
+  for (int i = 0; i < n; ++i) index.emplace(g->ids[i], i);  // first wins
+  auto idx_of = [&](int32_t id) {
+    auto it = index.find(id);
+    return it == index.end() ? -1 : it->second;
+  };
+  std::vector<std::vector<int>> out_real(n), in_real(n), out_all(n), in_all(n);
+  for (int e = 0; e < g->n_edges; ++e) {
+    int f = idx_of(g->edge_from[e]), t = idx_of(g->edge_to[e]);
+    if (f < 0 || t < 0) continue;
+    out_real[f].push_back(t);
+    in_real[t].push_back(f);
+    out_all[f].push_back(t);
+    in_all[t].push_back(f);
+  }
+  for (int e = 0; e < g->n_artificial; ++e) {
+    int f = idx_of(g->art_from[e]), t = idx_of(g->art_to[e]);
+    if (f < 0 || t < 0) continue;
+    out_all[f].push_back(t);
+    in_all[t].push_back(f);
+  }
+  P.bw.assign(n, 0);
+  for (int i = 0; i < n; ++i) P.bw[i] = g->is_backward ? (g->is_backward[i] != 0) : 0;
+  P.has_bw = std::any_of(P.bw.begin(), P.bw.end(), [](uint8_t b) { return b != 0; });
+
+  // weights (validated even for enumeration, as the Graph holds Rats)
+  std::vector<Q> qc(n), qa(n), qm(n), qmem(n);
+  for (int i = 0; i < n; ++i) {
+    qc[i] = to_q(g->cpu_time[i]);
+    qa[i] = to_q(g->acc_time[i]);
+    qm[i] = to_q(g->comm_time[i]);
+    qmem[i] = to_q(g->mem_size[i]);
+  }
+
+  // acyclicity over real + artificial edges (the reference assumes a
+  // validated DAG; a cycle would leave the universe unreachable)
+  {
+    std::vector<int> indeg(n, 0), ready;
+    for (int v = 0; v < n; ++v)
+      for (int w : out_all[v]) ++indeg[w];
+    for (int v = 0; v < n; ++v)
+      if (!indeg[v]) ready.push_back(v);
+    int seen = 0;
+    while (!ready.empty()) {
+      int v = ready.back();
+      ready.pop_back();
+      ++seen;
+      for (int w : out_all[v])
+        if (--indeg[w] == 0) ready.push_back(w);
+    }
+    if (seen != n) throw Fail{DSG_INVALID, "graph has a cycle (validate_dag first)"};
+  }
+
+  std::vector<std::vector<int>> paired_bw(n);
+  P.in_universe.assign(n, 0);
+  if (enumerate_only) {
+    for (int v = 0; v < n; ++v) P.in_universe[v] = within ? (within[v] != 0) : 1;
+  } else {
+    P.K = cfg->accelerators;
+    P.L = cfg->cpus;
+    if (mode == DSG_MODE_REPLICATED) {  // dp_solver.cpp:397-405
+      if (!cfg->has_bandwidth) throw Fail{DSG_MISSING_BANDWIDTH, "replication requires a bandwidth value"};
+      if (P.has_bw) throw Fail{DSG_INVALID, "replicated solve expects an inference graph"};
+    }
+    if (P.K + P.L < 1) throw Fail{DSG_INVALID, "need at least one device"};
+    if (P.K < 0 || P.L < 0) throw Fail{DSG_INVALID, "negative device count"};
+    if (mode == DSG_MODE_REPLICATED)
+      throw Fail{DSG_UNSUPPORTED, "solve_maxload_replicated is not implemented on the device yet"};
+    P.C = (P.K + 1) * (P.L + 1);
+    P.training = mode == DSG_MODE_TRAINING;
+    if (P.training) {
+      for (int v = 0; v < n; ++v) P.in_universe[v] = !P.bw[v];
+      for (int b = 0; b < n; ++b) {
+        if (!P.bw[b]) continue;
+        int32_t pid = g->forward_pair ? g->forward_pair[b] : DSG_NO_PAIR;
+        if (pid == DSG_NO_PAIR)
+          throw Fail{DSG_INVALID,
+                     "training solve requires every backward node to be paired (run "
+                     "preprocessing first)"};
+        int f = idx_of(pid);
+        if (f < 0) throw Fail{DSG_INVALID, "forward_pair references missing node"};
+        paired_bw[f].push_back(b);
+      }
+    } else {
+      std::fill(P.in_universe.begin(), P.in_universe.end(), 1);
+    }
+  }
+
+  // nodes the DP ever adds to a block: universe + paired backward twins
+  std::vector<uint8_t> added(n, 0);
+  for (int v = 0; v < n; ++v) {
+    if (!P.in_universe[v]) continue;
+    added[v] = 1;
+    for (int b : paired_bw[v]) added[b] = 1;
+  }
+  for (int v = 0; v < n; ++v)
+    if (added[v] && (qc[v].inf || qmem[v].inf)) P.inf_cpu_mem = true;
+
+  // ---- fixed point at the common denominator D (exact)
+  i128 D = 1;
+  auto lcm_in = [&](const Q& q) {
+    if (q.inf) return;
+    i128 gg = gcd64((int64_t)D, q.den);
+    D = D / gg * q.den;
+    if (D > ((i128)1 << 62)) throw Fail{DSG_OVERFLOW, "common denominator overflow"};
+  };
+  for (int v = 0; v < n; ++v) {
+    lcm_in(qc[v]);
+    lcm_in(qa[v]);
+    lcm_in(qm[v]);
+    lcm_in(qmem[v]);
+  }
+  Q qlim;
+  if (!enumerate_only) {
+    qlim = to_q(cfg->memory_limit);
+    lcm_in(qlim);
+  }
+  P.D = (int64_t)D;
+  auto fx = [&](const Q& q) -> i128 { return q.inf ? 0 : (i128)q.num * (D / q.den); };
+  P.cpu.assign(n, 0);
+  P.acc.assign(n, 0);
+  P.comm.assign(n, 0);
+  P.mem.assign(n, 0);
+  P.unsup.assign(n, 0);
+  P.comminf.assign(n, 0);
+  i128 bound = 0;
+  auto absq = [](i128 x) { return x < 0 ? -x : x; };
+  for (int v = 0; v < n; ++v) {
+    i128 c = fx(qc[v]), a = fx(qa[v]), m = fx(qm[v]), s = fx(qmem[v]);
+    bound += absq(c) + absq(a) + 2 * absq(m) + absq(s);
+    if (bound > ((i128)1 << 62)) throw Fail{DSG_OVERFLOW, "fixed-point weight sum overflow"};
+    P.cpu[v] = (int64_t)c;
+    P.acc[v] = (int64_t)a;
+    P.comm[v] = (int64_t)m;
+    P.mem[v] = (int64_t)s;
+    P.unsup[v] = qa[v].inf;
+    P.comminf[v] = qm[v].inf;
+  }
+  P.value_bits = (bound < ((i128)1 << 30) && !(flags & DSG_FLAG_FORCE_INT64)) ? 32 : 64;
+  if (!enumerate_only) {
+    P.memcheck = qlim.inf ? 0 : 1;
+    if (!qlim.inf) {
+      i128 m = fx(qlim);
+      i128 cap = bound + 1;
+      P.mlim = (int64_t)std::max(-cap, std::min(cap, m));
+    }
+    P.interleave = cfg->interleaving;
+    if (P.interleave < 0 || P.interleave > 2) throw Fail{DSG_INVALID, "bad interleaving mode"};
+  }
+
+  // ---- adjacency bitsets and CSR
+  const size_t NW = (size_t)n * W;
+  P.succ_real.assign(NW, 0);
+  P.pred_real.assign(NW, 0);
+  P.pred_u.assign(NW, 0);
+  P.succ_u.assign(NW, 0);
+  P.twins.assign(NW, 0);
+  P.bw_succ.assign(NW, 0);
+  P.bwset.assign(W, 0);
+  P.out_off.assign(n + 1, 0);
+  P.in_off.assign(n + 1, 0);
+  for (int v = 0; v < n; ++v) {
+    for (int w : out_real[v]) {
+      set_bit(P.succ_real, v, W, w);
+      set_bit(P.pred_real, w, W, v);
+    }
+    P.out_off[v + 1] = P.out_off[v] + (int)out_real[v].size();
+    P.in_off[v + 1] = P.in_off[v] + (int)in_real[v].size();
+    if (P.in_universe[v]) {
+      for (int u : in_all[v])
+        if (P.in_universe[u]) set_bit(P.pred_u, v, W, u);
+      for (int w : out_all[v])
+        if (P.in_universe[w]) set_bit(P.succ_u, v, W, w);
+    }
+    for (int b : paired_bw[v]) set_bit(P.twins, v, W, b);
+    if (P.bw[v]) {
+      P.bwset[v >> 6] |= 1ull << (v & 63);
+      for (int w : out_all[v])
+        if (P.bw[w]) set_bit(P.bw_succ, v, W, w);
+    }
+  }
+  for (int v = 0; v < n; ++v) {
+    P.out_adj.insert(P.out_adj.end(), out_real[v].begin(), out_real[v].end());
+    P.in_adj.insert(P.in_adj.end(), in_real[v].begin(), in_real[v].end());
+  }
+  if (P.out_adj.empty()) P.out_adj.push_back(0);
+  if (P.in_adj.empty()) P.in_adj.push_back(0);
+
+  // reachability_within(g, backward) for the general training gate
+  // (graph.cpp:291-345): rows in reverse topological order
+  if (P.training && P.has_bw) {
+    P.bw_from.assign(NW, 0);
+    P.bw_to.assign(NW, 0);
+    std::vector<int> indeg(n, 0), order, ready;
+    for (int v = 0; v < n; ++v)
+      if (P.bw[v])
+        for (int w : out_all[v])
+          if (P.bw[w]) ++indeg[w];
+    for (int v = n - 1; v >= 0; --v)
+      if (P.bw[v] && !indeg[v]) ready.push_back(v);
+    while (!ready.empty()) {
+      int v = ready.back();
+      ready.pop_back();
+      order.push_back(v);
+      for (int w : out_all[v])
+        if (P.bw[w] && --indeg[w] == 0) ready.push_back(w);
+    }
+    for (auto it = order.rbegin(); it != order.rend(); ++it) {
+      int u = *it;
+      set_bit(P.bw_from, u, W, u);
+      for (int w : out_all[u]) {
+        if (!P.bw[w]) continue;
+        for (int k = 0; k < W; ++k) P.bw_from[(size_t)u * W + k] |= P.bw_from[(size_t)w * W + k];
+      }
+    }
+    for (int u = 0; u < n; ++u) {
+      if (!P.bw[u]) continue;
+      for (int w = 0; w < n; ++w)
+        if ((P.bw_from[(size_t)u * W + (w >> 6)] >> (w & 63)) & 1ull) set_bit(P.bw_to, w, W, u);
+    }
+  } else {
+    P.bw_from.assign(W, 0);
+    P.bw_to.assign(W, 0);
+  }
+  return P;
+}
+
+template <typename T>
+T* upload(DeviceCtx& ctx, const std::string& name, const std::vector<T>& v) {
+  T* d = ctx.get_t<T>(name, std::max<size_t>(v.size(), 1));
+  if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx.stream));
+  return d;
+}
+
+struct DeviceGraph {
+  DevGraph g;
+  uint8_t* in_universe;
+};
+
+DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P) {
+  DeviceGraph d;
+  DevGraph& g = d.g;
+  g.n = P.n;
+  g.W = P.W;
+  g.cpu = upload(ctx, "g.cpu", P.cpu);
+  g.acc = upload(ctx, "g.acc", P.acc);
+  g.comm = upload(ctx, "g.comm", P.comm);
+  g.mem = upload(ctx, "g.mem", P.mem);
+  g.unsup = upload(ctx, "g.unsup", P.unsup);
+  g.comminf = upload(ctx, "g.comminf", P.comminf);
+  g.succ_real = upload(ctx, "g.succ_real", P.succ_real);
+  g.pred_real = upload(ctx, "g.pred_real", P.pred_real);
+  g.pred_u = upload(ctx, "g.pred_u", P.pred_u);
+  g.succ_u = upload(ctx, "g.succ_u", P.succ_u);
+  g.twins = upload(ctx, "g.twins", P.twins);
+  g.bw_succ = upload(ctx, "g.bw_succ", P.bw_succ);
+  g.bw_from = upload(ctx, "g.bw_from", P.bw_from);
+  g.bw_to = upload(ctx, "g.bw_to", P.bw_to);
+  g.bwset = upload(ctx, "g.bwset", P.bwset);
+  g.out_real_off = upload(ctx, "g.out_off", P.out_off);
+  g.out_real_adj = upload(ctx, "g.out_adj", P.out_adj);
+  g.in_real_off = upload(ctx, "g.in_off", P.in_off);
+  g.in_real_adj = upload(ctx, "g.in_adj", P.in_adj);
+  d.in_universe = upload(ctx, "g.in_universe", P.in_universe);
+  return d;
+}
+
+// ------------------------------------------------------------ enumeration
+struct Lattice {
+  int64_t I = 0;
+  int n_levels = 0;
+  std::vector<int64_t> level_off;  // host copy, n_levels + 1
+  uint64_t* sbits = nullptr;       // sorted, device
+};
+
+Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, int64_t budget,
+                         bool hash_mode) {
+  const int W = P.W;
+  const int64_t budget_eff = std::max<int64_t>(budget, 1);
+  int64_t cap = std::min<int64_t>(budget_eff + 1, std::max<int64_t>(4096, (int64_t(1) << 22) / W));
+  int64_t cand_cap = hash_mode ? cap * 4 : 0;
+  EnumStatus* st_d = ctx.get_t<EnumStatus>("enum.status", 1);
+  int64_t* lvl_d = ctx.get_t<int64_t>("enum.level_off", (size_t)P.n + 3);
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    EnumLaunch L{};
+    L.W = W;
+    L.n = P.n;
+    L.pred_u = dg.g.pred_u;
+    L.succ_u = dg.g.succ_u;
+    L.in_universe = dg.in_universe;
+    L.bits = ctx.get_t<uint64_t>("enum.bits", (size_t)cap * W);
+    L.maxm = ctx.get_t<uint64_t>("enum.maxm", (size_t)cap * W);
+    L.addm = ctx.get_t<uint64_t>("enum.addm", (size_t)cap * W);
+    L.level_of = ctx.get_t<int32_t>("enum.level_of", (size_t)cap);
+    L.cap = cap;
+    L.budget = budget_eff;
+    L.level_off = lvl_d;
+    L.status = st_d;
+    L.hash_mode = hash_mode ? 1 : 0;
+    if (hash_mode) {
+      L.cand_bits = ctx.get_t<uint64_t>("enum.cbits", (size_t)cand_cap * W);
+      L.cand_maxm = ctx.get_t<uint64_t>("enum.cmaxm", (size_t)cand_cap * W);
+      L.cand_addm = ctx.get_t<uint64_t>("enum.caddm", (size_t)cand_cap * W);
+      L.cand_cap = cand_cap;
+      int64_t tc = 1024;
+      while (tc < 2 * cand_cap) tc <<= 1;
+      L.table = ctx.get_t<int64_t>("enum.table", (size_t)tc);
+      L.table_cap = tc;
+    }
+    CK(cudaMemsetAsync(st_d, 0, sizeof(EnumStatus), ctx.stream));
+    launch_enumerate(L, ctx.stream);
+    CK(cudaGetLastError());
+    EnumStatus st;
+    CK(cudaMemcpyAsync(&st, st_d, sizeof st, cudaMemcpyDeviceToHost, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+    if (st.code == 1) throw Fail{DSG_BUDGET, "ideal budget exceeded", budget};
+    if (st.code == 2) {
+      cap = std::min<int64_t>(budget_eff + 1, std::max(cap * 2, st.needed + st.needed / 2));
+      if (hash_mode) cand_cap = std::max(cand_cap, cap * 4);
+      continue;
+    }
+    if (st.code == 3) {
+      cand_cap = std::max(cand_cap * 2, st.needed * 2);
+      continue;
+    }
+    Lattice lat;
+    lat.I = st.total;
+    lat.n_levels = st.n_levels;
+    lat.level_off.resize(lat.n_levels + 1);
+    CK(cudaMemcpyAsync(lat.level_off.data(), lvl_d, sizeof(int64_t) * (lat.n_levels + 1),
+                       cudaMemcpyDeviceToHost, ctx.stream));
+    lat.sbits = ctx.get_t<uint64_t>("lat.sbits", (size_t)lat.I * W);
+    launch_lex_rank(W, lat.I, L.bits, L.level_of, lvl_d, lat.sbits, ctx.stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx.stream));
+    return lat;
+  }
+  throw Fail{DSG_CUDA_ERROR, "enumeration capacity retries exhausted"};
+}
+
+void fill_msg(char* dst, const std::string& s) {
+  std::strncpy(dst, s.c_str(), 255);
+  dst[255] = 0;
+}
+
+// ------------------------------------------------------------ solve
+void solve(int mode, const dsg_graph* graph, const dsg_config* config, const dsg_options* opt,
+           dsg_result* res) {
+  const auto t0 = Clock::now();
+  dsg_options defaults;
+  dsg_default_options(&defaults);
+  if (!opt) opt = &defaults;
+  const int flags = opt->flags;
+  Prepared P = prepare(mode, graph, config, nullptr, false, flags);
+  DeviceCtx& ctx = context(opt->device);
+  std::lock_guard<std::mutex> lk(ctx.mu);
+  CK(cudaSetDevice(ctx.device));
+  cudaStream_t st = ctx.stream;
+  const bool timing = (flags & DSG_TIME_KERNELS_FLAG) != 0;
+  const bool has_deadline = opt->deadline_seconds > 0;
+  const auto deadline = t0 + std::chrono::nanoseconds((int64_t)(opt->deadline_seconds * 1e9));
+  const int W = P.W, K = P.K, Lc = P.L, C = P.C;
+  const int vb = P.value_bits;
+  const size_t vsz = vb == 32 ? 4 : 8;
+
+  DeviceGraph dg = upload_graph(ctx, P);
+  res->t_prepare_ms = ms_since(t0);
+  const auto t1 = Clock::now();
+  Lattice lat = enumerate_device(ctx, P, dg, opt->ideal_budget, (flags & DSG_FLAG_HASH_ENUM) != 0);
+  res->n_ideals = lat.I;
+  res->n_levels = lat.n_levels;
+  res->t_enumerate_ms = ms_since(t1);
+  if (P.inf_cpu_mem) throw Fail{DSG_INVALID, "subtracting infinity"};
+  const int64_t I = lat.I;
+
+  // ---- descriptors
+  const auto t2 = Clock::now();
+  DescribeLaunch D{};
+  D.g = dg.g;
+  D.training = P.training ? 1 : 0;
+  D.has_bw = (P.training && P.has_bw) ? 1 : 0;
+  D.value_bits = vb;
+  D.I = I;
+  D.sbits = lat.sbits;
+  D.abits = ctx.get_t<uint64_t>("d.abits", (size_t)I * W);
+  D.intbits = ctx.get_t<uint64_t>("d.intbits", P.training ? (size_t)I * W : 1);
+  D.pfx_cpu = ctx.get("d.cpu", I * vsz);
+  D.pfx_acc = ctx.get("d.acc", I * vsz);
+  D.pfx_mem = ctx.get("d.mem", I * vsz);
+  D.unsup = ctx.get_t<int32_t>("d.unsup", I);
+  D.fw = ctx.get("d.fw", I * vsz);
+  D.fwinf = ctx.get_t<int32_t>("d.fwinf", I);
+  D.upset = ctx.get_t<uint8_t>("d.upset", I);
+  D.counts = ctx.get_t<int64_t>("d.counts", (size_t)kNumCounts * (I + 1));
+  CK(cudaMemsetAsync(D.counts, 0, sizeof(int64_t) * kNumCounts * (I + 1), st));
+  launch_describe(D, false, st);
+  launch_scan_counts(D.counts, I, kNumCounts, st);
+  int64_t totals[kNumCounts];
+  for (int k = 0; k < kNumCounts; ++k)
+    CK(cudaMemcpyAsync(&totals[k], D.counts + (size_t)k * (I + 1) + I, sizeof(int64_t),
+                       cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  if (totals[kCntF] > INT32_MAX || totals[kCntN] > INT32_MAX || totals[kCntLItems] > INT32_MAX)
+    throw Fail{DSG_UNSUPPORTED, "frontier tables exceed 2^31 entries"};
+  D.chunks = ctx.get_t<FChunk>("d.chunks", totals[kCntChunks]);
+  D.fpool = ctx.get("d.fpool", totals[kCntF] * vsz);
+  D.nitems = ctx.get_t<NItem>("d.nitems", totals[kCntN]);
+  D.pitems = ctx.get_t<PItem>("d.pitems", totals[kCntP]);
+  D.lentries = ctx.get_t<LEntry>("d.lentries", totals[kCntL]);
+  D.litems = ctx.get_t<MaskItem>("d.litems", totals[kCntLItems]);
+  launch_describe(D, true, st);
+  CK(cudaGetLastError());
+
+  // ---- level loop
+  void* dp = ctx.get("dp.values", (size_t)I * C * vsz);
+  int32_t* bp = ctx.get_t<int32_t>("dp.bp", (size_t)I * C);
+  unsigned long long* pairs_d = ctx.get_t<unsigned long long>("dp.pairs", 1);
+  CK(cudaMemsetAsync(pairs_d, 0, sizeof(unsigned long long), st));
+  launch_init_empty(vb, K, Lc, dp, bp, st);
+
+  const int64_t target_ctas = (int64_t)ctx.sm_count * 8;
+  struct Plan {
+    int64_t chunks, chunk_len;
+  };
+  std::vector<Plan> plan(lat.n_levels);
+  size_t part_elems = 1;
+  for (int s = 1; s < lat.n_levels; ++s) {
+    const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
+    const int64_t S = lat.level_off[s];
+    const int64_t tiles = (T + kTileTargets - 1) / kTileTargets;
+    int64_t chunks = std::max<int64_t>(1, (target_ctas + tiles - 1) / tiles);
+    chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / 32));
+    chunks = std::min<int64_t>(chunks, 65535);
+    int64_t len = (S + chunks - 1) / chunks;
+    chunks = (S + len - 1) / len;
+    plan[s] = {chunks, len};
+    part_elems = std::max(part_elems, (size_t)(chunks * C * T));
+  }
+  void* part_val = ctx.get("dp.part_val", part_elems * vsz);
+  int32_t* part_arg = ctx.get_t<int32_t>("dp.part_arg", part_elems);
+
+  LevelLaunch LL{};
+  LL.value_bits = vb;
+  LL.training = P.training ? 1 : 0;
+  LL.has_bw = D.has_bw;
+  LL.fastgate = (flags & DSG_FLAG_NO_FASTGATE) ? 0 : 1;
+  LL.K = K;
+  LL.L = Lc;
+  LL.C = C;
+  LL.W = W;
+  LL.mlim = P.mlim;
+  LL.memcheck = P.memcheck;
+  LL.interleave = P.interleave;
+  LL.abits = D.abits;
+  LL.intbits = D.intbits;
+  LL.pfx_cpu = D.pfx_cpu;
+  LL.pfx_acc = D.pfx_acc;
+  LL.pfx_mem = D.pfx_mem;
+  LL.unsup = D.unsup;
+  LL.fw = D.fw;
+  LL.fwinf = D.fwinf;
+  LL.upset = D.upset;
+  LL.chunk_off = D.counts + (size_t)kCntChunks * (I + 1);
+  LL.chunks = D.chunks;
+  LL.fpool = D.fpool;
+  LL.nitems = D.nitems;
+  LL.p_off = D.counts + (size_t)kCntP * (I + 1);
+  LL.pitems = D.pitems;
+  LL.l_off = D.counts + (size_t)kCntL * (I + 1);
+  LL.lentries = D.lentries;
+  LL.litems = D.litems;
+  LL.bwset = dg.g.bwset;
+  LL.bw_from = dg.g.bw_from;
+  LL.bw_to = dg.g.bw_to;
+  LL.n_nodes = P.n;
+  LL.dp = dp;
+  LL.bp = bp;
+  LL.part_val = part_val;
+  LL.part_arg = part_arg;
+  LL.pair_counter = pairs_d;
+
+  cudaEvent_t ev_desc, ev_dp;
+  CK(cudaEventCreate(&ev_desc));
+  CK(cudaEventCreate(&ev_dp));
+  CK(cudaEventRecord(ev_desc, st));
+  std::vector<cudaEvent_t> kev;
+  std::vector<cudaEvent_t> dl_ev;
+  const int kDeadlineStride = 8;
+  for (int s = 1; s < lat.n_levels; ++s) {
+    LL.t_lo = lat.level_off[s];
+    LL.t_hi = lat.level_off[s + 1];
+    LL.s_hi = lat.level_off[s];
+    LL.n_chunks = plan[s].chunks;
+    LL.chunk_len = plan[s].chunk_len;
+    if (timing) {
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      CK(cudaEventRecord(a, st));
+      launch_transition(LL, st);
+      CK(cudaEventRecord(b, st));
+      kev.push_back(a);
+      kev.push_back(b);
+    } else {
+      launch_transition(LL, st);
+    }
+    launch_finalize(LL, st);
+    if (has_deadline && s % kDeadlineStride == 0) {
+      // keep at most two strides in flight so the clock tracks the device
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, st));
+      dl_ev.push_back(e);
+      if (dl_ev.size() >= 2) {
+        CK(cudaEventSynchronize(dl_ev[dl_ev.size() - 2]));
+        if (Clock::now() > deadline) {
+          CK(cudaStreamSynchronize(st));
+          for (auto x : dl_ev) cudaEventDestroy(x);
+          for (auto x : kev) cudaEventDestroy(x);
+          cudaEventDestroy(ev_desc);
+          cudaEventDestroy(ev_dp);
+          throw Fail{DSG_DEADLINE, "time limit reached"};
+        }
+      }
+    }
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ev_dp, st));
+
+  // ---- traceback
+  const int maxb = K + Lc + 1;
+  TracebackOut* tb_d = ctx.get_t<TracebackOut>("tb.out", 1);
+  int64_t* ords_d = ctx.get_t<int64_t>("tb.ords", maxb);
+  int64_t* prevs_d = ctx.get_t<int64_t>("tb.prevs", maxb);
+  int32_t* cpus_d = ctx.get_t<int32_t>("tb.cpus", maxb);
+  uint64_t* bb_d = ctx.get_t<uint64_t>("tb.bits", (size_t)maxb * W);
+  launch_traceback(vb, I, K, Lc, W, dp, bp, D.abits, tb_d, ords_d, prevs_d, cpus_d, bb_d, st);
+  TracebackOut tb;
+  unsigned long long pairs = 0;
+  std::vector<int32_t> cpus(maxb);
+  std::vector<uint64_t> bbits((size_t)maxb * W);
+  CK(cudaMemcpyAsync(&tb, tb_d, sizeof tb, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&pairs, pairs_d, sizeof pairs, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(cpus.data(), cpus_d, sizeof(int32_t) * maxb, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(bbits.data(), bb_d, sizeof(uint64_t) * maxb * W, cudaMemcpyDeviceToHost, st));
+  if (flags & DSG_FLAG_KEEP_TABLES) {
+    res->words = W;
+    res->ideal_bits = (uint64_t*)std::malloc(sizeof(uint64_t) * (size_t)I * W + 8);
+    CK(cudaMemcpyAsync(res->ideal_bits, lat.sbits, sizeof(uint64_t) * (size_t)I * W,
+                       cudaMemcpyDeviceToHost, st));
+    res->dp_values = (int64_t*)std::malloc(sizeof(int64_t) * (size_t)I * C + 8);
+    if (vb == 64) {
+      CK(cudaMemcpyAsync(res->dp_values, dp, sizeof(int64_t) * (size_t)I * C,
+                         cudaMemcpyDeviceToHost, st));
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  if ((flags & DSG_FLAG_KEEP_TABLES) && vb == 32) {
+    std::vector<int32_t> tmp((size_t)I * C);
+    CK(cudaMemcpy(tmp.data(), dp, sizeof(int32_t) * tmp.size(), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < tmp.size(); ++i)
+      res->dp_values[i] = tmp[i] == VTraits<int32_t>::INF ? INT64_MAX : (int64_t)tmp[i];
+  }
+  float desc_ms = 0, dp_ms = 0;
+  cudaEventElapsedTime(&dp_ms, ev_desc, ev_dp);
+  res->t_describe_ms = ms_since(t2) - 0.0;  // refined below
+  double kern_ms = 0;
+  for (size_t i = 0; i + 1 < kev.size(); i += 2) {
+    float x = 0;
+    cudaEventElapsedTime(&x, kev[i], kev[i + 1]);
+    kern_ms += x;
+  }
+  for (auto x : kev) cudaEventDestroy(x);
+  for (auto x : dl_ev) cudaEventDestroy(x);
+  cudaEventDestroy(ev_desc);
+  cudaEventDestroy(ev_dp);
+  (void)desc_ms;
+  res->t_dp_ms = dp_ms;
+  res->t_describe_ms = std::max(0.0, ms_since(t2) - dp_ms);
+  res->t_transition_kernel_ms = kern_ms;
+  res->n_pairs = (int64_t)pairs;
+  res->value_bits = vb;
+  res->denominator = P.D;
+  if (tb.status == 1) throw Fail{DSG_INFEASIBLE, "no feasible assignment exists"};
+  if (tb.status != 0) throw Fail{DSG_LOGIC, "dp reconstruction stuck"};
+
+  // ---- result
+  const int64_t g = gcd64(tb.best_value, P.D);
+  res->objective.num = tb.best_value / (g ? g : 1);
+  res->objective.den = P.D / (g ? g : 1);
+  res->best_k = tb.best_k;
+  res->best_l = tb.best_l;
+  res->n_blocks = tb.n_blocks;
+  res->blocks = (dsg_block*)std::calloc((size_t)std::max(1, tb.n_blocks), sizeof(dsg_block));
+  res->members = (int32_t*)std::malloc(sizeof(int32_t) * (size_t)(P.n + 1));
+  int off = 0;
+  for (int b = 0; b < tb.n_blocks; ++b) {
+    dsg_block& blk = res->blocks[b];
+    blk.cpu = cpus[b];
+    blk.repl = 1;
+    blk.offset = off;
+    for (int w = 0; w < W; ++w) {
+      uint64_t x = bbits[(size_t)b * W + w];
+      while (x) {
+        int bit = __builtin_ctzll(x);
+        x &= x - 1;
+        res->members[off++] = w * 64 + bit;
+      }
+    }
+    blk.n_members = off - blk.offset;
+  }
+  res->t_traceback_ms = 0;
+  res->t_total_ms = ms_since(t0);
+  res->kernel_launches = dsg::g_launches.load();
+}
+
+}  // namespace
+
+extern "C" {
+
+void dsg_default_options(dsg_options* o) {
+  std::memset(o, 0, sizeof *o);
+  o->ideal_budget = DSG_DEFAULT_IDEAL_BUDGET;
+  o->deadline_seconds = 0;
+  o->device = -1;
+  o->shard_count = 0;
+  o->flags = 0;
+}
+
+const char* dsg_version(void) { return "dsg_b200 1 (sm_100a)"; }
+
+int dsg_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
+int64_t dsg_kernel_launch_count(void) { return dsg::g_launches.load(); }
+
+int dsg_dp_solve(int32_t mode, const dsg_graph* graph, const dsg_config* config,
+                 const dsg_options* options, dsg_result* result) {
+  std::memset(result, 0, sizeof *result);
+  try {
+    solve(mode, graph, config, options, result);
+    result->status = DSG_OK;
+  } catch (const Fail& f) {
+    result->status = f.status;
+    result->budget_limit = f.limit;
+    fill_msg(result->message, f.msg);
+  } catch (const std::exception& e) {
+    result->status = DSG_LOGIC;
+    fill_msg(result->message, e.what());
+  }
+  return result->status;
+}
+
+void dsg_result_free(dsg_result* r) {
+  if (!r) return;
+  std::free(r->blocks);
+  std::free(r->members);
+  std::free(r->ideal_bits);
+  std::free(r->dp_values);
+  r->blocks = nullptr;
+  r->members = nullptr;
+  r->ideal_bits = nullptr;
+  r->dp_values = nullptr;
+}
+
+int dsg_enumerate_ideals(const dsg_graph* graph, const uint8_t* within, int64_t budget,
+                         const dsg_options* options, dsg_ideals* out) {
+  std::memset(out, 0, sizeof *out);
+  const auto t0 = Clock::now();
+  try {
+    dsg_options defaults;
+    dsg_default_options(&defaults);
+    const dsg_options* opt = options ? options : &defaults;
+    Prepared P = prepare(DSG_MODE_INFERENCE, graph, nullptr, within, true, opt->flags);
+    DeviceCtx& ctx = context(opt->device);
+    std::lock_guard<std::mutex> lk(ctx.mu);
+    CK(cudaSetDevice(ctx.device));
+    DeviceGraph dg = upload_graph(ctx, P);
+    Lattice lat = enumerate_device(ctx, P, dg, budget, (opt->flags & DSG_FLAG_HASH_ENUM) != 0);
+    out->count = lat.I;
+    out->words = P.W;
+    out->bits = (uint64_t*)std::malloc(sizeof(uint64_t) * (size_t)lat.I * P.W + 8);
+    CK(cudaMemcpy(out->bits, lat.sbits, sizeof(uint64_t) * (size_t)lat.I * P.W,
+                  cudaMemcpyDeviceToHost));
+    out->n_levels = lat.n_levels;
+    out->level_offsets = (int64_t*)std::malloc(sizeof(int64_t) * (lat.n_levels + 1));
+    std::memcpy(out->level_offsets, lat.level_off.data(), sizeof(int64_t) * (lat.n_levels + 1));
+    out->status = DSG_OK;
+  } catch (const Fail& f) {
+    out->status = f.status;
+    out->budget_limit = f.limit;
+    fill_msg(out->message, f.msg);
+  } catch (const std::exception& e) {
+    out->status = DSG_LOGIC;
+    fill_msg(out->message, e.what());
+  }
+  out->t_ms = ms_since(t0);
+  return out->status;
+}
+
+void dsg_ideals_free(dsg_ideals* out) {
+  if (!out) return;
+  std::free(out->bits);
+  std::free(out->level_offsets);
+  out->bits = nullptr;
+  out->level_offsets = nullptr;
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+// dsg_internal.h — host-side launch interfaces between the C-ABI driver
+// (capi.cu) and the kernel translation units.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dsg_device.cuh"
+
+namespace dsg {
+
+void count_launch();  // kernels launched by this library (bench evidence)
+
+// ---------------------------------------------------------------- K1
+struct EnumStatus {
+  int32_t code;      // 0 ok, 1 budget exceeded, 2 capacity, 3 candidate capacity
+  int32_t n_levels;
+  int64_t total;
+  int64_t needed;
+};
+
+struct EnumLaunch {
+  int W, n;
+  const uint64_t* pred_u;
+  const uint64_t* succ_u;
+  const uint8_t* in_universe;
+  uint64_t* bits;
+  uint64_t* maxm;
+  uint64_t* addm;
+  int32_t* level_of;
+  int64_t cap, budget;
+  int64_t* level_off;
+  EnumStatus* status;
+  int hash_mode;
+  uint64_t* cand_bits;
+  uint64_t* cand_maxm;
+  uint64_t* cand_addm;
+  int64_t cand_cap;
+  int64_t* table;
+  int64_t table_cap;
+};
+
+void launch_enumerate(const EnumLaunch& L, cudaStream_t st);
+void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const int32_t* level_of,
+                     const int64_t* level_off, uint64_t* out_bits, cudaStream_t st);
+
+// ------------------------------------------------------- descriptors
+// Per-ideal table sizes (pass 1) -> exclusive offsets (scan) -> fill (pass 2).
+enum CountSlot { kCntChunks = 0, kCntF, kCntN, kCntP, kCntL, kCntLItems, kNumCounts };
+
+struct DescribeLaunch {
+  DevGraph g;
+  int training;
+  int has_bw;        // graph has backward nodes (bw_reach exists)
+  int value_bits;    // 32 or 64
+  int64_t I;
+  const uint64_t* sbits;  // sorted ideal bitsets [I][W]
+  // outputs
+  uint64_t* abits;   // [I][W]
+  uint64_t* intbits; // [I][W] training
+  void* pfx_cpu;     // V[I]
+  void* pfx_acc;
+  void* pfx_mem;
+  int32_t* unsup;
+  void* fw;          // V[I]
+  int32_t* fwinf;
+  uint8_t* upset;    // training: Φ(J) is an up-set of the backward part
+  int64_t* counts;   // [kNumCounts][I + 1]  (pass 1 output, scanned in place)
+  // pools (pass 2)
+  FChunk* chunks;
+  void* fpool;       // V
+  NItem* nitems;
+  PItem* pitems;
+  LEntry* lentries;
+  MaskItem* litems;
+};
+
+void launch_describe(const DescribeLaunch& L, bool fill, cudaStream_t st);
+void launch_scan_counts(int64_t* counts, int64_t I, int n_arrays, cudaStream_t st);
+
+// ------------------------------------------------------- transition
+struct LevelLaunch {
+  int value_bits;
+  int training;
+  int has_bw;
+  int fastgate;
+  int K, L, C, W;
+  int64_t mlim;        // fixed point (clamped)
+  int memcheck;
+  int interleave;
+  int64_t t_lo, t_hi;  // targets
+  int64_t s_hi;        // sources [0, s_hi)
+  int64_t n_chunks;
+  int64_t chunk_len;
+  // tables
+  const uint64_t* abits;
+  const uint64_t* intbits;
+  const void* pfx_cpu;
+  const void* pfx_acc;
+  const void* pfx_mem;
+  const int32_t* unsup;
+  const void* fw;
+  const int32_t* fwinf;
+  const uint8_t* upset;
+  const int64_t* chunk_off;   // counts[kCntChunks] scanned, [I+1]
+  const FChunk* chunks;
+  const void* fpool;
+  const NItem* nitems;
+  const int64_t* p_off;
+  const PItem* pitems;
+  const int64_t* l_off;
+  const LEntry* lentries;
+  const MaskItem* litems;
+  const uint64_t* bwset;
+  const uint64_t* bw_from;
+  const uint64_t* bw_to;
+  int n_nodes;
+  // dp
+  void* dp;                   // V[I][C]
+  int32_t* bp;                // [I][C]
+  void* part_val;             // V[n_chunks][C][T]
+  int32_t* part_arg;
+  unsigned long long* pair_counter;
+};
+
+void launch_transition(const LevelLaunch& L, cudaStream_t st);
+void launch_finalize(const LevelLaunch& L, cudaStream_t st);
+void launch_init_empty(int value_bits, int K, int L, void* dp, int32_t* bp, cudaStream_t st);
+
+struct TracebackOut {
+  int32_t status;   // 0 ok, 1 infeasible, 2 stuck
+  int32_t best_k, best_l;
+  int32_t n_blocks;
+  int64_t best_value;
+};
+
+// ords/prevs/cpus/block_bits hold up to K+L entries (one per block).
+void launch_traceback(int value_bits, int64_t I, int K, int L, int W, const void* dp,
+                      const int32_t* bp, const uint64_t* abits, TracebackOut* out,
+                      int64_t* ords, int64_t* prevs, int32_t* cpus, uint64_t* block_bits,
+                      cudaStream_t st);
+
+}  // namespace dsg

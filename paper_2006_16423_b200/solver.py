@@ -1,0 +1,189 @@
+"""The reference's solver API (include/dagsplit/dp_solver.hpp:21-37,
+graph.hpp:253-258) backed by the sm_100a kernels in libdsg_b200.so.
+
+There is no CPU fallback: if the CUDA library is missing or no B200 is
+visible, every call raises DeviceError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Iterable, List, Optional
+
+import numpy as np
+
+from . import _abi
+from .errors import DeviceError, raise_for_status
+from .graph import DeviceConfig, Graph, SplitBlock, make_canonical_split
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdsg_b200.so")
+_lib: Optional[C.CDLL] = None
+
+
+def load_library() -> C.CDLL:
+    """Load the in-tree CUDA library (fails loudly when it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
+    lib = C.CDLL(LIB_PATH)
+    _abi.bind(lib, "dsg")
+    lib.dsg_device_count.restype = C.c_int
+    lib.dsg_version.restype = C.c_char_p
+    lib.dsg_kernel_launch_count.restype = C.c_int64
+    lib.dsg_default_options.argtypes = [C.POINTER(_abi.dsg_options)]
+    _lib = lib
+    return lib
+
+
+def kernel_launch_count() -> int:
+    return int(load_library().dsg_kernel_launch_count())
+
+
+@dataclass
+class SolveOptions:
+    """dp_solver.hpp:11-14 plus device knobs."""
+    deadline_seconds: Optional[float] = None
+    ideal_budget: int = _abi.DSG_DEFAULT_IDEAL_BUDGET
+    device: int = -1
+    flags: int = 0
+    shard_count: int = 0
+
+
+@dataclass
+class RawResult:
+    objective: object
+    blocks: List[SplitBlock]
+    best_k: int
+    best_l: int
+    n_ideals: int
+    n_pairs: int
+    n_levels: int
+    value_bits: int
+    denominator: int
+    stats: dict = field(default_factory=dict)
+    ideal_bits: Optional[np.ndarray] = None
+    dp_values: Optional[np.ndarray] = None
+
+
+def run_dp(lib: C.CDLL, prefix: str, mode: int, g: Graph, config: DeviceConfig,
+           opt: Optional[SolveOptions] = None) -> RawResult:
+    """Call <prefix>_dp_solve on the POD form of (g, config); raise on error.
+
+    Shared by the product path (prefix "dsg") and, in tests only, the oracle
+    libraries (prefixes "dsgo", "dsgref")."""
+    opt = opt or SolveOptions()
+    pg = _abi.pod_graph(g)
+    cfg = _abi.pod_config(config)
+    po = _abi.pod_options(opt.ideal_budget, opt.deadline_seconds, opt.device, opt.shard_count,
+                          opt.flags)
+    res = _abi.dsg_result()
+    getattr(lib, f"{prefix}_dp_solve")(mode, C.byref(pg.struct), C.byref(cfg), C.byref(po),
+                                       C.byref(res))
+    try:
+        raise_for_status(res.status, res.message, res.budget_limit)
+        blocks = []
+        for b in range(res.n_blocks):
+            blk = res.blocks[b]
+            members = [res.members[blk.offset + i] for i in range(blk.n_members)]
+            blocks.append(SplitBlock(cpu=bool(blk.cpu), members=members, repl=blk.repl))
+        stats = {k: getattr(res, k) for k in (
+            "t_prepare_ms", "t_enumerate_ms", "t_describe_ms", "t_dp_ms", "t_traceback_ms",
+            "t_total_ms", "t_transition_kernel_ms", "kernel_launches")}
+        out = RawResult(_abi.from_dsg_rat(res.objective), blocks, res.best_k, res.best_l,
+                        res.n_ideals, res.n_pairs, res.n_levels, res.value_bits, res.denominator,
+                        stats)
+        if res.ideal_bits:
+            n = res.n_ideals * res.words
+            out.ideal_bits = np.ctypeslib.as_array(res.ideal_bits, shape=(n,)).copy().reshape(
+                res.n_ideals, res.words)
+        if res.dp_values:
+            cells = (config.accelerators + 1) * (config.cpus + 1)
+            out.dp_values = np.ctypeslib.as_array(res.dp_values, shape=(res.n_ideals * cells,)).copy(
+            ).reshape(res.n_ideals, cells)
+        return out
+    finally:
+        getattr(lib, f"{prefix}_result_free")(C.byref(res))
+
+
+def _solve(mode: int, g: Graph, config: DeviceConfig, opt: Optional[SolveOptions]):
+    raw = run_dp(load_library(), "dsg", mode, g, config, opt)
+    split = make_canonical_split(g, config, raw.blocks, raw.objective)
+    split.stats = dict(raw.stats, n_ideals=raw.n_ideals, n_pairs=raw.n_pairs,
+                       n_levels=raw.n_levels, value_bits=raw.value_bits,
+                       best_k=raw.best_k, best_l=raw.best_l)
+    return split
+
+
+def solve_maxload_inference(g: Graph, config: DeviceConfig, opt: Optional[SolveOptions] = None):
+    """dp_solver.hpp:21-22 on the B200."""
+    return _solve(_abi.DSG_MODE_INFERENCE, g, config, opt)
+
+
+def solve_maxload_training(g: Graph, config: DeviceConfig, opt: Optional[SolveOptions] = None):
+    """dp_solver.hpp:28-29 on the B200."""
+    return _solve(_abi.DSG_MODE_TRAINING, g, config, opt)
+
+
+def solve_maxload_replicated(g: Graph, config: DeviceConfig, opt: Optional[SolveOptions] = None):
+    """dp_solver.hpp:36-37 on the B200."""
+    return _solve(_abi.DSG_MODE_REPLICATED, g, config, opt)
+
+
+@dataclass
+class IdealIndex:
+    """graph.hpp:243-249: ideals in size-major, lexicographic order."""
+    bits: np.ndarray          # [count, words] uint64
+    level_offsets: np.ndarray
+    universe: int
+
+    def count(self) -> int:
+        return int(self.bits.shape[0])
+
+    def ideal(self, ordinal: int) -> frozenset:
+        row = self.bits[ordinal]
+        return frozenset(w * 64 + b for w in range(row.shape[0]) for b in range(64)
+                         if (int(row[w]) >> b) & 1)
+
+    @property
+    def ideals(self) -> List[frozenset]:
+        return [self.ideal(i) for i in range(self.count())]
+
+
+def run_enumerate(lib: C.CDLL, prefix: str, g: Graph, within: Optional[Iterable[int]],
+                  budget: int, flags: int = 0, device: int = -1) -> IdealIndex:
+    pg = _abi.pod_graph(g)
+    w_arr = None
+    w_ptr = None
+    if within is not None:
+        w_arr = np.zeros(max(g.size(), 1), dtype=np.uint8)
+        for v in within:
+            w_arr[v] = 1
+        w_ptr = w_arr.ctypes.data_as(C.POINTER(C.c_uint8))
+    po = _abi.pod_options(budget, None, device, 0, flags)
+    out = _abi.dsg_ideals()
+    getattr(lib, f"{prefix}_enumerate_ideals")(C.byref(pg.struct), w_ptr, int(budget), C.byref(po),
+                                               C.byref(out))
+    try:
+        raise_for_status(out.status, out.message, out.budget_limit)
+        words = out.words
+        bits = np.ctypeslib.as_array(out.bits, shape=(out.count * words,)).copy().reshape(
+            out.count, words) if out.count else np.zeros((0, words), np.uint64)
+        offs = np.ctypeslib.as_array(out.level_offsets, shape=(out.n_levels + 1,)).copy()
+        return IdealIndex(bits, offs, g.size())
+    finally:
+        getattr(lib, f"{prefix}_ideals_free")(C.byref(out))
+
+
+def enumerate_ideals(g: Graph, budget: int = _abi.DSG_DEFAULT_IDEAL_BUDGET, flags: int = 0):
+    """graph.hpp:253 on the B200."""
+    return run_enumerate(load_library(), "dsg", g, None, budget, flags)
+
+
+def enumerate_ideals_within(g: Graph, within: Iterable[int],
+                            budget: int = _abi.DSG_DEFAULT_IDEAL_BUDGET, flags: int = 0):
+    """graph.hpp:256-258 on the B200."""
+    return run_enumerate(load_library(), "dsg", g, within, budget, flags)
