@@ -1,0 +1,334 @@
+#!/usr/bin/env python3
+"""Benchmark: max-load DP over ideals on B200 vs the reference CPU solver.
+
+Metric (BASELINE.json): "DP transitions/sec & time-to-optimal-partition at
+1/2/4/8 B200 vs CPU ref".  A transition is one nested ideal pair I' < I
+evaluated for all (K+1)(L+1) cells — the reference's apply_candidate count
+(dp_solver.cpp:197-233).  One step = one complete solve of the workload:
+lattice enumeration -> descriptors -> every DP level -> traceback.
+
+  value  device-resident: the graph is already in HBM (dsg_session_run); the
+         whole device pipeline is timed with CUDA events on the library's own
+         stream; L2 is flushed (256 MiB write) between steps.
+  e2e    through the reference-facing C-ABI call dsg_dp_solve with host
+         buffers: flatten + fixed point + H2D + all kernels + D2H of the split.
+
+Default workload (N=1): the InceptionV3-like stand-in C2 (configs[1];
+326 nodes, 36,596 ideals, 563,731,351 transitions, K=8, L=0), synthetic
+weights.  `--impl reference` times the unmodified reference
+(oracle/_ref/libdsg_ref.so) on the host cores on a bounded prefix sample of
+the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2006_16423_b200 import _abi, solver  # noqa: E402
+from paper_2006_16423_b200 import workloads as wl  # noqa: E402
+
+METRIC = "DP transitions/sec & time-to-optimal-partition at 1/2/4/8 B200 vs CPU ref"
+UNIT = "transitions/s"
+# bounded CPU sample: the C2 stand-in truncated after its first 4 modules
+# (stem + A x3 + B: 90 nodes, 2,614 ideals, 2,631,141 transitions)
+SAMPLE_MODULES = 4
+
+
+def algorithmic_bytes_per_transition(C: int, W: int, training: bool, W_fw: int = 0) -> int:
+    """compulsory source-side bytes of an untiled transition."""
+    if training:
+        return 8 * C + 8 * W_fw + 16 * W + 32
+    return 8 * C + 8 * W + 32
+
+
+def workload(name: str) -> wl.Workload:
+    if name.startswith("C5"):
+        pt = tuple(int(x) for x in name[3:].split(","))
+        return wl.sweep(*pt)
+    return wl.standin(name)
+
+
+def sample_workload(name: str):
+    w = workload(name)
+    spec = wl.ChainSpec(w.spec.stem, w.spec.modules[:SAMPLE_MODULES], 0)
+    g = wl.module_chain(spec)
+    if w.training:
+        g = wl.mirror_training(g)
+    cfg = wl.DeviceConfig(w.config.accelerators, w.config.cpus, wl._mem_limit(g, w.config.accelerators))
+    return g, cfg, spec, w.training
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    return world, rank, local
+
+
+def barrier_sync(world):
+    import torch
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(world, x: float) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def flush_l2(buf):
+    buf.fill_(1)  # 256 MiB > 126 MB L2
+
+
+def cpu_reference_rate(name: str, min_seconds: float, max_runs: int = 64):
+    """The unmodified reference (oracle/_ref) on the bounded sample, 1 thread
+    (the reference solver is single-threaded by contract)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_bind as ob  # checker / baseline only
+    g, cfg, spec, training = sample_workload(name)
+    _, _, pairs = wl.chain_counts(spec)
+    kind = "reference" if ob.available("ref") else "port"
+    mode = 1 if training else 0
+    runs, total = 0, 0.0
+    while runs < max_runs and (total < min_seconds or runs == 0):
+        t = time.perf_counter()
+        ob.dp("ref" if kind == "reference" else "port", mode, g, cfg)
+        total += time.perf_counter() - t
+        runs += 1
+    return pairs * runs / total, kind, runs, total, pairs, g.size()
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_bind as ob
+    w = workload(args.workload)
+    g, cfg, spec, training = sample_workload(args.workload)
+    _, ideals, pairs = wl.chain_counts(spec)
+    kind = "reference" if ob.available("ref") else "port"
+    mode = 1 if training else 0
+    lib = "ref" if kind == "reference" else "port"
+    for _ in range(args.warmup):
+        ob.dp(lib, mode, g, cfg)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        ob.dp(lib, mode, g, cfg)
+        times.append(time.perf_counter() - t)
+    total = sum(times)
+    value = pairs * args.steps / total
+    sample = (f"{w.name} stand-in truncated to its first {SAMPLE_MODULES} modules: {g.size()} nodes, "
+              f"{ideals} ideals, {pairs} transitions per step, K={cfg.accelerators}, L={cfg.cpus}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "rational(int64 num/den)",
+        "data": "synthetic", "config": {"workload": w.name, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    w = workload(args.workload)
+    mode = 1 if w.training else 0
+    nv, n_ideals, pairs_cf = w.counts
+    flags = _abi.DSG_FLAG_TIME_KERNELS
+    opt = solver.SolveOptions(flags=flags, device=local)
+    sess = solver.Session(mode, w.graph, w.config, opt)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    for _ in range(args.warmup):
+        sess.run()
+    launches0 = solver.kernel_launch_count()
+    step_ms, kern_ms, results = [], [], []
+    sampler = ClockSampler(local)
+    barrier_sync(world)
+    t_wall = time.perf_counter()
+    with sampler:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            r = sess.run()
+            step_ms.append(r.stats["t_device_ms"])
+            kern_ms.append(r.stats["t_transition_kernel_ms"])
+            results.append(r)
+    barrier_sync(world)
+    wall = time.perf_counter() - t_wall
+    launches = solver.kernel_launch_count() - launches0
+    r0 = results[0]
+    for r in results:
+        assert r.objective == r0.objective and r.n_pairs == r0.n_pairs
+    assert r0.n_ideals == n_ideals and r0.n_pairs == pairs_cf, (r0.n_ideals, r0.n_pairs)
+    dev_ms = max_over_ranks(world, sum(step_ms)) / args.steps
+    value = world * r0.n_pairs / (dev_ms / 1e3)
+
+    # e2e: the reference-facing C-ABI call with host buffers
+    from paper_2006_16423_b200.graph import make_canonical_split
+    e2e_ms, h2d, d2h = [], [], []
+    lib = solver.load_library()
+    solver.run_dp(lib, "dsg", mode, w.graph, w.config, solver.SolveOptions(device=local))
+    for i in range(max(1, args.steps)):
+        w.graph._pod_cache = None  # re-flatten the host Graph every step
+        t = time.perf_counter()
+        raw = solver.run_dp(lib, "dsg", mode, w.graph, w.config, solver.SolveOptions(device=local))
+        split = make_canonical_split(w.graph, w.config, raw.blocks, raw.objective)
+        e2e_ms.append(1e3 * (time.perf_counter() - t))
+        h2d.append(raw.stats["h2d_bytes"])
+        d2h.append(raw.stats["d2h_bytes"])
+        assert split.objective_value == r0.objective
+    e2e_step = max_over_ranks(world, statistics.mean(e2e_ms))
+    e2e_value = world * r0.n_pairs / (e2e_step / 1e3)
+
+    # roofline of the dominant kernel (fused transition)
+    W = (w.graph.size() + 63) // 64
+    C = (w.config.accelerators + 1) * (w.config.cpus + 1)
+    W_fw = (w.graph.size() // 2 + 63) // 64 if w.training else W
+    bpt = algorithmic_bytes_per_transition(C, W, w.training, W_fw)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    kern_avg_ms = statistics.mean(kern_ms)
+    achieved = r0.n_pairs * bpt / (kern_avg_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.workload)
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "int32" if r0.value_bits == 32 else "int64",
+        "data": "synthetic (seeded stand-in graph, SplitMix64 weights; SURVEY §8(d))",
+        "config": {"workload": w.name, "description": w.description, "nodes": w.graph.size(),
+                   "ideals": r0.n_ideals, "transitions": r0.n_pairs, "levels": r0.n_levels,
+                   "k": w.config.accelerators, "l": w.config.cpus, "cells": C,
+                   "fixed_point_denominator": r0.denominator, "l2": "flushed (256 MiB write) between steps",
+                   "parallelism": f"replica x{world}" if world > 1 else "single GPU",
+                   "objective": str(r0.objective)},
+        "time_to_optimal_partition_ms": {"device_resident": dev_ms, "e2e": e2e_step},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(statistics.mean(h2d)),
+                "d2h_bytes_per_step": int(statistics.mean(d2h)),
+                "ms_per_step": e2e_step, "call": "dsg_dp_solve (C-ABI, host buffers) + canonical split"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "transition_kernel (fused K2+K3+K4)",
+                     "bytes_per_transition": bpt,
+                     "kernel_ms_per_step": kern_avg_ms,
+                     "kernel_share_of_step": kern_avg_ms / dev_ms},
+        "wall_s": wall,
+    }
+    line["clocks"] = sampler.summary()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, kind, runs, secs, pairs, nodes = cpu_reference_rate(args.workload, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": (f"{w.name} truncated to its first {SAMPLE_MODULES} modules ({nodes} nodes, "
+                       f"{pairs} transitions), {runs} solves in {secs:.1f} s on 1 host core"),
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    sess.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -163,6 +163,10 @@ typedef struct dsg_result {
   double t_traceback_ms;  /* traceback + D2H */
   double t_total_ms;
   double t_transition_kernel_ms; /* sum of transition-kernel event times */
+  double t_device_ms;     /* CUDA-event time of the device pipeline (first
+                             enumeration launch .. last result copy) */
+  int64_t h2d_bytes;      /* host->device bytes copied by this call */
+  int64_t d2h_bytes;      /* device->host bytes copied by this call */
   /* DSG_FLAG_KEEP_TABLES: */
   int32_t words;            /* 64-bit words per ideal bitset */
   uint64_t* ideal_bits;     /* n_ideals * words, reference ordinal order */
@@ -192,6 +196,16 @@ int dsg_enumerate_ideals(const dsg_graph* graph, const uint8_t* within,
                          int64_t budget, const dsg_options* options,
                          dsg_ideals* out);
 void dsg_ideals_free(dsg_ideals* out);
+
+/* Resident session: flatten + fixed point + upload once, then run the device
+ * pipeline any number of times with the graph already in HBM (the same
+ * computation as dsg_dp_solve minus the host preparation and input copies).
+ * status_out->status reports creation errors; NULL on failure. */
+typedef struct dsg_session dsg_session;
+dsg_session* dsg_session_create(int32_t mode, const dsg_graph* graph, const dsg_config* config,
+                                const dsg_options* options, dsg_result* status_out);
+int dsg_session_run(dsg_session* session, dsg_result* result);
+void dsg_session_destroy(dsg_session* session);
 
 void dsg_default_options(dsg_options* options);
 const char* dsg_version(void);

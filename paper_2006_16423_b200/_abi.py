@@ -110,6 +110,9 @@ class dsg_result(C.Structure):
         ("t_traceback_ms", C.c_double),
         ("t_total_ms", C.c_double),
         ("t_transition_kernel_ms", C.c_double),
+        ("t_device_ms", C.c_double),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
         ("words", C.c_int32),
         ("ideal_bits", C.POINTER(C.c_uint64)),
         ("dp_values", C.POINTER(C.c_int64)),

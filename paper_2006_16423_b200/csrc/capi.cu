@@ -30,6 +30,14 @@
 
 #define DSG_TIME_KERNELS_FLAG DSG_FLAG_TIME_KERNELS
 
+// device->host copy on the solve's stream, counted for the e2e record
+#define D2H_3(dst, src, bytes)                                                           \
+  do {                                                                                   \
+    ctx.d2h_bytes += (int64_t)(bytes);                                                   \
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx.stream));            \
+  } while (0)
+#define D2H(...) D2H_3(__VA_ARGS__)
+
 namespace dsg {
 
 static std::atomic<int64_t> g_launches{0};
@@ -72,6 +80,7 @@ struct DeviceCtx {
   std::map<std::string, std::pair<void*, size_t>> bufs;
   void* pinned = nullptr;
   size_t pinned_cap = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;  // per solve, for the bench's e2e record
 
   void* get(const std::string& name, size_t bytes) {
     if (bytes == 0) bytes = 8;
@@ -84,6 +93,16 @@ struct DeviceCtx {
       b.second = cap;
     }
     return b.first;
+  }
+  void release_prefix(const std::string& prefix) {
+    for (auto it = bufs.begin(); it != bufs.end();) {
+      if (it->first.compare(0, prefix.size(), prefix) == 0) {
+        if (it->second.first) cudaFree(it->second.first);
+        it = bufs.erase(it);
+      } else {
+        ++it;
+      }
+    }
   }
   template <typename T>
   T* get_t(const std::string& name, size_t count) {
@@ -433,7 +452,10 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
 template <typename T>
 T* upload(DeviceCtx& ctx, const std::string& name, const std::vector<T>& v) {
   T* d = ctx.get_t<T>(name, std::max<size_t>(v.size(), 1));
-  if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx.stream));
+  if (!v.empty()) {
+    CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx.stream));
+    ctx.h2d_bytes += (int64_t)(v.size() * sizeof(T));
+  }
   return d;
 }
 
@@ -442,31 +464,31 @@ struct DeviceGraph {
   uint8_t* in_universe;
 };
 
-DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P) {
+DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P, const std::string& prefix) {
   DeviceGraph d;
   DevGraph& g = d.g;
   g.n = P.n;
   g.W = P.W;
-  g.cpu = upload(ctx, "g.cpu", P.cpu);
-  g.acc = upload(ctx, "g.acc", P.acc);
-  g.comm = upload(ctx, "g.comm", P.comm);
-  g.mem = upload(ctx, "g.mem", P.mem);
-  g.unsup = upload(ctx, "g.unsup", P.unsup);
-  g.comminf = upload(ctx, "g.comminf", P.comminf);
-  g.succ_real = upload(ctx, "g.succ_real", P.succ_real);
-  g.pred_real = upload(ctx, "g.pred_real", P.pred_real);
-  g.pred_u = upload(ctx, "g.pred_u", P.pred_u);
-  g.succ_u = upload(ctx, "g.succ_u", P.succ_u);
-  g.twins = upload(ctx, "g.twins", P.twins);
-  g.bw_succ = upload(ctx, "g.bw_succ", P.bw_succ);
-  g.bw_from = upload(ctx, "g.bw_from", P.bw_from);
-  g.bw_to = upload(ctx, "g.bw_to", P.bw_to);
-  g.bwset = upload(ctx, "g.bwset", P.bwset);
-  g.out_real_off = upload(ctx, "g.out_off", P.out_off);
-  g.out_real_adj = upload(ctx, "g.out_adj", P.out_adj);
-  g.in_real_off = upload(ctx, "g.in_off", P.in_off);
-  g.in_real_adj = upload(ctx, "g.in_adj", P.in_adj);
-  d.in_universe = upload(ctx, "g.in_universe", P.in_universe);
+  g.cpu = upload(ctx, prefix + "cpu", P.cpu);
+  g.acc = upload(ctx, prefix + "acc", P.acc);
+  g.comm = upload(ctx, prefix + "comm", P.comm);
+  g.mem = upload(ctx, prefix + "mem", P.mem);
+  g.unsup = upload(ctx, prefix + "unsup", P.unsup);
+  g.comminf = upload(ctx, prefix + "comminf", P.comminf);
+  g.succ_real = upload(ctx, prefix + "succ_real", P.succ_real);
+  g.pred_real = upload(ctx, prefix + "pred_real", P.pred_real);
+  g.pred_u = upload(ctx, prefix + "pred_u", P.pred_u);
+  g.succ_u = upload(ctx, prefix + "succ_u", P.succ_u);
+  g.twins = upload(ctx, prefix + "twins", P.twins);
+  g.bw_succ = upload(ctx, prefix + "bw_succ", P.bw_succ);
+  g.bw_from = upload(ctx, prefix + "bw_from", P.bw_from);
+  g.bw_to = upload(ctx, prefix + "bw_to", P.bw_to);
+  g.bwset = upload(ctx, prefix + "bwset", P.bwset);
+  g.out_real_off = upload(ctx, prefix + "out_off", P.out_off);
+  g.out_real_adj = upload(ctx, prefix + "out_adj", P.out_adj);
+  g.in_real_off = upload(ctx, prefix + "in_off", P.in_off);
+  g.in_real_adj = upload(ctx, prefix + "in_adj", P.in_adj);
+  d.in_universe = upload(ctx, prefix + "in_universe", P.in_universe);
   return d;
 }
 
@@ -516,7 +538,7 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
     launch_enumerate(L, ctx.stream);
     CK(cudaGetLastError());
     EnumStatus st;
-    CK(cudaMemcpyAsync(&st, st_d, sizeof st, cudaMemcpyDeviceToHost, ctx.stream));
+    D2H(&st, st_d, sizeof st);
     CK(cudaStreamSynchronize(ctx.stream));
     if (st.code == 1) throw Fail{DSG_BUDGET, "ideal budget exceeded", budget};
     if (st.code == 2) {
@@ -532,8 +554,7 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
     lat.I = st.total;
     lat.n_levels = st.n_levels;
     lat.level_off.resize(lat.n_levels + 1);
-    CK(cudaMemcpyAsync(lat.level_off.data(), lvl_d, sizeof(int64_t) * (lat.n_levels + 1),
-                       cudaMemcpyDeviceToHost, ctx.stream));
+    D2H(lat.level_off.data(), lvl_d, sizeof(int64_t) * (lat.n_levels + 1));
     lat.sbits = ctx.get_t<uint64_t>("lat.sbits", (size_t)lat.I * W);
     launch_lex_rank(W, lat.I, L.bits, L.level_of, lvl_d, lat.sbits, ctx.stream);
     CK(cudaGetLastError());
@@ -549,17 +570,12 @@ void fill_msg(char* dst, const std::string& s) {
 }
 
 // ------------------------------------------------------------ solve
-void solve(int mode, const dsg_graph* graph, const dsg_config* config, const dsg_options* opt,
-           dsg_result* res) {
-  const auto t0 = Clock::now();
-  dsg_options defaults;
-  dsg_default_options(&defaults);
-  if (!opt) opt = &defaults;
+// The device pipeline for an uploaded graph: enumeration -> descriptors ->
+// level loop -> traceback.  Only control-sized values cross PCIe (status,
+// level offsets, table totals, the result blocks).
+void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_options* opt,
+                dsg_result* res, Clock::time_point t0) {
   const int flags = opt->flags;
-  Prepared P = prepare(mode, graph, config, nullptr, false, flags);
-  DeviceCtx& ctx = context(opt->device);
-  std::lock_guard<std::mutex> lk(ctx.mu);
-  CK(cudaSetDevice(ctx.device));
   cudaStream_t st = ctx.stream;
   const bool timing = (flags & DSG_TIME_KERNELS_FLAG) != 0;
   const bool has_deadline = opt->deadline_seconds > 0;
@@ -567,9 +583,12 @@ void solve(int mode, const dsg_graph* graph, const dsg_config* config, const dsg
   const int W = P.W, K = P.K, Lc = P.L, C = P.C;
   const int vb = P.value_bits;
   const size_t vsz = vb == 32 ? 4 : 8;
-
-  DeviceGraph dg = upload_graph(ctx, P);
-  res->t_prepare_ms = ms_since(t0);
+  const int64_t launches0 = dsg::g_launches.load();
+  ctx.d2h_bytes = 0;
+  cudaEvent_t ev_start, ev_end;
+  CK(cudaEventCreate(&ev_start));
+  CK(cudaEventCreate(&ev_end));
+  CK(cudaEventRecord(ev_start, st));
   const auto t1 = Clock::now();
   Lattice lat = enumerate_device(ctx, P, dg, opt->ideal_budget, (flags & DSG_FLAG_HASH_ENUM) != 0);
   res->n_ideals = lat.I;
@@ -602,8 +621,7 @@ void solve(int mode, const dsg_graph* graph, const dsg_config* config, const dsg
   launch_scan_counts(D.counts, I, kNumCounts, st);
   int64_t totals[kNumCounts];
   for (int k = 0; k < kNumCounts; ++k)
-    CK(cudaMemcpyAsync(&totals[k], D.counts + (size_t)k * (I + 1) + I, sizeof(int64_t),
-                       cudaMemcpyDeviceToHost, st));
+    D2H(&totals[k], D.counts + (size_t)k * (I + 1) + I, sizeof(int64_t));
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
   if (totals[kCntF] > INT32_MAX || totals[kCntN] > INT32_MAX || totals[kCntLItems] > INT32_MAX)
@@ -745,25 +763,32 @@ void solve(int mode, const dsg_graph* graph, const dsg_config* config, const dsg
   unsigned long long pairs = 0;
   std::vector<int32_t> cpus(maxb);
   std::vector<uint64_t> bbits((size_t)maxb * W);
-  CK(cudaMemcpyAsync(&tb, tb_d, sizeof tb, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&pairs, pairs_d, sizeof pairs, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(cpus.data(), cpus_d, sizeof(int32_t) * maxb, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(bbits.data(), bb_d, sizeof(uint64_t) * maxb * W, cudaMemcpyDeviceToHost, st));
+  D2H(&tb, tb_d, sizeof tb);
+  D2H(&pairs, pairs_d, sizeof pairs);
+  D2H(cpus.data(), cpus_d, sizeof(int32_t) * maxb);
+  D2H(bbits.data(), bb_d, sizeof(uint64_t) * maxb * W);
   if (flags & DSG_FLAG_KEEP_TABLES) {
     res->words = W;
     res->ideal_bits = (uint64_t*)std::malloc(sizeof(uint64_t) * (size_t)I * W + 8);
-    CK(cudaMemcpyAsync(res->ideal_bits, lat.sbits, sizeof(uint64_t) * (size_t)I * W,
-                       cudaMemcpyDeviceToHost, st));
+    D2H(res->ideal_bits, lat.sbits, sizeof(uint64_t) * (size_t)I * W);
     res->dp_values = (int64_t*)std::malloc(sizeof(int64_t) * (size_t)I * C + 8);
     if (vb == 64) {
-      CK(cudaMemcpyAsync(res->dp_values, dp, sizeof(int64_t) * (size_t)I * C,
-                         cudaMemcpyDeviceToHost, st));
+      D2H(res->dp_values, dp, sizeof(int64_t) * (size_t)I * C);
     }
   }
+  CK(cudaEventRecord(ev_end, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
+  {
+    float dev_ms = 0;
+    cudaEventElapsedTime(&dev_ms, ev_start, ev_end);
+    res->t_device_ms = dev_ms;
+    cudaEventDestroy(ev_start);
+    cudaEventDestroy(ev_end);
+  }
   if ((flags & DSG_FLAG_KEEP_TABLES) && vb == 32) {
     std::vector<int32_t> tmp((size_t)I * C);
+    ctx.d2h_bytes += (int64_t)(sizeof(int32_t) * tmp.size());
     CK(cudaMemcpy(tmp.data(), dp, sizeof(int32_t) * tmp.size(), cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < tmp.size(); ++i)
       res->dp_values[i] = tmp[i] == VTraits<int32_t>::INF ? INT64_MAX : (int64_t)tmp[i];
@@ -818,12 +843,102 @@ void solve(int mode, const dsg_graph* graph, const dsg_config* config, const dsg
   }
   res->t_traceback_ms = 0;
   res->t_total_ms = ms_since(t0);
-  res->kernel_launches = dsg::g_launches.load();
+  res->kernel_launches = dsg::g_launches.load() - launches0;
+  res->h2d_bytes = ctx.h2d_bytes;
+  res->d2h_bytes = ctx.d2h_bytes;
+}
+
+void solve(int mode, const dsg_graph* graph, const dsg_config* config, const dsg_options* opt,
+           dsg_result* res) {
+  const auto t0 = Clock::now();
+  dsg_options defaults;
+  dsg_default_options(&defaults);
+  if (!opt) opt = &defaults;
+  Prepared P = prepare(mode, graph, config, nullptr, false, opt->flags);
+  DeviceCtx& ctx = context(opt->device);
+  std::lock_guard<std::mutex> lk(ctx.mu);
+  CK(cudaSetDevice(ctx.device));
+  ctx.h2d_bytes = 0;
+  DeviceGraph dg = upload_graph(ctx, P, "g.");
+  res->t_prepare_ms = ms_since(t0);
+  run_device(ctx, P, dg, opt, res, t0);
 }
 
 }  // namespace
 
+// A prepared solve whose graph stays resident on the device (bench: timing
+// with inputs already in HBM).
+struct dsg_session {
+  Prepared P;
+  DeviceCtx* ctx = nullptr;
+  DeviceGraph dg;
+  dsg_options opt;
+  std::string prefix;
+};
+
+namespace {
+std::atomic<int> g_session_ids{0};
+}  // namespace
+
 extern "C" {
+
+dsg_session* dsg_session_create(int32_t mode, const dsg_graph* graph, const dsg_config* config,
+                                const dsg_options* options, dsg_result* status_out) {
+  std::memset(status_out, 0, sizeof *status_out);
+  dsg_session* s = nullptr;
+  try {
+    auto t0 = Clock::now();
+    std::unique_ptr<dsg_session> sp(new dsg_session());
+    dsg_default_options(&sp->opt);
+    if (options) sp->opt = *options;
+    sp->P = prepare(mode, graph, config, nullptr, false, sp->opt.flags);
+    sp->ctx = &context(sp->opt.device);
+    std::lock_guard<std::mutex> lk(sp->ctx->mu);
+    CK(cudaSetDevice(sp->ctx->device));
+    sp->prefix = "s" + std::to_string(g_session_ids.fetch_add(1)) + ".";
+    sp->dg = upload_graph(*sp->ctx, sp->P, sp->prefix);
+    CK(cudaStreamSynchronize(sp->ctx->stream));
+    status_out->t_prepare_ms = ms_since(t0);
+    s = sp.release();
+    status_out->status = DSG_OK;
+  } catch (const Fail& f) {
+    status_out->status = f.status;
+    fill_msg(status_out->message, f.msg);
+  } catch (const std::exception& e) {
+    status_out->status = DSG_LOGIC;
+    fill_msg(status_out->message, e.what());
+  }
+  return s;
+}
+
+int dsg_session_run(dsg_session* s, dsg_result* result) {
+  std::memset(result, 0, sizeof *result);
+  try {
+    if (!s) throw Fail{DSG_INVALID, "null session"};
+    std::lock_guard<std::mutex> lk(s->ctx->mu);
+    CK(cudaSetDevice(s->ctx->device));
+    s->ctx->h2d_bytes = 0;  // inputs are resident
+    run_device(*s->ctx, s->P, s->dg, &s->opt, result, Clock::now());
+    result->status = DSG_OK;
+  } catch (const Fail& f) {
+    result->status = f.status;
+    result->budget_limit = f.limit;
+    fill_msg(result->message, f.msg);
+  } catch (const std::exception& e) {
+    result->status = DSG_LOGIC;
+    fill_msg(result->message, e.what());
+  }
+  return result->status;
+}
+
+void dsg_session_destroy(dsg_session* s) {
+  if (!s) return;
+  if (s->ctx) {
+    std::lock_guard<std::mutex> lk(s->ctx->mu);
+    s->ctx->release_prefix(s->prefix);
+  }
+  delete s;
+}
 
 void dsg_default_options(dsg_options* o) {
   std::memset(o, 0, sizeof *o);
@@ -888,7 +1003,7 @@ int dsg_enumerate_ideals(const dsg_graph* graph, const uint8_t* within, int64_t 
     DeviceCtx& ctx = context(opt->device);
     std::lock_guard<std::mutex> lk(ctx.mu);
     CK(cudaSetDevice(ctx.device));
-    DeviceGraph dg = upload_graph(ctx, P);
+    DeviceGraph dg = upload_graph(ctx, P, "g.");
     Lattice lat = enumerate_device(ctx, P, dg, budget, (opt->flags & DSG_FLAG_HASH_ENUM) != 0);
     out->count = lat.I;
     out->words = P.W;

@@ -35,6 +35,14 @@ def load_library() -> C.CDLL:
     lib.dsg_version.restype = C.c_char_p
     lib.dsg_kernel_launch_count.restype = C.c_int64
     lib.dsg_default_options.argtypes = [C.POINTER(_abi.dsg_options)]
+    lib.dsg_session_create.restype = C.c_void_p
+    lib.dsg_session_create.argtypes = [C.c_int32, C.POINTER(_abi.dsg_graph),
+                                       C.POINTER(_abi.dsg_config), C.POINTER(_abi.dsg_options),
+                                       C.POINTER(_abi.dsg_result)]
+    lib.dsg_session_run.argtypes = [C.c_void_p, C.POINTER(_abi.dsg_result)]
+    lib.dsg_session_run.restype = C.c_int
+    lib.dsg_session_destroy.argtypes = [C.c_void_p]
+    lib.dsg_session_destroy.restype = None
     _lib = lib
     return lib
 
@@ -69,6 +77,68 @@ class RawResult:
     dp_values: Optional[np.ndarray] = None
 
 
+STAT_FIELDS = ("t_prepare_ms", "t_enumerate_ms", "t_describe_ms", "t_dp_ms", "t_traceback_ms",
+               "t_total_ms", "t_transition_kernel_ms", "t_device_ms", "kernel_launches",
+               "h2d_bytes", "d2h_bytes")
+
+
+def _raw_from(res, config: DeviceConfig) -> RawResult:
+    blocks = []
+    for b in range(res.n_blocks):
+        blk = res.blocks[b]
+        members = [res.members[blk.offset + i] for i in range(blk.n_members)]
+        blocks.append(SplitBlock(cpu=bool(blk.cpu), members=members, repl=blk.repl))
+    stats = {k: getattr(res, k) for k in STAT_FIELDS}
+    return RawResult(_abi.from_dsg_rat(res.objective), blocks, res.best_k, res.best_l,
+                     res.n_ideals, res.n_pairs, res.n_levels, res.value_bits, res.denominator,
+                     stats)
+
+
+class Session:
+    """A solve whose flattened graph stays resident in HBM (dsg_session_*):
+    ``run()`` repeats the whole device pipeline without re-uploading inputs."""
+
+    def __init__(self, mode: int, g: Graph, config: DeviceConfig,
+                 opt: Optional[SolveOptions] = None):
+        lib = load_library()
+        opt = opt or SolveOptions()
+        self._lib = lib
+        self.config = config
+        self._pg = _abi.pod_graph(g)
+        self._cfg = _abi.pod_config(config)
+        self._po = _abi.pod_options(opt.ideal_budget, opt.deadline_seconds, opt.device,
+                                    opt.shard_count, opt.flags)
+        st = _abi.dsg_result()
+        self._h = lib.dsg_session_create(mode, C.byref(self._pg.struct), C.byref(self._cfg),
+                                         C.byref(self._po), C.byref(st))
+        raise_for_status(st.status, st.message, st.budget_limit)
+        self.prepare_ms = st.t_prepare_ms
+
+    def set_flags(self, flags: int) -> None:
+        # options are copied at creation; recreate to change them
+        raise NotImplementedError
+
+    def run(self) -> RawResult:
+        res = _abi.dsg_result()
+        self._lib.dsg_session_run(self._h, C.byref(res))
+        try:
+            raise_for_status(res.status, res.message, res.budget_limit)
+            return _raw_from(res, self.config)
+        finally:
+            self._lib.dsg_result_free(C.byref(res))
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.dsg_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def run_dp(lib: C.CDLL, prefix: str, mode: int, g: Graph, config: DeviceConfig,
            opt: Optional[SolveOptions] = None) -> RawResult:
     """Call <prefix>_dp_solve on the POD form of (g, config); raise on error.
@@ -85,17 +155,7 @@ def run_dp(lib: C.CDLL, prefix: str, mode: int, g: Graph, config: DeviceConfig,
                                        C.byref(res))
     try:
         raise_for_status(res.status, res.message, res.budget_limit)
-        blocks = []
-        for b in range(res.n_blocks):
-            blk = res.blocks[b]
-            members = [res.members[blk.offset + i] for i in range(blk.n_members)]
-            blocks.append(SplitBlock(cpu=bool(blk.cpu), members=members, repl=blk.repl))
-        stats = {k: getattr(res, k) for k in (
-            "t_prepare_ms", "t_enumerate_ms", "t_describe_ms", "t_dp_ms", "t_traceback_ms",
-            "t_total_ms", "t_transition_kernel_ms", "kernel_launches")}
-        out = RawResult(_abi.from_dsg_rat(res.objective), blocks, res.best_k, res.best_l,
-                        res.n_ideals, res.n_pairs, res.n_levels, res.value_bits, res.denominator,
-                        stats)
+        out = _raw_from(res, config)
         if res.ideal_bits:
             n = res.n_ideals * res.words
             out.ideal_bits = np.ctypeslib.as_array(res.ideal_bits, shape=(n,)).copy().reshape(
