@@ -110,7 +110,7 @@ typedef struct dsg_options {
   int32_t device;          /* CUDA ordinal, -1 = current device */
   int32_t shard_count;     /* wavefront shards (virtual on one GPU); 0/1 = off */
   int32_t flags;           /* DSG_FLAG_* */
-  int32_t reserved;
+  int32_t reserved;        /* > 0: cap on persistent-kernel CTAs (testing) */
 } dsg_options;
 
 #define DSG_FLAG_FORCE_INT64 1   /* never use the 32-bit value path */
@@ -118,6 +118,8 @@ typedef struct dsg_options {
 #define DSG_FLAG_HASH_ENUM 4     /* enumerate with the GPU hash set */
 #define DSG_FLAG_KEEP_TABLES 8   /* keep ideal list + dp table for inspection */
 #define DSG_FLAG_TIME_KERNELS 16 /* CUDA-event time every transition launch */
+#define DSG_FLAG_LEVEL_LAUNCH 32 /* one launch pair per level instead of the
+                                    persistent cooperative level kernel */
 
 enum dsg_status {
   DSG_OK = 0,
@@ -167,6 +169,8 @@ typedef struct dsg_result {
                              enumeration launch .. last result copy) */
   int64_t h2d_bytes;      /* host->device bytes copied by this call */
   int64_t d2h_bytes;      /* device->host bytes copied by this call */
+  int32_t persistent_blocks; /* CTAs of the persistent level kernel (0: per-level launches) */
+  int32_t pad_;
   /* DSG_FLAG_KEEP_TABLES: */
   int32_t words;            /* 64-bit words per ideal bitset */
   uint64_t* ideal_bits;     /* n_ideals * words, reference ordinal order */

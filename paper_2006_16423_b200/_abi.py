@@ -22,6 +22,8 @@ DSG_FLAG_FORCE_INT64 = 1
 DSG_FLAG_NO_FASTGATE = 2
 DSG_FLAG_HASH_ENUM = 4
 DSG_FLAG_KEEP_TABLES = 8
+DSG_FLAG_TIME_KERNELS = 16
+DSG_FLAG_LEVEL_LAUNCH = 32
 
 (DSG_OK, DSG_INFEASIBLE, DSG_BUDGET, DSG_DEADLINE, DSG_INVALID, DSG_OVERFLOW,
  DSG_MISSING_BANDWIDTH, DSG_CUDA_ERROR, DSG_LOGIC, DSG_UNSUPPORTED) = range(10)
@@ -113,6 +115,8 @@ class dsg_result(C.Structure):
         ("t_device_ms", C.c_double),
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
+        ("persistent_blocks", C.c_int32),
+        ("pad_", C.c_int32),
         ("words", C.c_int32),
         ("ideal_bits", C.POINTER(C.c_uint64)),
         ("dp_values", C.POINTER(C.c_int64)),
@@ -215,6 +219,7 @@ def pod_config(cfg: DeviceConfig) -> dsg_config:
 
 
 def pod_options(budget: int = DSG_DEFAULT_IDEAL_BUDGET, deadline_seconds: Optional[float] = None,
-                device: int = -1, shard_count: int = 0, flags: int = 0) -> dsg_options:
+                device: int = -1, shard_count: int = 0, flags: int = 0,
+                max_blocks: int = 0) -> dsg_options:
     return dsg_options(int(budget), float(deadline_seconds or 0.0), int(device),
-                       int(shard_count), int(flags), 0)
+                       int(shard_count), int(flags), int(max_blocks))

@@ -18,8 +18,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdsg_b200.so")
-SOURCES = ["capi.cu", "enumerate.cu", "describe.cu", "transition.cu"]
-HEADERS = ["dsg_device.cuh", "dsg_internal.h"]
+SOURCES = ["capi.cu", "enumerate.cu", "describe.cu", "transition.cu", "persistent.cu"]
+HEADERS = ["dsg_device.cuh", "dsg_internal.h", "scan.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

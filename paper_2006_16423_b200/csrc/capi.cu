@@ -615,6 +615,7 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   D.fw = ctx.get("d.fw", I * vsz);
   D.fwinf = ctx.get_t<int32_t>("d.fwinf", I);
   D.upset = ctx.get_t<uint8_t>("d.upset", I);
+  D.srec = ctx.get_t<SrcRec>("d.srec", I);
   D.counts = ctx.get_t<int64_t>("d.counts", (size_t)kNumCounts * (I + 1));
   CK(cudaMemsetAsync(D.counts, 0, sizeof(int64_t) * kNumCounts * (I + 1), st));
   launch_describe(D, false, st);
@@ -642,27 +643,7 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   CK(cudaMemsetAsync(pairs_d, 0, sizeof(unsigned long long), st));
   launch_init_empty(vb, K, Lc, dp, bp, st);
 
-  const int64_t target_ctas = (int64_t)ctx.sm_count * 8;
-  struct Plan {
-    int64_t chunks, chunk_len;
-  };
-  std::vector<Plan> plan(lat.n_levels);
-  size_t part_elems = 1;
-  for (int s = 1; s < lat.n_levels; ++s) {
-    const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
-    const int64_t S = lat.level_off[s];
-    const int64_t tiles = (T + kTileTargets - 1) / kTileTargets;
-    int64_t chunks = std::max<int64_t>(1, (target_ctas + tiles - 1) / tiles);
-    chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / 32));
-    chunks = std::min<int64_t>(chunks, 65535);
-    int64_t len = (S + chunks - 1) / chunks;
-    chunks = (S + len - 1) / len;
-    plan[s] = {chunks, len};
-    part_elems = std::max(part_elems, (size_t)(chunks * C * T));
-  }
-  void* part_val = ctx.get("dp.part_val", part_elems * vsz);
-  int32_t* part_arg = ctx.get_t<int32_t>("dp.part_arg", part_elems);
-
+  const bool persistent = !(flags & DSG_FLAG_LEVEL_LAUNCH);
   LevelLaunch LL{};
   LL.value_bits = vb;
   LL.training = P.training ? 1 : 0;
@@ -684,6 +665,7 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   LL.fw = D.fw;
   LL.fwinf = D.fwinf;
   LL.upset = D.upset;
+  LL.srec = D.srec;
   LL.chunk_off = D.counts + (size_t)kCntChunks * (I + 1);
   LL.chunks = D.chunks;
   LL.fpool = D.fpool;
@@ -699,23 +681,162 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   LL.n_nodes = P.n;
   LL.dp = dp;
   LL.bp = bp;
-  LL.part_val = part_val;
-  LL.part_arg = part_arg;
   LL.pair_counter = pairs_d;
+
+  // ---- chunk plan: (target tile x source chunk) work items per level
+  PersistInfo pinfo{};
+  if (persistent) {
+    query_persistent(LL, &pinfo);
+    if (opt->reserved > 0) pinfo.blocks = std::min(pinfo.blocks, opt->reserved);
+  }
+  const int64_t target_items =
+      persistent ? std::max(1, pinfo.blocks) : (int64_t)ctx.sm_count * 8;
+  std::vector<int64_t> n_chunks(lat.n_levels, 1), chunk_len(lat.n_levels, 1),
+      tile_base(lat.n_levels, 0);
+  std::vector<int32_t> mode(lat.n_levels, 0);
+  std::vector<int64_t> item_base(lat.n_levels + 1, 0), part_base(lat.n_levels, 0);
+  size_t part_elems = 1;
+  int64_t total_tiles = 0, total_items = 0;
+  // persistent, mode 0: (32-target group, chunk) CTA items whose 4 warps
+  // split the chunk (chunks down to 4 sources); mode 1 (few targets): (target,
+  // chunk) warp items with one source per lane.  Per-level path: 128-target
+  // tiles x chunks of >= 16 sources.
+  const int64_t kSmallLevel = 16;
+  for (int s = 1; s < lat.n_levels; ++s) {
+    const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
+    const int64_t S = lat.level_off[s];
+    int64_t units, min_chunk, items;
+    if (!persistent) {
+      units = (T + kTileTargets - 1) / kTileTargets;
+      min_chunk = 16;
+      items = target_items;
+    } else if (T < kSmallLevel) {
+      mode[s] = 1;
+      units = T;
+      min_chunk = kTileTargets;  // one source per thread
+      items = target_items;
+    } else {
+      units = (T + 31) / 32;
+      min_chunk = 4;
+      items = target_items;
+    }
+    int64_t chunks = std::max<int64_t>(1, (items + units - 1) / units);
+    chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / min_chunk));
+    int64_t len = (S + chunks - 1) / chunks;
+    chunks = (S + len - 1) / len;
+    n_chunks[s] = chunks;
+    chunk_len[s] = len;
+    tile_base[s] = total_tiles;
+    total_tiles += units;
+    item_base[s] = total_items;
+    total_items += units * chunks;
+    part_elems = std::max(part_elems, (size_t)(chunks * C * T));
+  }
+  item_base[lat.n_levels] = total_items;
+  if (persistent) {
+    // the dataflow kernel keeps every level's partials live at once
+    part_elems = 1;
+    for (int s = 1; s < lat.n_levels; ++s) {
+      part_base[s] = (int64_t)part_elems;
+      const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
+      const int64_t rows = mode[s] == 0 ? ((T + 31) / 32) * 32 : T;  // mode 0: whole groups
+      part_elems += (size_t)(n_chunks[s] * C * rows);
+    }
+  }
+  LL.part_val = ctx.get("dp.part_val", part_elems * vsz);
+  LL.part_arg = ctx.get_t<int32_t>("dp.part_arg", part_elems);
 
   cudaEvent_t ev_desc, ev_dp;
   CK(cudaEventCreate(&ev_desc));
   CK(cudaEventCreate(&ev_dp));
-  CK(cudaEventRecord(ev_desc, st));
   std::vector<cudaEvent_t> kev;
   std::vector<cudaEvent_t> dl_ev;
   const int kDeadlineStride = 8;
-  for (int s = 1; s < lat.n_levels; ++s) {
+  if (persistent) {
+    PersistPlan PP{};
+    PP.n_levels = lat.n_levels;
+    int64_t* lvl_d = ctx.get_t<int64_t>("pp.level_off", lat.level_off.size());
+    int64_t* nch_d = ctx.get_t<int64_t>("pp.n_chunks", n_chunks.size());
+    int64_t* cl_d = ctx.get_t<int64_t>("pp.chunk_len", chunk_len.size());
+    int64_t* tb_d0 = ctx.get_t<int64_t>("pp.tile_base", tile_base.size());
+    CK(cudaMemcpyAsync(lvl_d, lat.level_off.data(), sizeof(int64_t) * lat.level_off.size(),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(nch_d, n_chunks.data(), sizeof(int64_t) * n_chunks.size(),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(cl_d, chunk_len.data(), sizeof(int64_t) * chunk_len.size(),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(tb_d0, tile_base.data(), sizeof(int64_t) * tile_base.size(),
+                       cudaMemcpyHostToDevice, st));
+    PP.level_off = lvl_d;
+    PP.n_chunks = nch_d;
+    PP.chunk_len = cl_d;
+    PP.tile_base = tb_d0;
+    PP.tile_count = ctx.get_t<unsigned>("pp.tile_count", (size_t)total_tiles + 1);
+    CK(cudaMemsetAsync(PP.tile_count, 0, sizeof(unsigned) * (total_tiles + 1), st));
+    int32_t* mode_d = ctx.get_t<int32_t>("pp.mode", mode.size());
+    CK(cudaMemcpyAsync(mode_d, mode.data(), sizeof(int32_t) * mode.size(), cudaMemcpyHostToDevice, st));
+    PP.mode = mode_d;
+    int64_t* ib_d = ctx.get_t<int64_t>("pp.item_base", item_base.size());
+    CK(cudaMemcpyAsync(ib_d, item_base.data(), sizeof(int64_t) * item_base.size(),
+                       cudaMemcpyHostToDevice, st));
+    PP.item_base = ib_d;
+    int64_t* pb_d = ctx.get_t<int64_t>("pp.part_base", part_base.size());
+    CK(cudaMemcpyAsync(pb_d, part_base.data(), sizeof(int64_t) * part_base.size(),
+                       cudaMemcpyHostToDevice, st));
+    PP.part_base = pb_d;
+    PP.total_items = total_items;
+    {
+      std::vector<int32_t> lvl_of((size_t)I);
+      for (int s = 0; s < lat.n_levels; ++s)
+        for (int64_t o = lat.level_off[s]; o < lat.level_off[s + 1]; ++o) lvl_of[o] = s;
+      int32_t* lo_d = ctx.get_t<int32_t>("pp.level_of", (size_t)I);
+      CK(cudaMemcpyAsync(lo_d, lvl_of.data(), sizeof(int32_t) * I, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));  // lvl_of is a stack temporary
+      PP.level_of = lo_d;
+    }
+    unsigned* ctl = ctx.get_t<unsigned>("pp.ctl", (size_t)lat.n_levels + 64);
+    CK(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * (lat.n_levels + 64), st));
+    PP.stop = reinterpret_cast<int*>(ctl);
+    PP.err = reinterpret_cast<int*>(ctl + 1);
+    PP.done = ctl + 32;
+    {
+      // level 0 (the empty ideal) is final before the launch
+      const unsigned one = 1;
+      CK(cudaMemcpyAsync(PP.done, &one, sizeof one, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    PP.deadline_ns = 0;
+    if (has_deadline) {
+      uint64_t* gt_d = ctx.get_t<uint64_t>("pp.gt", 1);
+      uint64_t gt = 0;
+      launch_read_globaltimer(gt_d, st);
+      D2H(&gt, gt_d, sizeof gt);
+      CK(cudaStreamSynchronize(st));
+      const int64_t left = std::chrono::duration_cast<std::chrono::nanoseconds>(deadline - Clock::now()).count();
+      PP.deadline_ns = (int64_t)gt + std::max<int64_t>(left, 1);
+    }
+    CK(cudaEventRecord(ev_desc, st));
+    launch_persistent(LL, PP, st, &pinfo);
+    if (pinfo.launch_error != 0)
+      throw Fail{DSG_CUDA_ERROR, std::string("cooperative launch failed: ") +
+                                     cudaGetErrorString((cudaError_t)pinfo.launch_error)};
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev_dp, st));
+    int flags_h[2] = {0, 0};
+    D2H(flags_h, PP.stop, sizeof flags_h);
+    CK(cudaStreamSynchronize(st));
+    if (flags_h[1]) throw Fail{DSG_CUDA_ERROR, "dataflow watchdog fired"};
+    if (flags_h[0]) throw Fail{DSG_DEADLINE, "time limit reached"};
+  } else {
+    CK(cudaEventRecord(ev_desc, st));
+  }
+  res->persistent_blocks = persistent ? pinfo.blocks : 0;
+  for (int s = 1; s < lat.n_levels && !persistent; ++s) {
     LL.t_lo = lat.level_off[s];
     LL.t_hi = lat.level_off[s + 1];
     LL.s_hi = lat.level_off[s];
-    LL.n_chunks = plan[s].chunks;
-    LL.chunk_len = plan[s].chunk_len;
+    LL.n_chunks = n_chunks[s];
+    LL.chunk_len = chunk_len[s];
     if (timing) {
       cudaEvent_t a, b;
       CK(cudaEventCreate(&a));
@@ -749,7 +870,7 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
     }
   }
   CK(cudaGetLastError());
-  CK(cudaEventRecord(ev_dp, st));
+  if (!persistent) CK(cudaEventRecord(ev_dp, st));
 
   // ---- traceback
   const int maxb = K + Lc + 1;
@@ -809,7 +930,8 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   (void)desc_ms;
   res->t_dp_ms = dp_ms;
   res->t_describe_ms = std::max(0.0, ms_since(t2) - dp_ms);
-  res->t_transition_kernel_ms = kern_ms;
+  // persistent: the one cooperative launch spans ev_desc..ev_dp
+  res->t_transition_kernel_ms = persistent ? dp_ms : kern_ms;
   res->n_pairs = (int64_t)pairs;
   res->value_bits = vb;
   res->denominator = P.D;

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(128) describe_kernel(DescribeLaunch a) {
   int64_t chunk_base = FILL ? cnt[kCntChunks * stride + o] : 0;
   int64_t f_base = FILL ? cnt[kCntF * stride + o] : 0;
   int64_t n_base = FILL ? cnt[kCntN * stride + o] : 0;
+  FChunk first{};
   for (int c = 0; c < n_chunks; ++c) {
     int lo = c * 64;
     int hi = min(nF, lo + 64);
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(128) describe_kernel(DescribeLaunch a) {
       ch.off_n = (int32_t)(n_base + n_items);
       ch.infmask = infmask;
       a.chunks[chunk_base + c] = ch;
+      if (c == 0) first = ch;
     }
     n_items += nN;
   }
@@ -213,6 +215,20 @@ __global__ void __launch_bounds__(128) describe_kernel(DescribeLaunch a) {
   a.unsup[o] = un;
   ((V*)a.fw)[o] = (V)fwv;
   a.fwinf[o] = fwi;
+  SrcRec r;
+  r.cpu = cpu;
+  r.acc = acc;
+  r.mem = mem;
+  r.unsup = un;
+  r.n_chunks = n_chunks;
+  r.chunk0 = (int32_t)chunk_base;
+  r.n_f = first.n_f;
+  r.n_n = first.n_n;
+  r.off_f = first.off_f;
+  r.off_n = first.off_n;
+  r.pad = 0;
+  r.infmask = first.infmask;
+  a.srec[o] = r;
 }
 
 // In-place exclusive scan of one [n + 1] int64 array per block

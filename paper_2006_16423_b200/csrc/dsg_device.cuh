@@ -47,6 +47,18 @@ struct FChunk {
   uint64_t infmask; // producers whose comm is the infinite sentinel
 };
 
+// Everything the transition kernel needs about a SOURCE ideal before its
+// frontier walk, in one 64-byte record (4 x 16-byte broadcast loads):
+// prefix sums over A(J) and the first frontier chunk inline.
+struct __align__(16) SrcRec {
+  int64_t cpu, acc, mem;
+  int32_t unsup, n_chunks;
+  int32_t chunk0, n_f, n_n, off_f;
+  int32_t off_n, pad;
+  uint64_t infmask;
+};
+static_assert(sizeof(SrcRec) == 64, "SrcRec is one 64-byte record");
+
 // Upper neighbour n of the source closure: bit position of n in the target
 // closure bitset, and which chunk-local producers have a real edge to n.
 struct NItem {

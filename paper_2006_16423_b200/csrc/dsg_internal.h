@@ -65,6 +65,7 @@ struct DescribeLaunch {
   void* fw;          // V[I]
   int32_t* fwinf;
   uint8_t* upset;    // training: Φ(J) is an up-set of the backward part
+  SrcRec* srec;      // [I] source records
   int64_t* counts;   // [kNumCounts][I + 1]  (pass 1 output, scanned in place)
   // pools (pass 2)
   FChunk* chunks;
@@ -102,6 +103,7 @@ struct LevelLaunch {
   const void* fw;
   const int32_t* fwinf;
   const uint8_t* upset;
+  const SrcRec* srec;
   const int64_t* chunk_off;   // counts[kCntChunks] scanned, [I+1]
   const FChunk* chunks;
   const void* fpool;
@@ -124,6 +126,37 @@ struct LevelLaunch {
 };
 
 void launch_transition(const LevelLaunch& L, cudaStream_t st);
+
+// One cooperative launch for all levels (transition.cu).
+struct PersistPlan {
+  int n_levels;
+  const int64_t* level_off;  // [n_levels + 1]
+  const int32_t* mode;       // [n_levels] 0: lanes own targets, 1: lanes own sources
+  const int64_t* n_chunks;   // [n_levels] source chunks per target (group)
+  const int64_t* chunk_len;  // [n_levels]
+  const int64_t* tile_base;  // [n_levels] prefix of arrival counters over levels
+  const int64_t* item_base;  // [n_levels + 1] prefix of work items over levels
+  const int64_t* part_base;  // [n_levels] offset of each level's partials
+  const int32_t* level_of;   // [I] level of each ordinal
+  int64_t total_items;
+  unsigned* tile_count;      // [total counters], zeroed
+  unsigned* done;            // [n_levels] finished targets per level, zeroed
+  int* stop;                 // deadline reached / abort
+  int* err;                  // watchdog fired
+  int64_t deadline_ns;       // %globaltimer deadline, 0 = none
+};
+
+struct PersistInfo {
+  int query_only;
+  int blocks;      // in: requested grid (0 = full residency); out: launched grid
+  int per_sm;      // resident CTAs per SM
+  int launch_error;
+};
+
+void query_persistent(const LevelLaunch& L, PersistInfo* info);
+void launch_persistent(const LevelLaunch& L, const PersistPlan& P, cudaStream_t st,
+                       PersistInfo* info);
+void launch_read_globaltimer(uint64_t* out, cudaStream_t st);
 void launch_finalize(const LevelLaunch& L, cudaStream_t st);
 void launch_init_empty(int value_bits, int K, int L, void* dp, int32_t* bp, cudaStream_t st);
 

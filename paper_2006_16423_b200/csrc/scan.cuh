@@ -1,0 +1,393 @@
+// scan.cuh — the fused K2+K3+K4 pair scan shared by both level drivers.
+//
+// Replaces the reference's per-target DFS over sub-ideals
+// (walk_subideals + apply_candidate, /root/reference/proj/src/dp_solver.cpp:
+// 197-317) with a dense scan that needs no hash lookups and no allocation:
+//
+//   * K2 (pair enumeration): I' ⊆ I is a W-word AND-NOT test of the source
+//     bitset against the target bitset held in shared memory;
+//   * K3 (block cost): prefix differences from the 64-byte source record +
+//     the source-frontier walk of describe.cu (two 64-bit masks per chunk
+//     of <= 64 producers), see acc_block_cost;
+//   * K4 (min-max): per cell max(dp[I'][k-1][l], acc) and
+//     max(dp[I'][k][l-1], cpu) with a strict-< update; the argmin is
+//     2*I' + (cpu block), so "smallest (value, arg)" is a total order and the
+//     result does not depend on how sources are split across lanes, warps,
+//     CTAs or GPUs.
+//
+// Template knobs: V = int32_t/int64_t fixed point; LP1 = L+1 and KP1MAX =
+// max K+1 for register-resident cells (LP1 == 0: generic shared-memory
+// cells); TS = stride of the target column in shared memory (32/128 when
+// lanes own targets, 1 when all lanes share one target); UNIFORM = all lanes
+// walk the same sources (enables the warp-wide early skip).
+#pragma once
+
+#include <climits>
+#include <cstdint>
+
+#include "dsg_device.cuh"
+#include "dsg_internal.h"
+
+namespace dsg {
+namespace scan {
+
+template <typename V>
+__device__ __forceinline__ V vmax(V a, V b) {
+  return a > b ? a : b;
+}
+
+// combine_interleaving, graph.cpp:457-467
+template <typename V>
+__device__ __forceinline__ V combine(V in, V proc, V out, int mode) {
+  if (mode == 0) return in + proc + out;
+  if (mode == 1) return vmax(proc, (V)(in + out));
+  return vmax(proc, vmax(in, out));
+}
+
+__device__ __forceinline__ SrcRec load_rec(const SrcRec* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
+  SrcRec r;
+  r.cpu = (int64_t)(((uint64_t)(uint32_t)a.y << 32) | (uint32_t)a.x);
+  r.acc = (int64_t)(((uint64_t)(uint32_t)a.w << 32) | (uint32_t)a.z);
+  r.mem = (int64_t)(((uint64_t)(uint32_t)b.y << 32) | (uint32_t)b.x);
+  r.unsup = b.z;
+  r.n_chunks = b.w;
+  r.chunk0 = c.x;
+  r.n_f = c.y;
+  r.n_n = c.z;
+  r.off_f = c.w;
+  r.off_n = d.x;
+  r.pad = d.y;
+  r.infmask = ((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z;
+  return r;
+}
+
+// General backward-contiguity gate (is_contiguous over reachability_within
+// of the backward part, graph.cpp:349-363), used when the fast up-set test
+// does not apply.  tA: the target column (stride TS).
+template <int TS>
+__device__ bool bw_contiguous(const LevelLaunch& a, const uint64_t* tA,
+                              const uint64_t* __restrict__ sA) {
+  const int W = a.W;
+  uint64_t rf[kMaxWords], rt[kMaxWords], B[kMaxWords];
+  bool any = false;
+  for (int w = 0; w < W; ++w) {
+    B[w] = tA[w * TS] & ~sA[w] & a.bwset[w];
+    rf[w] = 0;
+    rt[w] = 0;
+    any |= B[w] != 0;
+  }
+  if (!any) return true;
+  for (int w = 0; w < W; ++w) {
+    uint64_t x = B[w];
+    while (x) {
+      int b = __ffsll((long long)x) - 1;
+      x &= x - 1;
+      int u = (w << 6) | b;
+      const uint64_t* f = a.bw_from + (size_t)u * W;
+      const uint64_t* t = a.bw_to + (size_t)u * W;
+      for (int k = 0; k < W; ++k) {
+        rf[k] |= f[k];
+        rt[k] |= t[k];
+      }
+    }
+  }
+  for (int w = 0; w < W; ++w)
+    if (rf[w] & rt[w] & ~B[w]) return false;
+  return true;
+}
+
+// One frontier chunk: hit = producers with an upper neighbour inside the
+// target, miss = producers with an upper neighbour outside it.
+template <typename V, int TS>
+__device__ __forceinline__ void frontier_chunk(const LevelLaunch& a, int n_f, int n_n, int off_f,
+                                               int off_n, uint64_t infm, const uint64_t* tA,
+                                               V& cin, V& csub, bool& cin_inf, int& cout_inf) {
+  const NItem* __restrict__ nitems = a.nitems;
+  const V* __restrict__ fpool = (const V*)a.fpool;
+  uint64_t hit = 0, miss = 0;
+  for (int i = 0; i < n_n; ++i) {
+    const uint4 it = __ldg(reinterpret_cast<const uint4*>(nitems + off_n + i));
+    const uint64_t pm = ((uint64_t)it.w << 32) | it.z;
+    const bool in = (tA[it.x * TS] >> it.y) & 1ull;
+    hit |= in ? pm : 0ull;
+    miss |= in ? 0ull : pm;
+  }
+  for (int j = 0; j < n_f; ++j) {
+    const V w = __ldg(fpool + off_f + j);
+    cin += ((hit >> j) & 1ull) ? w : (V)0;
+    csub += ((miss >> j) & 1ull) ? w : (V)0;
+  }
+  cin_inf |= (hit & infm) != 0ull;
+  cout_inf -= __popcll(miss & infm);
+}
+
+template <typename V>
+struct Target {
+  V cpu, acc, mem, fw;
+  int un, fwi;
+  bool up, active;
+  int64_t t, tl, l_lo, l_hi;
+};
+
+// Scalars of target t (tl = index within its level).
+template <typename V, bool TRAIN>
+__device__ __forceinline__ Target<V> target_scalars(const LevelLaunch& a, int64_t t, int64_t tl,
+                                                    bool active) {
+  Target<V> x;
+  x.tl = tl;
+  x.active = active;
+  x.t = t;
+  x.cpu = __ldg((const V*)a.pfx_cpu + t);
+  x.acc = __ldg((const V*)a.pfx_acc + t);
+  x.mem = __ldg((const V*)a.pfx_mem + t);
+  x.fw = __ldg((const V*)a.fw + t);
+  x.un = __ldg(a.unsup + t);
+  x.fwi = __ldg(a.fwinf + t);
+  x.up = TRAIN ? (__ldg(a.upset + t) != 0) : true;
+  x.l_lo = TRAIN ? __ldg(a.l_off + t) : 0;
+  x.l_hi = TRAIN ? __ldg(a.l_off + t + 1) : 0;
+  return x;
+}
+
+// Thread `lane` of a group of TS targets of [t_lo, t_hi): scalars, and (if
+// stage) its target / interior bitsets into its shared-memory column.
+template <typename V, bool TRAIN, int TS>
+__device__ __forceinline__ Target<V> load_target(const LevelLaunch& a, int64_t t_lo, int64_t t_hi,
+                                                 int64_t grp, int lane, uint64_t* colA,
+                                                 uint64_t* colInt, bool stage = true) {
+  const int W = a.W;
+  const int64_t tl = grp * TS + lane;
+  const bool active = t_lo + tl < t_hi;
+  const int64_t t = active ? t_lo + tl : t_lo;
+  if (stage) {
+    for (int w = 0; w < W; ++w) {
+      colA[w * TS] = active ? __ldg(a.abits + (size_t)t * W + w) : 0ull;
+      if (TRAIN) colInt[w * TS] = active ? __ldg(a.intbits + (size_t)t * W + w) : 0ull;
+    }
+  }
+  return target_scalars<V, TRAIN>(a, t, tl, active);
+}
+
+// Block cost of B = A(t) \ A(s) on an accelerator (BlockTracker::acc_load,
+// dp_solver.cpp:90-97), given the prefix difference proc; INF if infeasible.
+//   comm_out(B) = W(F(A)) - W({u in F(A') : succ(u)\A' ⊄ A})
+//                 + W(P'(A') ∩ Int(A))                         [training]
+//   comm_in(B)  = W({u in F(A') : (succ(u)\A') ∩ A ≠ ∅})
+//                 + W({u in L(A) : succ(u) ∩ A ⊄ A'})          [training]
+template <typename V, bool TRAIN, int TS>
+__device__ __forceinline__ V acc_block_cost(const LevelLaunch& a, int64_t s, const SrcRec& r,
+                                            V proc, const Target<V>& x, const uint64_t* tA,
+                                            const uint64_t* tInt) {
+  constexpr V INF = VTraits<V>::INF;
+  V cin = 0, csub = 0;
+  bool cin_inf = false;
+  int cout_inf = x.fwi;
+  if (r.n_chunks > 0)
+    frontier_chunk<V, TS>(a, r.n_f, r.n_n, r.off_f, r.off_n, r.infmask, tA, cin, csub, cin_inf,
+                          cout_inf);
+  for (int c = 1; c < r.n_chunks; ++c) {
+    const FChunk* ch = a.chunks + r.chunk0 + c;
+    frontier_chunk<V, TS>(a, __ldg(&ch->n_f), __ldg(&ch->n_n), __ldg(&ch->off_f),
+                          __ldg(&ch->off_n), __ldg(&ch->infmask), tA, cin, csub, cin_inf, cout_inf);
+  }
+  V cout = x.fw - csub;
+  if (TRAIN) {
+    const int64_t p0 = __ldg(a.p_off + s), p1 = __ldg(a.p_off + s + 1);
+    for (int64_t p = p0; p < p1; ++p) {
+      const PItem* pi = a.pitems + p;
+      const uint32_t word = __ldg(&pi->word), bit = __ldg(&pi->bit);
+      const bool in = (tInt[word * TS] >> bit) & 1ull;
+      cout += in ? (V)__ldg(&pi->weight) : (V)0;
+      cout_inf += (in && __ldg(&pi->inf)) ? 1 : 0;
+    }
+    const uint64_t* sA = a.abits + (size_t)s * a.W;
+    for (int64_t e = x.l_lo; e < x.l_hi; ++e) {
+      const LEntry le = a.lentries[e];
+      bool charged = false;
+      for (int i = 0; i < le.n_items; ++i) {
+        const MaskItem mi = a.litems[le.off_items + i];
+        charged |= (mi.mask & ~__ldg(sA + mi.word)) != 0ull;
+      }
+      cin += charged ? (V)le.weight : (V)0;
+      cin_inf |= charged && le.inf;
+    }
+  }
+  if (cin_inf || cout_inf > 0) return INF;
+  return combine<V>(cin, proc, cout, a.interleave);
+}
+
+// Scan sources s0, s0+step, ... < s1 for target x.  Cells in registers
+// (LP1 > 0) or in a shared-memory column colv/cola with stride CS (LP1 == 0).
+// Source dp rows use plain (coherent) loads: in the persistent kernel other
+// CTAs wrote them before the last grid barrier.
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int CS>
+__device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Target<V>& x,
+                                                 int64_t s0, int64_t s1, int step,
+                                                 const uint64_t* tA, const uint64_t* tInt, V* best,
+                                                 int32_t* barg, V* colv, int32_t* cola) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr bool kGeneric = LP1 == 0;
+  constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
+  const int W = a.W;
+  const int C = a.C;
+  const V* dp = (const V*)a.dp;
+  const V mlim = (V)a.mlim;
+  unsigned nested_cnt = 0;
+  for (int64_t s = s0; s < s1; s += step) {
+    // K2: I' ⊆ I
+    const uint64_t* __restrict__ sA = a.abits + (size_t)s * W;
+    bool nested = x.active;
+    for (int w = 0; w < W; ++w) nested &= (__ldg(sA + w) & ~tA[w * TS]) == 0ull;
+    if (UNIFORM && !__any_sync(0xffffffffu, nested)) continue;
+    if (!nested) continue;
+    ++nested_cnt;
+    if (TRAIN && a.has_bw) {
+      if (!(a.fastgate && x.up && __ldg(a.upset + s)) && !bw_contiguous<TS>(a, tA, sA)) continue;
+    }
+    const SrcRec r = load_rec(a.srec + s);
+    // K3: block cost
+    const V cpu = x.cpu - (V)r.cpu;
+    V acc = INF;
+    bool acc_ok = a.K > 0 && (x.un - r.unsup) == 0;
+    if (acc_ok && a.memcheck) acc_ok = !((V)(x.mem - (V)r.mem) > mlim);
+    if (acc_ok) acc = acc_block_cost<V, TRAIN, TS>(a, s, r, (V)(x.acc - (V)r.acc), x, tA, tInt);
+    // K4: min-max update, strict < keeps the smallest argmin
+    const V* sdp = dp + (size_t)s * C;
+    const int32_t aa = (int32_t)(2 * s), ac = aa + 1;
+    if (!kGeneric) {
+#pragma unroll
+      for (int c = 0; c < CMAX; ++c) {
+        const int k = c / (LP1 ? LP1 : 1);
+        const int l = c % (LP1 ? LP1 : 1);
+        if (c < C) {
+          if (k >= 1) {
+            const V v = vmax(sdp[c - LP1], acc);
+            if (v < best[c]) {
+              best[c] = v;
+              barg[c] = aa;
+            }
+          }
+          if (l >= 1) {
+            const V v = vmax(sdp[c - 1], cpu);
+            if (v < best[c]) {
+              best[c] = v;
+              barg[c] = ac;
+            }
+          }
+        }
+      }
+    } else {
+      const int lp1 = a.L + 1;
+      for (int k = 0; k <= a.K; ++k) {
+        for (int l = 0; l <= a.L; ++l) {
+          const int c = k * lp1 + l;
+          V b = colv[c * CS];
+          int32_t g = cola[c * CS];
+          if (k >= 1) {
+            const V v = vmax(sdp[c - lp1], acc);
+            if (v < b) {
+              b = v;
+              g = aa;
+            }
+          }
+          if (l >= 1) {
+            const V v = vmax(sdp[c - 1], cpu);
+            if (v < b) {
+              b = v;
+              g = ac;
+            }
+          }
+          colv[c * CS] = b;
+          cola[c * CS] = g;
+        }
+      }
+    }
+  }
+  return nested_cnt;
+}
+
+template <typename V, int LP1, int KP1MAX, int CS>
+__device__ __forceinline__ void init_cells(int C, V* best, int32_t* barg, V* colv, int32_t* cola) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr int CMAX = LP1 == 0 ? 1 : LP1 * KP1MAX;
+#pragma unroll
+  for (int c = 0; c < CMAX; ++c) {
+    best[c] = INF;
+    barg[c] = INT_MAX;
+  }
+  if (LP1 == 0) {
+    for (int c = 0; c < C; ++c) {
+      colv[c * CS] = INF;
+      cola[c * CS] = INT_MAX;
+    }
+  }
+}
+
+// lexicographic (value, arg) minimum
+template <typename V>
+__device__ __forceinline__ void vmin_arg(V& v, int32_t& g, V v2, int32_t g2) {
+  if (v2 < v || (v2 == v && g2 < g)) {
+    v = v2;
+    g = g2;
+  }
+}
+
+// monotone_pass, dp_solver.cpp:180-193 (in place, k then l ascending), on
+// register cells with compile-time indices
+template <typename V, int LP1, int CMAX>
+__device__ __forceinline__ void monotone_regs(V* v, int32_t* g, int C) {
+#pragma unroll
+  for (int c = 0; c < CMAX; ++c) {
+    const int k = c / (LP1 ? LP1 : 1), l = c % (LP1 ? LP1 : 1);
+    if (c < C) {
+      if (k > 0 && v[c - (LP1 ? LP1 : 1)] < v[c]) {
+        v[c] = v[c - (LP1 ? LP1 : 1)];
+        g[c] = -3;
+      }
+      if (l > 0 && v[c - 1] < v[c]) {
+        v[c] = v[c - 1];
+        g[c] = -4;
+      }
+    }
+  }
+}
+
+// ... and on a strided shared-memory / global column
+template <typename V>
+__device__ __forceinline__ void monotone_strided(V* v, int32_t* g, int stride, int K, int L) {
+  const int lp1 = L + 1;
+  for (int k = 0; k <= K; ++k) {
+    for (int l = 0; l <= L; ++l) {
+      const int c = k * lp1 + l;
+      V cur = v[c * stride];
+      int32_t ga = g[c * stride];
+      if (k > 0 && v[(c - lp1) * stride] < cur) {
+        cur = v[(c - lp1) * stride];
+        ga = -3;
+      }
+      if (l > 0 && v[(c - 1) * stride] < cur) {
+        cur = v[(c - 1) * stride];
+        ga = -4;
+      }
+      v[c * stride] = cur;
+      g[c * stride] = ga;
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+}  // namespace scan
+}  // namespace dsg

@@ -59,6 +59,7 @@ class SolveOptions:
     device: int = -1
     flags: int = 0
     shard_count: int = 0
+    max_blocks: int = 0  # > 0 caps the persistent kernel's grid (testing)
 
 
 @dataclass
@@ -107,7 +108,7 @@ class Session:
         self._pg = _abi.pod_graph(g)
         self._cfg = _abi.pod_config(config)
         self._po = _abi.pod_options(opt.ideal_budget, opt.deadline_seconds, opt.device,
-                                    opt.shard_count, opt.flags)
+                                    opt.shard_count, opt.flags, opt.max_blocks)
         st = _abi.dsg_result()
         self._h = lib.dsg_session_create(mode, C.byref(self._pg.struct), C.byref(self._cfg),
                                          C.byref(self._po), C.byref(st))
@@ -149,7 +150,7 @@ def run_dp(lib: C.CDLL, prefix: str, mode: int, g: Graph, config: DeviceConfig,
     pg = _abi.pod_graph(g)
     cfg = _abi.pod_config(config)
     po = _abi.pod_options(opt.ideal_budget, opt.deadline_seconds, opt.device, opt.shard_count,
-                          opt.flags)
+                          opt.flags, opt.max_blocks)
     res = _abi.dsg_result()
     getattr(lib, f"{prefix}_dp_solve")(mode, C.byref(pg.struct), C.byref(cfg), C.byref(po),
                                        C.byref(res))

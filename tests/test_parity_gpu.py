@@ -57,6 +57,33 @@ def test_golden_objective_alternate_paths(gpu, flags):
         assert obj == rat_from_json(case["objective"]), case["name"]
 
 
+@pytest.mark.parametrize("flags,max_blocks", [(_abi.DSG_FLAG_LEVEL_LAUNCH, 0), (0, 1), (0, 3),
+                                               (_abi.DSG_FLAG_FORCE_INT64, 2)],
+                         ids=["level-launch", "persistent-1cta", "persistent-3cta", "int64-2cta"])
+def test_driver_variants_match_golden(gpu, flags, max_blocks):
+    """Per-level launches and tiny persistent grids (every CTA owns many work
+    items, exercising the tile counters and the grid barrier) agree."""
+    for case in CORPUS[::5]:
+        g = graph_from_json(case["graph"])
+        cfg = config_from_case(case)
+        f = solver.solve_maxload_training if case["mode"] == 1 else solver.solve_maxload_inference
+        try:
+            got = f(g, cfg, solver.SolveOptions(flags=flags, max_blocks=max_blocks)).objective_value
+        except InfeasibleError:
+            got = INF
+        assert got == rat_from_json(case["objective"]), case["name"]
+
+
+def test_standin_driver_variants_agree(gpu):
+    w = wl.standin("C3")
+    base = device_solve(1, w.graph, w.config)
+    for flags, mb in [(_abi.DSG_FLAG_LEVEL_LAUNCH, 0), (0, 5), (_abi.DSG_FLAG_FORCE_INT64, 0)]:
+        s = solver.solve_maxload_training(w.graph, w.config,
+                                          solver.SolveOptions(flags=flags, max_blocks=mb))
+        assert s.objective_value == base.objective_value
+        assert s.stats["n_pairs"] == base.stats["n_pairs"]
+
+
 @pytest.mark.parametrize("hash_mode", [False, True], ids=["canonical", "hashset"])
 @pytest.mark.parametrize("case", IDEALS, ids=[c["name"] for c in IDEALS])
 def test_golden_ideal_lists(gpu, case, hash_mode):
