@@ -702,6 +702,10 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   // chunk) warp items with one source per lane.  Per-level path: 128-target
   // tiles x chunks of >= 16 sources.
   const int64_t kSmallLevel = 16;
+  // persistent: explicit chunk boundaries per level.  Sources of the newest
+  // level (s-1) get small chunks, ordered last, because only they wait for
+  // the previous level; older sources get large chunks that start early.
+  std::vector<int64_t> chunk_lo, chunk_base(lat.n_levels, 0);
   for (int s = 1; s < lat.n_levels; ++s) {
     const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
     const int64_t S = lat.level_off[s];
@@ -721,11 +725,39 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
       items = target_items;
     }
     int64_t chunks = std::max<int64_t>(1, (items + units - 1) / units);
-    chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / min_chunk));
-    int64_t len = (S + chunks - 1) / chunks;
-    chunks = (S + len - 1) / len;
-    n_chunks[s] = chunks;
-    chunk_len[s] = len;
+    if (persistent) {
+      // old sources [0, R) in cost-balanced chunks (about the same number of
+      // pairs per item, so no CTA falls behind the wavefront); the newest
+      // level's sources [R, S) in short chunks, because only they wait for
+      // level s-1 and so sit on the critical path
+      const int64_t R = s >= 2 ? lat.level_off[s - 1] : 0;
+      int64_t rlen, olen;
+      if (mode[s] == 0) {
+        const int64_t pairs = S * T;
+        const int64_t p_item = std::max<int64_t>(8192, pairs / std::max<int64_t>(1, 2 * target_items));
+        rlen = 16;
+        olen = std::max<int64_t>(16, p_item / 32);
+      } else {
+        rlen = kTileTargets;  // one source per thread
+        olen = kTileTargets;
+      }
+      const int64_t rc = (S - R + rlen - 1) / rlen;
+      const int64_t oc = (R + olen - 1) / olen;
+      olen = oc ? (R + oc - 1) / oc : 1;  // even split of the old region
+      chunk_base[s] = (int64_t)chunk_lo.size();
+      for (int64_t c = 0; c < oc; ++c) chunk_lo.push_back(std::min(R, c * olen));
+      for (int64_t c = 0; c < rc; ++c) chunk_lo.push_back(R + c * rlen);
+      chunk_lo.push_back(S);
+      chunks = oc + rc;
+      n_chunks[s] = chunks;
+      chunk_len[s] = 0;
+    } else {
+      chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / min_chunk));
+      int64_t len = (S + chunks - 1) / chunks;
+      chunks = (S + len - 1) / len;
+      n_chunks[s] = chunks;
+      chunk_len[s] = len;
+    }
     tile_base[s] = total_tiles;
     total_tiles += units;
     item_base[s] = total_items;
@@ -739,7 +771,9 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
     for (int s = 1; s < lat.n_levels; ++s) {
       part_base[s] = (int64_t)part_elems;
       const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
-      const int64_t rows = mode[s] == 0 ? ((T + 31) / 32) * 32 : T;  // mode 0: whole groups
+      // mode 0 merges 32-bit values with atomics (no partials); 64-bit
+      // values and mode 1 keep one partial per (target, cell, chunk)
+      const int64_t rows = mode[s] == 0 ? (vb == 32 ? 0 : ((T + 31) / 32) * 32) : T;
       part_elems += (size_t)(n_chunks[s] * C * rows);
     }
   }
@@ -757,6 +791,14 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
     PP.n_levels = lat.n_levels;
     int64_t* lvl_d = ctx.get_t<int64_t>("pp.level_off", lat.level_off.size());
     int64_t* nch_d = ctx.get_t<int64_t>("pp.n_chunks", n_chunks.size());
+    int64_t* clo_d = ctx.get_t<int64_t>("pp.chunk_lo", chunk_lo.size() + 1);
+    CK(cudaMemcpyAsync(clo_d, chunk_lo.data(), sizeof(int64_t) * chunk_lo.size(),
+                       cudaMemcpyHostToDevice, st));
+    int64_t* cb_d = ctx.get_t<int64_t>("pp.chunk_base", chunk_base.size());
+    CK(cudaMemcpyAsync(cb_d, chunk_base.data(), sizeof(int64_t) * chunk_base.size(),
+                       cudaMemcpyHostToDevice, st));
+    PP.chunk_lo = clo_d;
+    PP.chunk_base = cb_d;
     int64_t* cl_d = ctx.get_t<int64_t>("pp.chunk_len", chunk_len.size());
     int64_t* tb_d0 = ctx.get_t<int64_t>("pp.tile_base", tile_base.size());
     CK(cudaMemcpyAsync(lvl_d, lat.level_off.data(), sizeof(int64_t) * lat.level_off.size(),
@@ -815,8 +857,33 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
       const int64_t left = std::chrono::duration_cast<std::chrono::nanoseconds>(deadline - Clock::now()).count();
       PP.deadline_ns = (int64_t)gt + std::max<int64_t>(left, 1);
     }
+    PP.keys = ctx.get_t<unsigned long long>("pp.keys", vb == 32 ? (size_t)I * C : 1);
+    if (vb == 32) CK(cudaMemsetAsync(PP.keys, 0xff, sizeof(unsigned long long) * I * C, st));
+    const char* trace_file = std::getenv("DSG_TRACE_FILE");
+    PP.trace = nullptr;
+    if (trace_file && *trace_file) {
+      PP.trace = ctx.get_t<uint64_t>("pp.trace", (size_t)total_items * 4);
+      CK(cudaMemsetAsync(PP.trace, 0, sizeof(uint64_t) * total_items * 4, st));
+    }
     CK(cudaEventRecord(ev_desc, st));
     launch_persistent(LL, PP, st, &pinfo);
+    if (PP.trace) {
+      // debug trace: header, per-level plan, per-item timestamps
+      std::vector<uint64_t> tr((size_t)total_items * 4);
+      CK(cudaMemcpyAsync(tr.data(), PP.trace, sizeof(uint64_t) * tr.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (FILE* f = std::fopen(trace_file, "wb")) {
+        int64_t hdr[4] = {lat.n_levels, total_items, pinfo.blocks, 0};
+        std::fwrite(hdr, sizeof hdr, 1, f);
+        std::fwrite(lat.level_off.data(), sizeof(int64_t), lat.level_off.size(), f);
+        std::fwrite(item_base.data(), sizeof(int64_t), item_base.size(), f);
+        std::fwrite(n_chunks.data(), sizeof(int64_t), n_chunks.size(), f);
+        std::vector<int64_t> m64(mode.begin(), mode.end());
+        std::fwrite(m64.data(), sizeof(int64_t), m64.size(), f);
+        std::fwrite(tr.data(), sizeof(uint64_t), tr.size(), f);
+        std::fclose(f);
+      }
+    }
     if (pinfo.launch_error != 0)
       throw Fail{DSG_CUDA_ERROR, std::string("cooperative launch failed: ") +
                                      cudaGetErrorString((cudaError_t)pinfo.launch_error)};

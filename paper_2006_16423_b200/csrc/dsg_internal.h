@@ -133,7 +133,9 @@ struct PersistPlan {
   const int64_t* level_off;  // [n_levels + 1]
   const int32_t* mode;       // [n_levels] 0: lanes own targets, 1: lanes own sources
   const int64_t* n_chunks;   // [n_levels] source chunks per target (group)
-  const int64_t* chunk_len;  // [n_levels]
+  const int64_t* chunk_len;  // [n_levels] (unused by the dataflow kernel)
+  const int64_t* chunk_lo;   // chunk boundaries: level s chunk c covers
+  const int64_t* chunk_base; //   [chunk_lo[b+c], chunk_lo[b+c+1]), b = chunk_base[s]
   const int64_t* tile_base;  // [n_levels] prefix of arrival counters over levels
   const int64_t* item_base;  // [n_levels + 1] prefix of work items over levels
   const int64_t* part_base;  // [n_levels] offset of each level's partials
@@ -144,6 +146,9 @@ struct PersistPlan {
   int* stop;                 // deadline reached / abort
   int* err;                  // watchdog fired
   int64_t deadline_ns;       // %globaltimer deadline, 0 = none
+  uint64_t* trace;           // optional [total_items][4] timestamps (DSG_TRACE_FILE)
+  unsigned long long* keys;  // [I][C] packed (value^sign, arg) for mode-0 merges of
+                             // 32-bit values; 0xff.. = no candidate
 };
 
 struct PersistInfo {

@@ -43,6 +43,10 @@ constexpr int kWarps = kTileTargets / 32;  // warps per CTA (4)
 constexpr int kGroup = 32;                 // targets per mode-0 item
 constexpr uint64_t kWatchdogNs = 20000000000ull;
 
+__device__ __forceinline__ unsigned long long pack_key(int32_t v, int32_t arg) {
+  return ((unsigned long long)((uint32_t)v ^ 0x80000000u) << 32) | (uint32_t)arg;
+}
+
 template <typename V>
 __device__ __forceinline__ void warp_argmin(V& v, int32_t& g) {
 #pragma unroll
@@ -114,6 +118,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
                                                                          const PersistPlan p) {
   constexpr V INF = VTraits<V>::INF;
   constexpr bool kGeneric = LP1 == 0;
+  constexpr bool kKeys = sizeof(V) == 4;
   constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
   constexpr int TS = kGroup;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -140,17 +145,18 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
     const int64_t t_lo = p.level_off[s], t_hi = p.level_off[s + 1];
     const int64_t T = t_hi - t_lo;
     const int64_t chunks = p.n_chunks[s];
-    const int64_t clen = p.chunk_len[s];
     const int mode = p.mode[s];
     const size_t pb = (size_t)p.part_base[s];
     const int64_t it = gi - p.item_base[s];
     const int64_t units = mode == 0 ? (T + TS - 1) / TS : T;
     const int64_t unit = it % units;
     const int64_t chunk = it / units;
-    const int64_t s0 = chunk * clen;
-    const int64_t s1 = min(s0 + clen, t_lo);
+    const int64_t s0 = p.chunk_lo[p.chunk_base[s] + chunk];
+    const int64_t s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
     // sources [s0, s1) must be final
+    const uint64_t tr0 = p.trace ? globaltimer() : 0;
     if (!wait_levels(p, p.level_of[s0], p.level_of[s1 - 1])) break;
+    const uint64_t tr1 = p.trace ? globaltimer() : 0;
     if (blockIdx.x == 0 && tid == 0 && p.deadline_ns && globaltimer() > (uint64_t)p.deadline_ns)
       atomicExch(p.stop, 1);
 
@@ -196,8 +202,25 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
           }
         }
       }
-      if (warp == 0)
-        write_partial<V, CMAX, kGeneric, TS>(a, pb, unit, chunk, chunks, lane, best, barg, colv, cola);
+      if (warp == 0) {
+        if (kKeys) {
+          // 32-bit values: one packed (value, arg) atomicMin per cell — the
+          // L2 merges the chunks, the finalizer reads C words per target
+          if (x.active) {
+            unsigned long long* key = p.keys + (size_t)x.t * C;
+            if (!kGeneric) {
+#pragma unroll
+              for (int c = 0; c < CMAX; ++c)
+                if (c < C && best[c] != INF) atomicMin(key + c, pack_key((int32_t)best[c], barg[c]));
+            } else {
+              for (int c = 0; c < C; ++c)
+                if (colv[c * TS] != INF) atomicMin(key + c, pack_key((int32_t)colv[c * TS], cola[c * TS]));
+            }
+          }
+        } else {
+          write_partial<V, CMAX, kGeneric, TS>(a, pb, unit, chunk, chunks, lane, best, barg, colv, cola);
+        }
+      }
       n_act = min((int64_t)TS, T - unit * TS);
     } else {
       // ------------------------------------ lanes own sources
@@ -245,6 +268,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
     }
     // arrival: the last chunk of this unit finalizes its targets
     __syncthreads();
+    const uint64_t tr2 = p.trace ? globaltimer() : 0;
     if (tid == 0) {
       __threadfence();  // cumulative release of this CTA's partials
       s_last = atomicAdd(p.tile_count + p.tile_base[s] + unit, 1u) == chunks - 1;
@@ -253,7 +277,22 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
     __syncthreads();
     if (s_last) {
       const int64_t tl0 = mode == 0 ? unit * TS : unit;
-      if (mode == 0) {
+      if (mode == 0 && kKeys) {
+        for (int r = tid; r < C * TS; r += kTileTargets) {
+          const int c = r / TS, tl_local = r % TS;
+          V v = INF;
+          int32_t g = -1;
+          if (tl_local < n_act) {
+            const unsigned long long k = __ldcg(p.keys + (size_t)(t_lo + tl0 + tl_local) * C + c);
+            if (k != ~0ull) {
+              v = (V)(int32_t)((uint32_t)(k >> 32) ^ 0x80000000u);
+              g = (int32_t)(uint32_t)(k & 0xffffffffull);
+            }
+          }
+          m_val[r] = v;
+          m_arg[r] = g;
+        }
+      } else if (mode == 0) {
         // lanes = the group's targets, warps over chunks (coalesced
         // [chunk][cell][lane] lines), then the 4 warps merge in shared memory
         const size_t ubase = pb + (size_t)unit * chunks * C * TS + lane;
@@ -328,6 +367,13 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
       }
     }
     __syncthreads();
+    if (p.trace && tid == 0) {
+      uint64_t* tr = p.trace + gi * 4;
+      tr[0] = tr0;
+      tr[1] = tr1;
+      tr[2] = tr2;
+      tr[3] = globaltimer() | (s_last ? (1ull << 63) : 0ull);
+    }
   }
   for (int off = 16; off > 0; off >>= 1)
     nested_total += __shfl_xor_sync(0xffffffffu, nested_total, off);

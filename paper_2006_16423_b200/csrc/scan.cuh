@@ -279,28 +279,37 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
         }
       }
     } else {
+      // generic cells: batches of 8 so the source-row loads are all in
+      // flight before the shared-memory read-modify-writes
       const int lp1 = a.L + 1;
-      for (int k = 0; k <= a.K; ++k) {
-        for (int l = 0; l <= a.L; ++l) {
-          const int c = k * lp1 + l;
-          V b = colv[c * CS];
-          int32_t g = cola[c * CS];
-          if (k >= 1) {
-            const V v = vmax(sdp[c - lp1], acc);
-            if (v < b) {
-              b = v;
+      constexpr int B = 8;
+      for (int c0 = 0; c0 < C; c0 += B) {
+        V va[B], vc[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+          const int c = c0 + i;
+          va[i] = (c < C && c >= lp1) ? sdp[c - lp1] : INF;
+          vc[i] = (c < C && (c % lp1) != 0) ? sdp[c - 1] : INF;
+        }
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+          const int c = c0 + i;
+          if (c < C) {
+            V b = colv[c * CS];
+            int32_t g = cola[c * CS];
+            const V v1 = vmax(va[i], acc);
+            if (v1 < b) {
+              b = v1;
               g = aa;
             }
-          }
-          if (l >= 1) {
-            const V v = vmax(sdp[c - 1], cpu);
-            if (v < b) {
-              b = v;
+            const V v2 = vmax(vc[i], cpu);
+            if (v2 < b) {
+              b = v2;
               g = ac;
             }
+            colv[c * CS] = b;
+            cola[c * CS] = g;
           }
-          colv[c * CS] = b;
-          cola[c * CS] = g;
         }
       }
     }
