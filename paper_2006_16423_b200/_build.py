@@ -83,6 +83,8 @@ def build_oracle(ref: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "-j", jobs, "all"], check=True)
     if ref and os.path.isdir("/root/reference/proj/src"):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "-j", jobs, "ref"], check=True)
+        # the reference's own test programs linked against the B200 drop-in
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "integration"), "-j", jobs], check=True)
 
 
 if __name__ == "__main__":

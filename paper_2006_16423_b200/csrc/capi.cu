@@ -203,6 +203,10 @@ struct Prepared {
   int interleave = 0;
   bool has_bw = false;
   bool inf_cpu_mem = false;  // deferred std::domain_error("subtracting infinity")
+  bool repl = false;         // solve_maxload_replicated
+  int repl_combine = 0;
+  int64_t repl_bn = 1, repl_bd = 1;
+  int repl_sign = 1;
 };
 
 void set_bit(std::vector<uint64_t>& m, int row, int W, int v) {
@@ -288,8 +292,16 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     }
     if (P.K + P.L < 1) throw Fail{DSG_INVALID, "need at least one device"};
     if (P.K < 0 || P.L < 0) throw Fail{DSG_INVALID, "negative device count"};
-    if (mode == DSG_MODE_REPLICATED)
-      throw Fail{DSG_UNSUPPORTED, "solve_maxload_replicated is not implemented on the device yet"};
+    if (mode == DSG_MODE_REPLICATED) {
+      const Q b = to_q(cfg->bandwidth);
+      if (b.inf) throw Fail{DSG_INVALID, "dividing by infinity"};
+      if (b.num == 0 && P.K >= 2) throw Fail{DSG_INVALID, "division by zero"};
+      P.repl = true;
+      P.repl_combine = cfg->replication_combine == DSG_REPL_MAX ? 1 : 0;
+      P.repl_bn = b.num < 0 ? -b.num : (b.num == 0 ? 1 : b.num);
+      P.repl_bd = b.den;
+      P.repl_sign = b.num < 0 ? -1 : 1;
+    }
     P.C = (P.K + 1) * (P.L + 1);
     P.training = mode == DSG_MODE_TRAINING;
     if (P.training) {
@@ -339,8 +351,21 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     qlim = to_q(cfg->memory_limit);
     lcm_in(qlim);
   }
-  P.D = (int64_t)D;
-  auto fx = [&](const Q& q) -> i128 { return q.inf ? 0 : (i128)q.num * (D / q.den); };
+  // replication divides by r <= K and by the bandwidth: scale every value by
+  // S = lcm(1..K) * |b_num| so base/r and (r-1)*mem*b_den/(r*b_num) stay
+  // exact integers (replicated_load, dp_solver.cpp:100-108)
+  i128 S = 1, lcmK = 1;
+  if (P.repl) {
+    for (int r = 2; r <= P.K; ++r) {
+      lcmK = lcmK / gcd64((int64_t)lcmK, r) * r;
+      if (lcmK > ((i128)1 << 40)) throw Fail{DSG_OVERFLOW, "replication scale overflow"};
+    }
+    S = lcmK * P.repl_bn;
+    if (S > ((i128)1 << 50)) throw Fail{DSG_OVERFLOW, "replication scale overflow"};
+  }
+  if (D * S > ((i128)1 << 62)) throw Fail{DSG_OVERFLOW, "common denominator overflow"};
+  P.D = (int64_t)(D * S);
+  auto fx = [&](const Q& q) -> i128 { return q.inf ? 0 : (i128)q.num * (D / q.den) * S; };
   P.cpu.assign(n, 0);
   P.acc.assign(n, 0);
   P.comm.assign(n, 0);
@@ -359,6 +384,13 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     P.mem[v] = (int64_t)s;
     P.unsup[v] = qa[v].inf;
     P.comminf[v] = qm[v].inf;
+  }
+  if (P.repl) {
+    // sync terms reach (K-1)/K * Σ|mem| * b_den / |b_num| on top of the loads
+    i128 mem_total = 0;
+    for (int v = 0; v < n; ++v) mem_total += absq((i128)P.mem[v]);
+    bound += 2 * (mem_total / P.repl_bn + 1) * P.repl_bd;
+    if (bound > ((i128)1 << 62)) throw Fail{DSG_OVERFLOW, "fixed-point weight sum overflow"};
   }
   P.value_bits = (bound < ((i128)1 << 30) && !(flags & DSG_FLAG_FORCE_INT64)) ? 32 : 64;
   if (!enumerate_only) {
@@ -656,6 +688,13 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   LL.mlim = P.mlim;
   LL.memcheck = P.memcheck;
   LL.interleave = P.interleave;
+  LL.repl = P.repl ? 1 : 0;
+  LL.repl_combine = P.repl_combine;
+  LL.repl_bn = P.repl_bn;
+  LL.repl_bd = P.repl_bd;
+  LL.repl_sign = P.repl_sign;
+  if ((i128)I * (K + 2) >= ((i128)1 << 31))
+    throw Fail{DSG_UNSUPPORTED, "ideal count x (accelerators + 2) exceeds the 31-bit argmin"};
   LL.abits = D.abits;
   LL.intbits = D.intbits;
   LL.pfx_cpu = D.pfx_cpu;
@@ -1017,8 +1056,8 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   int off = 0;
   for (int b = 0; b < tb.n_blocks; ++b) {
     dsg_block& blk = res->blocks[b];
-    blk.cpu = cpus[b];
-    blk.repl = 1;
+    blk.cpu = cpus[b] & 1;
+    blk.repl = cpus[b] >> 1;
     blk.offset = off;
     for (int w = 0; w < W; ++w) {
       uint64_t x = bbits[(size_t)b * W + w];

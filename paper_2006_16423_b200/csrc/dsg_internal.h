@@ -89,6 +89,11 @@ struct LevelLaunch {
   int64_t mlim;        // fixed point (clamped)
   int memcheck;
   int interleave;
+  int repl;            // replicated solve (dp_solver.cpp:100-108)
+  int repl_combine;    // 0 Sum, 1 Max
+  int64_t repl_bn;     // |bandwidth numerator|
+  int64_t repl_bd;     // bandwidth denominator
+  int repl_sign;       // sign of the bandwidth
   int64_t t_lo, t_hi;  // targets
   int64_t s_hi;        // sources [0, s_hi)
   int64_t n_chunks;

@@ -422,6 +422,7 @@ void run_variant(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, Pe
 template <typename V, bool TRAIN>
 void dispatch_cells(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
   const int lp1 = L.L + 1, kp1 = L.K + 1;
+  if (L.repl) return run_variant<V, 0, 0, TRAIN>(L, P, st, info);  // replication: generic cells
   if (lp1 == 1 && kp1 <= 9) return run_variant<V, 1, 9, TRAIN>(L, P, st, info);
   if (lp1 == 1 && kp1 <= 17) return run_variant<V, 1, 17, TRAIN>(L, P, st, info);
   if (lp1 == 2 && kp1 <= 9) return run_variant<V, 2, 9, TRAIN>(L, P, st, info);

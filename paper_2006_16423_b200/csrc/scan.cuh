@@ -253,9 +253,38 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     bool acc_ok = a.K > 0 && (x.un - r.unsup) == 0;
     if (acc_ok && a.memcheck) acc_ok = !((V)(x.mem - (V)r.mem) > mlim);
     if (acc_ok) acc = acc_block_cost<V, TRAIN, TS>(a, s, r, (V)(x.acc - (V)r.acc), x, tA, tInt);
-    // K4: min-max update, strict < keeps the smallest argmin
+    // K4: min-max update, strict < keeps the smallest argmin.  arg =
+    // src*(K+2) + r for an accelerator block on r replicas, + K+1 for a CPU
+    // block: within one source the reference tries r = 1..k, then the CPU
+    // (dp_solver.cpp:205-230), so the smallest arg is its first improvement.
     const V* sdp = dp + (size_t)s * C;
-    const int32_t aa = (int32_t)(2 * s), ac = aa + 1;
+    const int32_t base_arg = (int32_t)(s * (a.K + 2));
+    const int32_t aa = base_arg + 1, ac = base_arg + a.K + 1;
+    if (kGeneric && a.repl && acc != INF) {
+      // replication (dp_solver.cpp:100-108, 209-219): values are scaled so
+      // base/r and (r-1)*mem/(r*B) are exact integers (capi.cu)
+      const V mem_blk = (V)(x.mem - (V)r.mem);
+      const int lp1 = a.L + 1;
+      for (int rr = 1; rr <= a.K; ++rr) {
+        V load = acc;
+        if (rr > 1) {
+          const V divided = acc / (V)rr;
+          const V sync = (V)a.repl_sign * ((mem_blk / (V)a.repl_bn) * (V)a.repl_bd * (V)(rr - 1) / (V)rr);
+          load = a.repl_combine == 0 ? (V)(divided + sync) : vmax(divided, sync);
+        }
+        for (int k = rr; k <= a.K; ++k) {
+          for (int l = 0; l <= a.L; ++l) {
+            const int c = k * lp1 + l;
+            const V v = vmax(sdp[c - rr * lp1], load);
+            if (v < colv[c * CS] || (v == colv[c * CS] && base_arg + rr < cola[c * CS])) {
+              colv[c * CS] = v;
+              cola[c * CS] = base_arg + rr;
+            }
+          }
+        }
+      }
+      acc = INF;  // accelerator candidates done; the CPU ones below
+    }
     if (!kGeneric) {
 #pragma unroll
       for (int c = 0; c < CMAX; ++c) {

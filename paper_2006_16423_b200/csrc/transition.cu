@@ -152,16 +152,23 @@ __global__ void traceback_kernel(int64_t I, int K, int L, int W, const V* dp, co
       --l;
       continue;
     }
-    const int64_t prev = (int64_t)(b >> 1);
-    const int cpu = b & 1;
+    // arg = prev*(K+2) + r (accelerator block on r replicas) or + K+1 (CPU)
+    const int64_t prev = (int64_t)(b / (K + 2));
+    const int code = b % (K + 2);
+    const int cpu = code == K + 1;
+    const int repl = cpu ? 1 : code;
+    if ((!cpu && repl > k) || prev >= ord) {
+      out->status = 2;
+      return;
+    }
     ords[nb] = ord;
     prevs[nb] = prev;
-    cpus[nb] = cpu;
+    cpus[nb] = cpu | (repl << 1);
     for (int w = 0; w < W; ++w)
       block_bits[(size_t)nb * W + w] = abits[(size_t)ord * W + w] & ~abits[(size_t)prev * W + w];
     ++nb;
     if (cpu) --l;
-    else --k;
+    else k -= repl;
     ord = prev;
   }
   out->n_blocks = nb;
@@ -184,6 +191,7 @@ void launch_tile(const LevelLaunch& L, dim3 grid, cudaStream_t st) {
 template <typename V, bool TRAIN>
 void dispatch_tile(const LevelLaunch& L, dim3 grid, cudaStream_t st) {
   const int lp1 = L.L + 1, kp1 = L.K + 1;
+  if (L.repl) return launch_tile<V, 0, 0, TRAIN>(L, grid, st);  // replication: generic cells
   if (lp1 == 1 && kp1 <= 9) return launch_tile<V, 1, 9, TRAIN>(L, grid, st);
   if (lp1 == 1 && kp1 <= 17) return launch_tile<V, 1, 17, TRAIN>(L, grid, st);
   if (lp1 == 2 && kp1 <= 9) return launch_tile<V, 2, 9, TRAIN>(L, grid, st);

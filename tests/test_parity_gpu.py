@@ -176,8 +176,44 @@ def test_error_semantics(gpu):
     assert ei.value.limit == 1000
     with pytest.raises(ValueError, match="infinity"):
         device_solve(0, wl.Graph([wl.make_node(1, INF, 1, 0, 1)]), DeviceConfig(1, 1, 4))
-    with pytest.raises(Unsupported):
-        solver.solve_maxload_replicated(d4, DeviceConfig(2, 0, 4, bandwidth=1))
+    from paper_2006_16423_b200.errors import MissingBandwidth
+    with pytest.raises(MissingBandwidth):
+        solver.solve_maxload_replicated(d4, DeviceConfig(2, 0, 4))
+    with pytest.raises(ValueError, match="inference graph"):
+        solver.solve_maxload_replicated(wl.mirror_training(d4), DeviceConfig(2, 0, 4, bandwidth=1))
+
+
+def test_replication_known_answers(gpu):
+    """test_dp_solver.cpp:145-164: one block of base 10, weight 4."""
+    from paper_2006_16423_b200.graph import ReplicationCombine
+    g = wl.Graph([wl.make_node(1, 10, 10, 0, 4)])
+    s = solver.solve_maxload_replicated(g, DeviceConfig(2, 0, 4, bandwidth=1))
+    assert s.objective_value == 7 and s.replication == {"acc1": 2}
+    s = solver.solve_maxload_replicated(
+        g, DeviceConfig(2, 0, 4, bandwidth=1, replication_combine=ReplicationCombine.Max))
+    assert s.objective_value == 5
+    assert solver.solve_maxload_replicated(g, DeviceConfig(1, 0, 4, bandwidth=1)).objective_value == 10
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_replication_matches_oracle(gpu, seed):
+    from fractions import Fraction
+    from paper_2006_16423_b200.graph import ReplicationCombine
+    g, cfg = random_dag(7000 + seed, n_lo=4, n_hi=12)
+    cfg.accelerators = 1 + seed % 5
+    cfg.bandwidth = [Fraction(1), Fraction(3, 2), Fraction(1000000), Fraction(1, 7)][seed % 4]
+    cfg.replication_combine = ReplicationCombine(seed % 2)
+    try:
+        want = ob.dp("port", 2, g, cfg).objective
+    except InfeasibleError:
+        want = INF
+    try:
+        split = solver.solve_maxload_replicated(g, cfg)
+        got = split.objective_value
+        assert not verify_split(g, cfg, split, training=False)
+    except InfeasibleError:
+        got = INF
+    assert got == want
 
 
 def test_deadline(gpu):
