@@ -211,6 +211,38 @@ dsg_session* dsg_session_create(int32_t mode, const dsg_graph* graph, const dsg_
 int dsg_session_run(dsg_session* session, dsg_result* result);
 void dsg_session_destroy(dsg_session* session);
 
+/* Multi-GPU wavefront (one process per GPU).  Every rank
+ * creates a session for the same graph, then:
+ *   dsg_session_shard_prepare(s, rank, world, &mine)   lattice + tables, export IPC handles
+ *   <all-gather the world handles in rank order>       (e.g. torch.distributed)
+ *   dsg_session_shard_attach(s, all)                   open the peers' tables (NVLink P2P)
+ * and per solve:
+ *   dsg_session_shard_reset(s)  ->  <barrier across ranks>  ->  dsg_session_run(s)
+ *   ->  <barrier across ranks>.
+ * Rank r owns the target units u with u % world == r; its finalizers store
+ * the finished dp rows into every rank's table and bump every rank's level
+ * counter, so no host-side collective runs per level.  Rank 0 returns the
+ * split; the others return status and their transition counts. */
+#define DSG_MAX_SHARDS 64
+typedef struct dsg_shard_handle {
+  int32_t rank;
+  int32_t device;
+  int64_t n_ideals;
+  uint8_t dp[64];   /* cudaIpcMemHandle_t of the dp table */
+  uint8_t bp[64];   /* ... back pointers */
+  uint8_t ctl[64];  /* ... control words (level counters at +32) */
+} dsg_shard_handle;
+
+int dsg_session_shard_prepare(dsg_session* session, int32_t rank, int32_t world,
+                              dsg_shard_handle* handle_out, dsg_result* status_out);
+int dsg_session_shard_attach(dsg_session* session, const dsg_shard_handle* all_handles,
+                             dsg_result* status_out);
+int dsg_session_shard_reset(dsg_session* session, dsg_result* status_out);
+/* Re-flatten and re-upload a (same-shaped) graph into a session: the
+ * host->device leg of an end-to-end solve without re-attaching peers. */
+int dsg_session_reload(dsg_session* session, const dsg_graph* graph, const dsg_config* config,
+                       dsg_result* status_out);
+
 void dsg_default_options(dsg_options* options);
 const char* dsg_version(void);
 /* Number of CUDA devices visible (0 if none); never fails. */

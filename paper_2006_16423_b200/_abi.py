@@ -137,6 +137,17 @@ class dsg_ideals(C.Structure):
     ]
 
 
+class dsg_shard_handle(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32),
+        ("device", C.c_int32),
+        ("n_ideals", C.c_int64),
+        ("dp", C.c_uint8 * 64),
+        ("bp", C.c_uint8 * 64),
+        ("ctl", C.c_uint8 * 64),
+    ]
+
+
 def bind(lib: C.CDLL, prefix: str) -> None:
     """Declare argtypes for the <prefix>_dp_solve / _enumerate_ideals family."""
     solve = getattr(lib, f"{prefix}_dp_solve")

@@ -81,6 +81,7 @@ struct DeviceCtx {
   void* pinned = nullptr;
   size_t pinned_cap = 0;
   int64_t h2d_bytes = 0, d2h_bytes = 0;  // per solve, for the bench's e2e record
+  cudaEvent_t ev_end = nullptr;
 
   void* get(const std::string& name, size_t bytes) {
     if (bytes == 0) bytes = 8;
@@ -533,7 +534,7 @@ struct Lattice {
 };
 
 Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, int64_t budget,
-                         bool hash_mode) {
+                         bool hash_mode, const std::string& pfx) {
   const int W = P.W;
   const int64_t budget_eff = std::max<int64_t>(budget, 1);
   int64_t cap = std::min<int64_t>(budget_eff + 1, std::max<int64_t>(4096, (int64_t(1) << 22) / W));
@@ -587,7 +588,7 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
     lat.n_levels = st.n_levels;
     lat.level_off.resize(lat.n_levels + 1);
     D2H(lat.level_off.data(), lvl_d, sizeof(int64_t) * (lat.n_levels + 1));
-    lat.sbits = ctx.get_t<uint64_t>("lat.sbits", (size_t)lat.I * W);
+    lat.sbits = ctx.get_t<uint64_t>(pfx + "lat.sbits", (size_t)lat.I * W);
     launch_lex_rank(W, lat.I, L.bits, L.level_of, lvl_d, lat.sbits, ctx.stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx.stream));
@@ -601,54 +602,83 @@ void fill_msg(char* dst, const std::string& s) {
   dst[255] = 0;
 }
 
+// one end-of-pipeline event per device context (phase 2 records it)
+cudaEvent_t pl_ev_end(DeviceCtx& ctx) {
+  if (!ctx.ev_end) CK(cudaEventCreate(&ctx.ev_end));
+  return ctx.ev_end;
+}
+
+struct Pipeline;
+void write_trace(DeviceCtx& ctx, const Pipeline& pl, const char* path);
+
 // ------------------------------------------------------------ solve
-// The device pipeline for an uploaded graph: enumeration -> descriptors ->
-// level loop -> traceback.  Only control-sized values cross PCIe (status,
-// level offsets, table totals, the result blocks).
-void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_options* opt,
-                dsg_result* res, Clock::time_point t0) {
+// Phase 1: lattice, descriptors, chunk plan, DP buffers.  Phase 2: reset, all
+// DP levels (one persistent cooperative launch), traceback.  Every solve runs
+// both phases (nothing is cached between solves); buffers are named per
+// session so their addresses stay stable across solves of the same graph —
+// which is what lets a sharded session (one process per GPU) exchange CUDA
+// IPC handles of its dp / bp / level-counter buffers once and then run every
+// solve with the finalizers of all ranks storing rows into all ranks' tables
+// over NVLink (persistent.cu).
+struct Pipeline {
+  std::string pfx;
+  Lattice lat;
+  int64_t I = 0;
+  DescribeLaunch D{};
+  LevelLaunch LL{};
+  PersistPlan PP{};
+  PersistInfo pinfo{};
+  bool persistent = true;
+  std::vector<int64_t> n_chunks, chunk_len, item_base;
+  std::vector<int32_t> mode;
+  int64_t total_tiles = 0, total_items = 0;
+  unsigned* ctl = nullptr;  // [0] stop, [1] err, [32 + s] level s done
+  size_t ctl_words = 0;
+  int rank = 0, world = 1;
+  std::vector<void*> peer_dp;
+  std::vector<int32_t*> peer_bp;
+  std::vector<unsigned*> peer_done;
+  std::vector<void*> ipc_opened;
+  double t_enum_ms = 0, t_desc_ms = 0;
+};
+
+void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_options* opt,
+            Pipeline& pl) {
   const int flags = opt->flags;
   cudaStream_t st = ctx.stream;
-  const bool timing = (flags & DSG_TIME_KERNELS_FLAG) != 0;
-  const bool has_deadline = opt->deadline_seconds > 0;
-  const auto deadline = t0 + std::chrono::nanoseconds((int64_t)(opt->deadline_seconds * 1e9));
+  const std::string& pfx = pl.pfx;
   const int W = P.W, K = P.K, Lc = P.L, C = P.C;
   const int vb = P.value_bits;
   const size_t vsz = vb == 32 ? 4 : 8;
-  const int64_t launches0 = dsg::g_launches.load();
-  ctx.d2h_bytes = 0;
-  cudaEvent_t ev_start, ev_end;
-  CK(cudaEventCreate(&ev_start));
-  CK(cudaEventCreate(&ev_end));
-  CK(cudaEventRecord(ev_start, st));
   const auto t1 = Clock::now();
-  Lattice lat = enumerate_device(ctx, P, dg, opt->ideal_budget, (flags & DSG_FLAG_HASH_ENUM) != 0);
-  res->n_ideals = lat.I;
-  res->n_levels = lat.n_levels;
-  res->t_enumerate_ms = ms_since(t1);
+  pl.lat = enumerate_device(ctx, P, dg, opt->ideal_budget, (flags & DSG_FLAG_HASH_ENUM) != 0, pfx);
+  const Lattice& lat = pl.lat;
+  pl.t_enum_ms = ms_since(t1);
   if (P.inf_cpu_mem) throw Fail{DSG_INVALID, "subtracting infinity"};
   const int64_t I = lat.I;
+  pl.I = I;
 
   // ---- descriptors
   const auto t2 = Clock::now();
-  DescribeLaunch D{};
+  DescribeLaunch& D = pl.D;
+  D = DescribeLaunch{};
   D.g = dg.g;
   D.training = P.training ? 1 : 0;
   D.has_bw = (P.training && P.has_bw) ? 1 : 0;
   D.value_bits = vb;
   D.I = I;
   D.sbits = lat.sbits;
-  D.abits = ctx.get_t<uint64_t>("d.abits", (size_t)I * W);
-  D.intbits = ctx.get_t<uint64_t>("d.intbits", P.training ? (size_t)I * W : 1);
-  D.pfx_cpu = ctx.get("d.cpu", I * vsz);
-  D.pfx_acc = ctx.get("d.acc", I * vsz);
-  D.pfx_mem = ctx.get("d.mem", I * vsz);
-  D.unsup = ctx.get_t<int32_t>("d.unsup", I);
-  D.fw = ctx.get("d.fw", I * vsz);
-  D.fwinf = ctx.get_t<int32_t>("d.fwinf", I);
-  D.upset = ctx.get_t<uint8_t>("d.upset", I);
-  D.srec = ctx.get_t<SrcRec>("d.srec", I);
-  D.counts = ctx.get_t<int64_t>("d.counts", (size_t)kNumCounts * (I + 1));
+  D.abits = ctx.get_t<uint64_t>(pfx + "d.abits", (size_t)I * W);
+  D.intbits = ctx.get_t<uint64_t>(pfx + "d.intbits", P.training ? (size_t)I * W : 1);
+  D.pfx_cpu = ctx.get(pfx + "d.cpu", I * vsz);
+  D.pfx_acc = ctx.get(pfx + "d.acc", I * vsz);
+  D.pfx_mem = ctx.get(pfx + "d.mem", I * vsz);
+  D.unsup = ctx.get_t<int32_t>(pfx + "d.unsup", I);
+  D.fw = ctx.get(pfx + "d.fw", I * vsz);
+  D.fwinf = ctx.get_t<int32_t>(pfx + "d.fwinf", I);
+  D.upset = ctx.get_t<uint8_t>(pfx + "d.upset", I);
+  D.srec = ctx.get_t<SrcRec>(pfx + "d.srec", I);
+  D.counts = ctx.get_t<int64_t>(pfx + "d.counts", (size_t)kNumCounts * (I + 1));
   CK(cudaMemsetAsync(D.counts, 0, sizeof(int64_t) * kNumCounts * (I + 1), st));
   launch_describe(D, false, st);
   launch_scan_counts(D.counts, I, kNumCounts, st);
@@ -659,24 +689,20 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   CK(cudaGetLastError());
   if (totals[kCntF] > INT32_MAX || totals[kCntN] > INT32_MAX || totals[kCntLItems] > INT32_MAX)
     throw Fail{DSG_UNSUPPORTED, "frontier tables exceed 2^31 entries"};
-  D.chunks = ctx.get_t<FChunk>("d.chunks", totals[kCntChunks]);
-  D.fpool = ctx.get("d.fpool", totals[kCntF] * vsz);
-  D.nitems = ctx.get_t<NItem>("d.nitems", totals[kCntN]);
-  D.pitems = ctx.get_t<PItem>("d.pitems", totals[kCntP]);
-  D.lentries = ctx.get_t<LEntry>("d.lentries", totals[kCntL]);
-  D.litems = ctx.get_t<MaskItem>("d.litems", totals[kCntLItems]);
+  D.chunks = ctx.get_t<FChunk>(pfx + "d.chunks", totals[kCntChunks]);
+  D.fpool = ctx.get(pfx + "d.fpool", totals[kCntF] * vsz);
+  D.nitems = ctx.get_t<NItem>(pfx + "d.nitems", totals[kCntN]);
+  D.pitems = ctx.get_t<PItem>(pfx + "d.pitems", totals[kCntP]);
+  D.lentries = ctx.get_t<LEntry>(pfx + "d.lentries", totals[kCntL]);
+  D.litems = ctx.get_t<MaskItem>(pfx + "d.litems", totals[kCntLItems]);
   launch_describe(D, true, st);
   CK(cudaGetLastError());
+  pl.t_desc_ms = ms_since(t2);
 
-  // ---- level loop
-  void* dp = ctx.get("dp.values", (size_t)I * C * vsz);
-  int32_t* bp = ctx.get_t<int32_t>("dp.bp", (size_t)I * C);
-  unsigned long long* pairs_d = ctx.get_t<unsigned long long>("dp.pairs", 1);
-  CK(cudaMemsetAsync(pairs_d, 0, sizeof(unsigned long long), st));
-  launch_init_empty(vb, K, Lc, dp, bp, st);
-
-  const bool persistent = !(flags & DSG_FLAG_LEVEL_LAUNCH);
-  LevelLaunch LL{};
+  // ---- DP tables and launch parameters
+  pl.persistent = !(flags & DSG_FLAG_LEVEL_LAUNCH);
+  LevelLaunch& LL = pl.LL;
+  LL = LevelLaunch{};
   LL.value_bits = vb;
   LL.training = P.training ? 1 : 0;
   LL.has_bw = D.has_bw;
@@ -718,216 +744,243 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   LL.bw_from = dg.g.bw_from;
   LL.bw_to = dg.g.bw_to;
   LL.n_nodes = P.n;
-  LL.dp = dp;
-  LL.bp = bp;
-  LL.pair_counter = pairs_d;
+  LL.dp = ctx.get(pfx + "dp.values", (size_t)I * C * vsz);
+  LL.bp = ctx.get_t<int32_t>(pfx + "dp.bp", (size_t)I * C);
+  LL.pair_counter = ctx.get_t<unsigned long long>(pfx + "dp.pairs", 1);
 
-  // ---- chunk plan: (target tile x source chunk) work items per level
-  PersistInfo pinfo{};
-  if (persistent) {
-    query_persistent(LL, &pinfo);
-    if (opt->reserved > 0) pinfo.blocks = std::min(pinfo.blocks, opt->reserved);
+  // ---- chunk plan
+  pl.pinfo = PersistInfo{};
+  if (pl.persistent) {
+    query_persistent(LL, &pl.pinfo);
+    if (opt->reserved > 0) pl.pinfo.blocks = std::min(pl.pinfo.blocks, opt->reserved);
   }
   const int64_t target_items =
-      persistent ? std::max(1, pinfo.blocks) : (int64_t)ctx.sm_count * 8;
-  std::vector<int64_t> n_chunks(lat.n_levels, 1), chunk_len(lat.n_levels, 1),
-      tile_base(lat.n_levels, 0);
-  std::vector<int32_t> mode(lat.n_levels, 0);
-  std::vector<int64_t> item_base(lat.n_levels + 1, 0), part_base(lat.n_levels, 0);
-  size_t part_elems = 1;
-  int64_t total_tiles = 0, total_items = 0;
-  // persistent, mode 0: (32-target group, chunk) CTA items whose 4 warps
-  // split the chunk (chunks down to 4 sources); mode 1 (few targets): (target,
-  // chunk) warp items with one source per lane.  Per-level path: 128-target
-  // tiles x chunks of >= 16 sources.
-  const int64_t kSmallLevel = 16;
-  // persistent: explicit chunk boundaries per level.  Sources of the newest
-  // level (s-1) get small chunks, ordered last, because only they wait for
-  // the previous level; older sources get large chunks that start early.
+      pl.persistent ? std::max(1, pl.pinfo.blocks) : (int64_t)ctx.sm_count * 8;
+  pl.n_chunks.assign(lat.n_levels, 1);
+  pl.chunk_len.assign(lat.n_levels, 1);
+  pl.mode.assign(lat.n_levels, 0);
+  pl.item_base.assign(lat.n_levels + 1, 0);
+  std::vector<int64_t> tile_base(lat.n_levels, 0), part_base(lat.n_levels, 0);
   std::vector<int64_t> chunk_lo, chunk_base(lat.n_levels, 0);
+  size_t part_elems = 1;
+  pl.total_tiles = 0;
+  pl.total_items = 0;
+  // persistent, mode 0 (>= 16 targets): (32-target group, chunk) CTA items
+  // whose 4 warps split the chunk; mode 1 (< 16 targets): (target, chunk)
+  // items with one source per thread.  Old sources [0, R) in cost-balanced
+  // chunks (no CTA falls behind the wavefront); the newest level's sources
+  // [R, S) in short chunks, ordered last, because only they wait for level
+  // s-1 and so sit on the critical path.  Per-level path: 128-target tiles
+  // x uniform chunks of >= 16 sources.
+  const int64_t kSmallLevel = 16;
   for (int s = 1; s < lat.n_levels; ++s) {
     const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
     const int64_t S = lat.level_off[s];
-    int64_t units, min_chunk, items;
-    if (!persistent) {
+    int64_t units, min_chunk;
+    if (!pl.persistent) {
       units = (T + kTileTargets - 1) / kTileTargets;
       min_chunk = 16;
-      items = target_items;
     } else if (T < kSmallLevel) {
-      mode[s] = 1;
+      pl.mode[s] = 1;
       units = T;
-      min_chunk = kTileTargets;  // one source per thread
-      items = target_items;
+      min_chunk = kTileTargets;
     } else {
       units = (T + 31) / 32;
       min_chunk = 4;
-      items = target_items;
     }
-    int64_t chunks = std::max<int64_t>(1, (items + units - 1) / units);
-    if (persistent) {
-      // old sources [0, R) in cost-balanced chunks (about the same number of
-      // pairs per item, so no CTA falls behind the wavefront); the newest
-      // level's sources [R, S) in short chunks, because only they wait for
-      // level s-1 and so sit on the critical path
+    int64_t chunks = std::max<int64_t>(1, (target_items + units - 1) / units);
+    if (pl.persistent) {
       const int64_t R = s >= 2 ? lat.level_off[s - 1] : 0;
       int64_t rlen, olen;
-      if (mode[s] == 0) {
+      if (pl.mode[s] == 0) {
         const int64_t pairs = S * T;
         const int64_t p_item = std::max<int64_t>(8192, pairs / std::max<int64_t>(1, 2 * target_items));
         rlen = 16;
         olen = std::max<int64_t>(16, p_item / 32);
       } else {
-        rlen = kTileTargets;  // one source per thread
+        rlen = kTileTargets;
         olen = kTileTargets;
       }
       const int64_t rc = (S - R + rlen - 1) / rlen;
       const int64_t oc = (R + olen - 1) / olen;
-      olen = oc ? (R + oc - 1) / oc : 1;  // even split of the old region
+      olen = oc ? (R + oc - 1) / oc : 1;
       chunk_base[s] = (int64_t)chunk_lo.size();
       for (int64_t c = 0; c < oc; ++c) chunk_lo.push_back(std::min(R, c * olen));
       for (int64_t c = 0; c < rc; ++c) chunk_lo.push_back(R + c * rlen);
       chunk_lo.push_back(S);
       chunks = oc + rc;
-      n_chunks[s] = chunks;
-      chunk_len[s] = 0;
+      pl.chunk_len[s] = 0;
     } else {
       chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / min_chunk));
-      int64_t len = (S + chunks - 1) / chunks;
+      const int64_t len = (S + chunks - 1) / chunks;
       chunks = (S + len - 1) / len;
-      n_chunks[s] = chunks;
-      chunk_len[s] = len;
+      pl.chunk_len[s] = len;
     }
-    tile_base[s] = total_tiles;
-    total_tiles += units;
-    item_base[s] = total_items;
-    total_items += units * chunks;
+    pl.n_chunks[s] = chunks;
+    tile_base[s] = pl.total_tiles;
+    pl.total_tiles += units;
+    pl.item_base[s] = pl.total_items;
+    pl.total_items += units * chunks;
     part_elems = std::max(part_elems, (size_t)(chunks * C * T));
   }
-  item_base[lat.n_levels] = total_items;
-  if (persistent) {
-    // the dataflow kernel keeps every level's partials live at once
+  pl.item_base[lat.n_levels] = pl.total_items;
+  if (pl.persistent) {
+    // the dataflow kernel keeps every level's partials live at once; mode 0
+    // with 32-bit values merges through atomics instead
     part_elems = 1;
     for (int s = 1; s < lat.n_levels; ++s) {
       part_base[s] = (int64_t)part_elems;
       const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
-      // mode 0 merges 32-bit values with atomics (no partials); 64-bit
-      // values and mode 1 keep one partial per (target, cell, chunk)
-      const int64_t rows = mode[s] == 0 ? (vb == 32 ? 0 : ((T + 31) / 32) * 32) : T;
-      part_elems += (size_t)(n_chunks[s] * C * rows);
+      const int64_t rows = pl.mode[s] == 0 ? (vb == 32 ? 0 : ((T + 31) / 32) * 32) : T;
+      part_elems += (size_t)(pl.n_chunks[s] * C * rows);
     }
   }
-  LL.part_val = ctx.get("dp.part_val", part_elems * vsz);
-  LL.part_arg = ctx.get_t<int32_t>("dp.part_arg", part_elems);
+  LL.part_val = ctx.get(pfx + "dp.part_val", part_elems * vsz);
+  LL.part_arg = ctx.get_t<int32_t>(pfx + "dp.part_arg", part_elems);
+  if (!pl.persistent) return;
+
+  // ---- persistent plan (device copies)
+  PersistPlan& PP = pl.PP;
+  PP = PersistPlan{};
+  PP.n_levels = lat.n_levels;
+  auto up64 = [&](const std::string& name, const std::vector<int64_t>& v) {
+    int64_t* d = ctx.get_t<int64_t>(pfx + name, v.size() + 1);
+    CK(cudaMemcpyAsync(d, v.data(), sizeof(int64_t) * v.size(), cudaMemcpyHostToDevice, st));
+    ctx.h2d_bytes += (int64_t)(sizeof(int64_t) * v.size());
+    return (const int64_t*)d;
+  };
+  PP.level_off = up64("pp.level_off", lat.level_off);
+  PP.n_chunks = up64("pp.n_chunks", pl.n_chunks);
+  PP.chunk_len = up64("pp.chunk_len", pl.chunk_len);
+  PP.chunk_lo = up64("pp.chunk_lo", chunk_lo);
+  PP.chunk_base = up64("pp.chunk_base", chunk_base);
+  PP.tile_base = up64("pp.tile_base", tile_base);
+  PP.item_base = up64("pp.item_base", pl.item_base);
+  PP.part_base = up64("pp.part_base", part_base);
+  PP.total_items = pl.total_items;
+  {
+    int32_t* mode_d = ctx.get_t<int32_t>(pfx + "pp.mode", pl.mode.size());
+    CK(cudaMemcpyAsync(mode_d, pl.mode.data(), sizeof(int32_t) * pl.mode.size(),
+                       cudaMemcpyHostToDevice, st));
+    PP.mode = mode_d;
+    std::vector<int32_t> lvl_of((size_t)I);
+    for (int s = 0; s < lat.n_levels; ++s)
+      for (int64_t o = lat.level_off[s]; o < lat.level_off[s + 1]; ++o) lvl_of[o] = s;
+    int32_t* lo_d = ctx.get_t<int32_t>(pfx + "pp.level_of", (size_t)I);
+    CK(cudaMemcpyAsync(lo_d, lvl_of.data(), sizeof(int32_t) * I, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // host vectors are temporaries
+    PP.level_of = lo_d;
+  }
+  PP.tile_count = ctx.get_t<unsigned>(pfx + "pp.tile_count", (size_t)pl.total_tiles + 1);
+  pl.ctl_words = (size_t)lat.n_levels + 64;
+  pl.ctl = ctx.get_t<unsigned>(pfx + "pp.ctl", pl.ctl_words);
+  PP.stop = reinterpret_cast<int*>(pl.ctl);
+  PP.err = reinterpret_cast<int*>(pl.ctl + 1);
+  PP.done = pl.ctl + 32;
+  PP.keys = ctx.get_t<unsigned long long>(pfx + "pp.keys", vb == 32 ? (size_t)I * C : 1);
+  // peer tables: this GPU only, until a sharded session attaches its peers
+  if (pl.world == 1) {
+    pl.peer_dp.assign(1, LL.dp);
+    pl.peer_bp.assign(1, LL.bp);
+    pl.peer_done.assign(1, PP.done);
+  }
+  void** pd = ctx.get_t<void*>(pfx + "pp.peer_dp", pl.world);
+  int32_t** pb = ctx.get_t<int32_t*>(pfx + "pp.peer_bp", pl.world);
+  unsigned** pn = ctx.get_t<unsigned*>(pfx + "pp.peer_done", pl.world);
+  CK(cudaMemcpyAsync(pd, pl.peer_dp.data(), sizeof(void*) * pl.world, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(pb, pl.peer_bp.data(), sizeof(int32_t*) * pl.world, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(pn, pl.peer_done.data(), sizeof(unsigned*) * pl.world, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  PP.peer_dp = pd;
+  PP.peer_bp = pb;
+  PP.peer_done = pn;
+  PP.rank = pl.rank;
+  PP.world = pl.world;
+}
+
+void write_trace(DeviceCtx& ctx, const Pipeline& pl, const char* path) {
+  // debug trace (DSG_TRACE_FILE): header, per-level plan, per-item timestamps
+  std::vector<uint64_t> tr((size_t)pl.total_items * 4);
+  CK(cudaMemcpyAsync(tr.data(), pl.PP.trace, sizeof(uint64_t) * tr.size(), cudaMemcpyDeviceToHost,
+                     ctx.stream));
+  CK(cudaStreamSynchronize(ctx.stream));
+  if (FILE* f = std::fopen(path, "wb")) {
+    int64_t hdr[4] = {pl.lat.n_levels, pl.total_items, pl.pinfo.blocks, pl.rank};
+    std::fwrite(hdr, sizeof hdr, 1, f);
+    std::fwrite(pl.lat.level_off.data(), sizeof(int64_t), pl.lat.level_off.size(), f);
+    std::fwrite(pl.item_base.data(), sizeof(int64_t), pl.item_base.size(), f);
+    std::fwrite(pl.n_chunks.data(), sizeof(int64_t), pl.n_chunks.size(), f);
+    std::vector<int64_t> m64(pl.mode.begin(), pl.mode.end());
+    std::fwrite(m64.data(), sizeof(int64_t), m64.size(), f);
+    std::fwrite(tr.data(), sizeof(uint64_t), tr.size(), f);
+    std::fclose(f);
+  }
+}
+
+// Per-solve state: counters, merge keys, the empty ideal's dp row.
+void reset_tables(DeviceCtx& ctx, const Prepared& P, Pipeline& pl) {
+  cudaStream_t st = ctx.stream;
+  const int vb = P.value_bits;
+  CK(cudaMemsetAsync(pl.LL.pair_counter, 0, sizeof(unsigned long long), st));
+  launch_init_empty(vb, P.K, P.L, pl.LL.dp, pl.LL.bp, st);
+  if (pl.persistent) {
+    CK(cudaMemsetAsync(pl.PP.tile_count, 0, sizeof(unsigned) * (pl.total_tiles + 1), st));
+    CK(cudaMemsetAsync(pl.ctl, 0, sizeof(unsigned) * pl.ctl_words, st));
+    // level 0 (the empty ideal) is final before the launch
+    launch_fill_u32(pl.PP.done, 1, 1u, st);
+    if (vb == 32)
+      CK(cudaMemsetAsync(pl.PP.keys, 0xff, sizeof(unsigned long long) * pl.I * P.C, st));
+  }
+  CK(cudaStreamSynchronize(st));
+}
+
+void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline& pl,
+            dsg_result* res, Clock::time_point t0) {
+  const int flags = opt->flags;
+  cudaStream_t st = ctx.stream;
+  const bool timing = (flags & DSG_TIME_KERNELS_FLAG) != 0;
+  const bool has_deadline = opt->deadline_seconds > 0;
+  const auto deadline = t0 + std::chrono::nanoseconds((int64_t)(opt->deadline_seconds * 1e9));
+  const Lattice& lat = pl.lat;
+  const int64_t I = pl.I;
+  const int W = P.W, K = P.K, Lc = P.L, C = P.C;
+  const int vb = P.value_bits;
+  LevelLaunch& LL = pl.LL;
+  void* dp = LL.dp;
+  int32_t* bp = LL.bp;
 
   cudaEvent_t ev_desc, ev_dp;
   CK(cudaEventCreate(&ev_desc));
   CK(cudaEventCreate(&ev_dp));
-  std::vector<cudaEvent_t> kev;
-  std::vector<cudaEvent_t> dl_ev;
+  std::vector<cudaEvent_t> kev, dl_ev;
   const int kDeadlineStride = 8;
-  if (persistent) {
-    PersistPlan PP{};
-    PP.n_levels = lat.n_levels;
-    int64_t* lvl_d = ctx.get_t<int64_t>("pp.level_off", lat.level_off.size());
-    int64_t* nch_d = ctx.get_t<int64_t>("pp.n_chunks", n_chunks.size());
-    int64_t* clo_d = ctx.get_t<int64_t>("pp.chunk_lo", chunk_lo.size() + 1);
-    CK(cudaMemcpyAsync(clo_d, chunk_lo.data(), sizeof(int64_t) * chunk_lo.size(),
-                       cudaMemcpyHostToDevice, st));
-    int64_t* cb_d = ctx.get_t<int64_t>("pp.chunk_base", chunk_base.size());
-    CK(cudaMemcpyAsync(cb_d, chunk_base.data(), sizeof(int64_t) * chunk_base.size(),
-                       cudaMemcpyHostToDevice, st));
-    PP.chunk_lo = clo_d;
-    PP.chunk_base = cb_d;
-    int64_t* cl_d = ctx.get_t<int64_t>("pp.chunk_len", chunk_len.size());
-    int64_t* tb_d0 = ctx.get_t<int64_t>("pp.tile_base", tile_base.size());
-    CK(cudaMemcpyAsync(lvl_d, lat.level_off.data(), sizeof(int64_t) * lat.level_off.size(),
-                       cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(nch_d, n_chunks.data(), sizeof(int64_t) * n_chunks.size(),
-                       cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(cl_d, chunk_len.data(), sizeof(int64_t) * chunk_len.size(),
-                       cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(tb_d0, tile_base.data(), sizeof(int64_t) * tile_base.size(),
-                       cudaMemcpyHostToDevice, st));
-    PP.level_off = lvl_d;
-    PP.n_chunks = nch_d;
-    PP.chunk_len = cl_d;
-    PP.tile_base = tb_d0;
-    PP.tile_count = ctx.get_t<unsigned>("pp.tile_count", (size_t)total_tiles + 1);
-    CK(cudaMemsetAsync(PP.tile_count, 0, sizeof(unsigned) * (total_tiles + 1), st));
-    int32_t* mode_d = ctx.get_t<int32_t>("pp.mode", mode.size());
-    CK(cudaMemcpyAsync(mode_d, mode.data(), sizeof(int32_t) * mode.size(), cudaMemcpyHostToDevice, st));
-    PP.mode = mode_d;
-    int64_t* ib_d = ctx.get_t<int64_t>("pp.item_base", item_base.size());
-    CK(cudaMemcpyAsync(ib_d, item_base.data(), sizeof(int64_t) * item_base.size(),
-                       cudaMemcpyHostToDevice, st));
-    PP.item_base = ib_d;
-    int64_t* pb_d = ctx.get_t<int64_t>("pp.part_base", part_base.size());
-    CK(cudaMemcpyAsync(pb_d, part_base.data(), sizeof(int64_t) * part_base.size(),
-                       cudaMemcpyHostToDevice, st));
-    PP.part_base = pb_d;
-    PP.total_items = total_items;
-    {
-      std::vector<int32_t> lvl_of((size_t)I);
-      for (int s = 0; s < lat.n_levels; ++s)
-        for (int64_t o = lat.level_off[s]; o < lat.level_off[s + 1]; ++o) lvl_of[o] = s;
-      int32_t* lo_d = ctx.get_t<int32_t>("pp.level_of", (size_t)I);
-      CK(cudaMemcpyAsync(lo_d, lvl_of.data(), sizeof(int32_t) * I, cudaMemcpyHostToDevice, st));
-      CK(cudaStreamSynchronize(st));  // lvl_of is a stack temporary
-      PP.level_of = lo_d;
-    }
-    unsigned* ctl = ctx.get_t<unsigned>("pp.ctl", (size_t)lat.n_levels + 64);
-    CK(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * (lat.n_levels + 64), st));
-    PP.stop = reinterpret_cast<int*>(ctl);
-    PP.err = reinterpret_cast<int*>(ctl + 1);
-    PP.done = ctl + 32;
-    {
-      // level 0 (the empty ideal) is final before the launch
-      const unsigned one = 1;
-      CK(cudaMemcpyAsync(PP.done, &one, sizeof one, cudaMemcpyHostToDevice, st));
-      CK(cudaStreamSynchronize(st));
-    }
+  if (pl.persistent) {
+    PersistPlan& PP = pl.PP;
     PP.deadline_ns = 0;
     if (has_deadline) {
-      uint64_t* gt_d = ctx.get_t<uint64_t>("pp.gt", 1);
+      uint64_t* gt_d = ctx.get_t<uint64_t>(pl.pfx + "pp.gt", 1);
       uint64_t gt = 0;
       launch_read_globaltimer(gt_d, st);
       D2H(&gt, gt_d, sizeof gt);
       CK(cudaStreamSynchronize(st));
-      const int64_t left = std::chrono::duration_cast<std::chrono::nanoseconds>(deadline - Clock::now()).count();
+      const int64_t left =
+          std::chrono::duration_cast<std::chrono::nanoseconds>(deadline - Clock::now()).count();
       PP.deadline_ns = (int64_t)gt + std::max<int64_t>(left, 1);
     }
-    PP.keys = ctx.get_t<unsigned long long>("pp.keys", vb == 32 ? (size_t)I * C : 1);
-    if (vb == 32) CK(cudaMemsetAsync(PP.keys, 0xff, sizeof(unsigned long long) * I * C, st));
     const char* trace_file = std::getenv("DSG_TRACE_FILE");
     PP.trace = nullptr;
     if (trace_file && *trace_file) {
-      PP.trace = ctx.get_t<uint64_t>("pp.trace", (size_t)total_items * 4);
-      CK(cudaMemsetAsync(PP.trace, 0, sizeof(uint64_t) * total_items * 4, st));
+      PP.trace = ctx.get_t<uint64_t>(pl.pfx + "pp.trace", (size_t)pl.total_items * 4);
+      CK(cudaMemsetAsync(PP.trace, 0, sizeof(uint64_t) * pl.total_items * 4, st));
     }
     CK(cudaEventRecord(ev_desc, st));
-    launch_persistent(LL, PP, st, &pinfo);
-    if (PP.trace) {
-      // debug trace: header, per-level plan, per-item timestamps
-      std::vector<uint64_t> tr((size_t)total_items * 4);
-      CK(cudaMemcpyAsync(tr.data(), PP.trace, sizeof(uint64_t) * tr.size(), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (FILE* f = std::fopen(trace_file, "wb")) {
-        int64_t hdr[4] = {lat.n_levels, total_items, pinfo.blocks, 0};
-        std::fwrite(hdr, sizeof hdr, 1, f);
-        std::fwrite(lat.level_off.data(), sizeof(int64_t), lat.level_off.size(), f);
-        std::fwrite(item_base.data(), sizeof(int64_t), item_base.size(), f);
-        std::fwrite(n_chunks.data(), sizeof(int64_t), n_chunks.size(), f);
-        std::vector<int64_t> m64(mode.begin(), mode.end());
-        std::fwrite(m64.data(), sizeof(int64_t), m64.size(), f);
-        std::fwrite(tr.data(), sizeof(uint64_t), tr.size(), f);
-        std::fclose(f);
-      }
-    }
-    if (pinfo.launch_error != 0)
+    launch_persistent(LL, PP, st, &pl.pinfo);
+    if (pl.pinfo.launch_error != 0)
       throw Fail{DSG_CUDA_ERROR, std::string("cooperative launch failed: ") +
-                                     cudaGetErrorString((cudaError_t)pinfo.launch_error)};
+                                     cudaGetErrorString((cudaError_t)pl.pinfo.launch_error)};
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev_dp, st));
+    if (PP.trace) write_trace(ctx, pl, trace_file);
     int flags_h[2] = {0, 0};
     D2H(flags_h, PP.stop, sizeof flags_h);
     CK(cudaStreamSynchronize(st));
@@ -935,84 +988,78 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
     if (flags_h[0]) throw Fail{DSG_DEADLINE, "time limit reached"};
   } else {
     CK(cudaEventRecord(ev_desc, st));
-  }
-  res->persistent_blocks = persistent ? pinfo.blocks : 0;
-  for (int s = 1; s < lat.n_levels && !persistent; ++s) {
-    LL.t_lo = lat.level_off[s];
-    LL.t_hi = lat.level_off[s + 1];
-    LL.s_hi = lat.level_off[s];
-    LL.n_chunks = n_chunks[s];
-    LL.chunk_len = chunk_len[s];
-    if (timing) {
-      cudaEvent_t a, b;
-      CK(cudaEventCreate(&a));
-      CK(cudaEventCreate(&b));
-      CK(cudaEventRecord(a, st));
-      launch_transition(LL, st);
-      CK(cudaEventRecord(b, st));
-      kev.push_back(a);
-      kev.push_back(b);
-    } else {
-      launch_transition(LL, st);
-    }
-    launch_finalize(LL, st);
-    if (has_deadline && s % kDeadlineStride == 0) {
-      // keep at most two strides in flight so the clock tracks the device
-      cudaEvent_t e;
-      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      CK(cudaEventRecord(e, st));
-      dl_ev.push_back(e);
-      if (dl_ev.size() >= 2) {
-        CK(cudaEventSynchronize(dl_ev[dl_ev.size() - 2]));
-        if (Clock::now() > deadline) {
-          CK(cudaStreamSynchronize(st));
-          for (auto x : dl_ev) cudaEventDestroy(x);
-          for (auto x : kev) cudaEventDestroy(x);
-          cudaEventDestroy(ev_desc);
-          cudaEventDestroy(ev_dp);
-          throw Fail{DSG_DEADLINE, "time limit reached"};
+    for (int s = 1; s < lat.n_levels; ++s) {
+      LL.t_lo = lat.level_off[s];
+      LL.t_hi = lat.level_off[s + 1];
+      LL.s_hi = lat.level_off[s];
+      LL.n_chunks = pl.n_chunks[s];
+      LL.chunk_len = pl.chunk_len[s];
+      if (timing) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, st));
+        launch_transition(LL, st);
+        CK(cudaEventRecord(b, st));
+        kev.push_back(a);
+        kev.push_back(b);
+      } else {
+        launch_transition(LL, st);
+      }
+      launch_finalize(LL, st);
+      if (has_deadline && s % kDeadlineStride == 0) {
+        // keep at most two strides in flight so the clock tracks the device
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventRecord(e, st));
+        dl_ev.push_back(e);
+        if (dl_ev.size() >= 2) {
+          CK(cudaEventSynchronize(dl_ev[dl_ev.size() - 2]));
+          if (Clock::now() > deadline) {
+            CK(cudaStreamSynchronize(st));
+            for (auto x : dl_ev) cudaEventDestroy(x);
+            for (auto x : kev) cudaEventDestroy(x);
+            cudaEventDestroy(ev_desc);
+            cudaEventDestroy(ev_dp);
+            throw Fail{DSG_DEADLINE, "time limit reached"};
+          }
         }
       }
     }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev_dp, st));
   }
-  CK(cudaGetLastError());
-  if (!persistent) CK(cudaEventRecord(ev_dp, st));
+  res->persistent_blocks = pl.persistent ? pl.pinfo.blocks : 0;
 
-  // ---- traceback
-  const int maxb = K + Lc + 1;
-  TracebackOut* tb_d = ctx.get_t<TracebackOut>("tb.out", 1);
-  int64_t* ords_d = ctx.get_t<int64_t>("tb.ords", maxb);
-  int64_t* prevs_d = ctx.get_t<int64_t>("tb.prevs", maxb);
-  int32_t* cpus_d = ctx.get_t<int32_t>("tb.cpus", maxb);
-  uint64_t* bb_d = ctx.get_t<uint64_t>("tb.bits", (size_t)maxb * W);
-  launch_traceback(vb, I, K, Lc, W, dp, bp, D.abits, tb_d, ords_d, prevs_d, cpus_d, bb_d, st);
-  TracebackOut tb;
+  // ---- traceback (rank 0 of a sharded run holds every row)
   unsigned long long pairs = 0;
+  D2H(&pairs, LL.pair_counter, sizeof pairs);
+  const bool do_traceback = pl.rank == 0;
+  const int maxb = K + Lc + 1;
+  TracebackOut tb{};
   std::vector<int32_t> cpus(maxb);
   std::vector<uint64_t> bbits((size_t)maxb * W);
-  D2H(&tb, tb_d, sizeof tb);
-  D2H(&pairs, pairs_d, sizeof pairs);
-  D2H(cpus.data(), cpus_d, sizeof(int32_t) * maxb);
-  D2H(bbits.data(), bb_d, sizeof(uint64_t) * maxb * W);
+  if (do_traceback) {
+    TracebackOut* tb_d = ctx.get_t<TracebackOut>(pl.pfx + "tb.out", 1);
+    int64_t* ords_d = ctx.get_t<int64_t>(pl.pfx + "tb.ords", maxb);
+    int64_t* prevs_d = ctx.get_t<int64_t>(pl.pfx + "tb.prevs", maxb);
+    int32_t* cpus_d = ctx.get_t<int32_t>(pl.pfx + "tb.cpus", maxb);
+    uint64_t* bb_d = ctx.get_t<uint64_t>(pl.pfx + "tb.bits", (size_t)maxb * W);
+    launch_traceback(vb, I, K, Lc, W, dp, bp, pl.D.abits, tb_d, ords_d, prevs_d, cpus_d, bb_d, st);
+    D2H(&tb, tb_d, sizeof tb);
+    D2H(cpus.data(), cpus_d, sizeof(int32_t) * maxb);
+    D2H(bbits.data(), bb_d, sizeof(uint64_t) * maxb * W);
+  }
   if (flags & DSG_FLAG_KEEP_TABLES) {
     res->words = W;
     res->ideal_bits = (uint64_t*)std::malloc(sizeof(uint64_t) * (size_t)I * W + 8);
     D2H(res->ideal_bits, lat.sbits, sizeof(uint64_t) * (size_t)I * W);
     res->dp_values = (int64_t*)std::malloc(sizeof(int64_t) * (size_t)I * C + 8);
-    if (vb == 64) {
-      D2H(res->dp_values, dp, sizeof(int64_t) * (size_t)I * C);
-    }
+    if (vb == 64) D2H(res->dp_values, dp, sizeof(int64_t) * (size_t)I * C);
   }
-  CK(cudaEventRecord(ev_end, st));
+  CK(cudaEventRecord(pl_ev_end(ctx), st));
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
-  {
-    float dev_ms = 0;
-    cudaEventElapsedTime(&dev_ms, ev_start, ev_end);
-    res->t_device_ms = dev_ms;
-    cudaEventDestroy(ev_start);
-    cudaEventDestroy(ev_end);
-  }
   if ((flags & DSG_FLAG_KEEP_TABLES) && vb == 32) {
     std::vector<int32_t> tmp((size_t)I * C);
     ctx.d2h_bytes += (int64_t)(sizeof(int32_t) * tmp.size());
@@ -1020,9 +1067,8 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
     for (size_t i = 0; i < tmp.size(); ++i)
       res->dp_values[i] = tmp[i] == VTraits<int32_t>::INF ? INT64_MAX : (int64_t)tmp[i];
   }
-  float desc_ms = 0, dp_ms = 0;
+  float dp_ms = 0;
   cudaEventElapsedTime(&dp_ms, ev_desc, ev_dp);
-  res->t_describe_ms = ms_since(t2) - 0.0;  // refined below
   double kern_ms = 0;
   for (size_t i = 0; i + 1 < kev.size(); i += 2) {
     float x = 0;
@@ -1033,14 +1079,17 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
   for (auto x : dl_ev) cudaEventDestroy(x);
   cudaEventDestroy(ev_desc);
   cudaEventDestroy(ev_dp);
-  (void)desc_ms;
   res->t_dp_ms = dp_ms;
-  res->t_describe_ms = std::max(0.0, ms_since(t2) - dp_ms);
   // persistent: the one cooperative launch spans ev_desc..ev_dp
-  res->t_transition_kernel_ms = persistent ? dp_ms : kern_ms;
+  res->t_transition_kernel_ms = pl.persistent ? dp_ms : kern_ms;
   res->n_pairs = (int64_t)pairs;
+  res->n_ideals = I;
+  res->n_levels = lat.n_levels;
   res->value_bits = vb;
   res->denominator = P.D;
+  res->t_enumerate_ms = pl.t_enum_ms;
+  res->t_describe_ms = pl.t_desc_ms;
+  if (!do_traceback) return;
   if (tb.status == 1) throw Fail{DSG_INFEASIBLE, "no feasible assignment exists"};
   if (tb.status != 0) throw Fail{DSG_LOGIC, "dp reconstruction stuck"};
 
@@ -1062,14 +1111,30 @@ void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const 
     for (int w = 0; w < W; ++w) {
       uint64_t x = bbits[(size_t)b * W + w];
       while (x) {
-        int bit = __builtin_ctzll(x);
+        const int bit = __builtin_ctzll(x);
         x &= x - 1;
         res->members[off++] = w * 64 + bit;
       }
     }
     blk.n_members = off - blk.offset;
   }
-  res->t_traceback_ms = 0;
+}
+
+// Full device pipeline with event timing of the whole thing.
+void run_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_options* opt,
+                Pipeline& pl, dsg_result* res, Clock::time_point t0, bool reset) {
+  const int64_t launches0 = dsg::g_launches.load();
+  ctx.d2h_bytes = 0;
+  cudaEvent_t ev_start;
+  CK(cudaEventCreate(&ev_start));
+  CK(cudaEventRecord(ev_start, ctx.stream));
+  phase1(ctx, P, dg, opt, pl);
+  if (reset) reset_tables(ctx, P, pl);
+  phase2(ctx, P, opt, pl, res, t0);
+  float dev_ms = 0;
+  cudaEventElapsedTime(&dev_ms, ev_start, pl_ev_end(ctx));
+  cudaEventDestroy(ev_start);
+  res->t_device_ms = dev_ms;
   res->t_total_ms = ms_since(t0);
   res->kernel_launches = dsg::g_launches.load() - launches0;
   res->h2d_bytes = ctx.h2d_bytes;
@@ -1089,23 +1154,42 @@ void solve(int mode, const dsg_graph* graph, const dsg_config* config, const dsg
   ctx.h2d_bytes = 0;
   DeviceGraph dg = upload_graph(ctx, P, "g.");
   res->t_prepare_ms = ms_since(t0);
-  run_device(ctx, P, dg, opt, res, t0);
+  Pipeline pl;
+  run_device(ctx, P, dg, opt, pl, res, t0, true);
 }
 
 }  // namespace
 
 // A prepared solve whose graph stays resident on the device (bench: timing
-// with inputs already in HBM).
+// with inputs already in HBM), optionally one shard of a multi-GPU solve.
 struct dsg_session {
   Prepared P;
   DeviceCtx* ctx = nullptr;
   DeviceGraph dg;
   dsg_options opt;
-  std::string prefix;
+  Pipeline pl;
+  bool sharded = false;
+  bool reset_done = false;
 };
 
 namespace {
 std::atomic<int> g_session_ids{0};
+
+template <typename F>
+int guarded(dsg_result* result, F&& f) {
+  try {
+    f();
+    result->status = DSG_OK;
+  } catch (const Fail& e) {
+    result->status = e.status;
+    result->budget_limit = e.limit;
+    fill_msg(result->message, e.msg);
+  } catch (const std::exception& e) {
+    result->status = DSG_LOGIC;
+    fill_msg(result->message, e.what());
+  }
+  return result->status;
+}
 }  // namespace
 
 extern "C" {
@@ -1114,7 +1198,7 @@ dsg_session* dsg_session_create(int32_t mode, const dsg_graph* graph, const dsg_
                                 const dsg_options* options, dsg_result* status_out) {
   std::memset(status_out, 0, sizeof *status_out);
   dsg_session* s = nullptr;
-  try {
+  guarded(status_out, [&] {
     auto t0 = Clock::now();
     std::unique_ptr<dsg_session> sp(new dsg_session());
     dsg_default_options(&sp->opt);
@@ -1123,47 +1207,161 @@ dsg_session* dsg_session_create(int32_t mode, const dsg_graph* graph, const dsg_
     sp->ctx = &context(sp->opt.device);
     std::lock_guard<std::mutex> lk(sp->ctx->mu);
     CK(cudaSetDevice(sp->ctx->device));
-    sp->prefix = "s" + std::to_string(g_session_ids.fetch_add(1)) + ".";
-    sp->dg = upload_graph(*sp->ctx, sp->P, sp->prefix);
+    sp->pl.pfx = "s" + std::to_string(g_session_ids.fetch_add(1)) + ".";
+    sp->dg = upload_graph(*sp->ctx, sp->P, sp->pl.pfx);
     CK(cudaStreamSynchronize(sp->ctx->stream));
     status_out->t_prepare_ms = ms_since(t0);
     s = sp.release();
-    status_out->status = DSG_OK;
-  } catch (const Fail& f) {
-    status_out->status = f.status;
-    fill_msg(status_out->message, f.msg);
-  } catch (const std::exception& e) {
-    status_out->status = DSG_LOGIC;
-    fill_msg(status_out->message, e.what());
-  }
+  });
   return s;
 }
 
 int dsg_session_run(dsg_session* s, dsg_result* result) {
   std::memset(result, 0, sizeof *result);
-  try {
+  return guarded(result, [&] {
     if (!s) throw Fail{DSG_INVALID, "null session"};
     std::lock_guard<std::mutex> lk(s->ctx->mu);
     CK(cudaSetDevice(s->ctx->device));
     s->ctx->h2d_bytes = 0;  // inputs are resident
-    run_device(*s->ctx, s->P, s->dg, &s->opt, result, Clock::now());
-    result->status = DSG_OK;
-  } catch (const Fail& f) {
-    result->status = f.status;
-    result->budget_limit = f.limit;
-    fill_msg(result->message, f.msg);
-  } catch (const std::exception& e) {
-    result->status = DSG_LOGIC;
-    fill_msg(result->message, e.what());
-  }
-  return result->status;
+    if (s->sharded) {
+      // dsg_session_shard_reset ran phase 1 + the reset on every rank, and
+      // the caller passed a cross-rank barrier since
+      if (!s->reset_done) throw Fail{DSG_INVALID, "sharded run without dsg_session_shard_reset"};
+      s->reset_done = false;
+      const int64_t launches0 = dsg::g_launches.load();
+      s->ctx->d2h_bytes = 0;
+      cudaEvent_t ev_start;
+      CK(cudaEventCreate(&ev_start));
+      CK(cudaEventRecord(ev_start, s->ctx->stream));
+      phase2(*s->ctx, s->P, &s->opt, s->pl, result, Clock::now());
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev_start, pl_ev_end(*s->ctx));
+      cudaEventDestroy(ev_start);
+      result->t_device_ms = ms;
+      result->kernel_launches = dsg::g_launches.load() - launches0;
+      result->d2h_bytes = s->ctx->d2h_bytes;
+      return;
+    }
+    run_device(*s->ctx, s->P, s->dg, &s->opt, s->pl, result, Clock::now(), true);
+  });
+}
+
+int dsg_session_shard_prepare(dsg_session* s, int32_t rank, int32_t world,
+                              dsg_shard_handle* handle_out, dsg_result* status_out) {
+  std::memset(status_out, 0, sizeof *status_out);
+  std::memset(handle_out, 0, sizeof *handle_out);
+  return guarded(status_out, [&] {
+    if (!s) throw Fail{DSG_INVALID, "null session"};
+    if (world < 1 || rank < 0 || rank >= world || world > DSG_MAX_SHARDS)
+      throw Fail{DSG_INVALID, "bad rank / world"};
+    if (s->opt.flags & DSG_FLAG_LEVEL_LAUNCH)
+      throw Fail{DSG_UNSUPPORTED, "sharding needs the persistent level kernel"};
+    std::lock_guard<std::mutex> lk(s->ctx->mu);
+    CK(cudaSetDevice(s->ctx->device));
+    s->sharded = true;  // world == 1 too: same reset / run protocol
+    s->pl.rank = rank;
+    s->pl.world = world;
+    // placeholder peer tables (self) so phase 1 can size them
+    s->pl.peer_dp.assign(world, nullptr);
+    s->pl.peer_bp.assign(world, nullptr);
+    s->pl.peer_done.assign(world, nullptr);
+    phase1(*s->ctx, s->P, s->dg, &s->opt, s->pl);
+    handle_out->rank = rank;
+    handle_out->device = s->ctx->device;
+    handle_out->n_ideals = s->pl.I;
+    CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out->dp), s->pl.LL.dp));
+    CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out->bp), s->pl.LL.bp));
+    CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out->ctl), s->pl.ctl));
+  });
+}
+
+int dsg_session_shard_attach(dsg_session* s, const dsg_shard_handle* all, dsg_result* status_out) {
+  std::memset(status_out, 0, sizeof *status_out);
+  return guarded(status_out, [&] {
+    if (!s) throw Fail{DSG_INVALID, "null session"};
+    std::lock_guard<std::mutex> lk(s->ctx->mu);
+    CK(cudaSetDevice(s->ctx->device));
+    Pipeline& pl = s->pl;
+    for (int r = 0; r < pl.world; ++r) {
+      if (all[r].rank != r) throw Fail{DSG_INVALID, "shard handles out of rank order"};
+      if (all[r].n_ideals != pl.I) throw Fail{DSG_INVALID, "shards disagree on the lattice"};
+      if (r == pl.rank) {
+        pl.peer_dp[r] = pl.LL.dp;
+        pl.peer_bp[r] = pl.LL.bp;
+        pl.peer_done[r] = pl.PP.done;
+        continue;
+      }
+      void *d = nullptr, *b = nullptr, *c = nullptr;
+      CK(cudaIpcOpenMemHandle(&d, *reinterpret_cast<const cudaIpcMemHandle_t*>(all[r].dp),
+                              cudaIpcMemLazyEnablePeerAccess));
+      CK(cudaIpcOpenMemHandle(&b, *reinterpret_cast<const cudaIpcMemHandle_t*>(all[r].bp),
+                              cudaIpcMemLazyEnablePeerAccess));
+      CK(cudaIpcOpenMemHandle(&c, *reinterpret_cast<const cudaIpcMemHandle_t*>(all[r].ctl),
+                              cudaIpcMemLazyEnablePeerAccess));
+      pl.ipc_opened.push_back(d);
+      pl.ipc_opened.push_back(b);
+      pl.ipc_opened.push_back(c);
+      pl.peer_dp[r] = d;
+      pl.peer_bp[r] = static_cast<int32_t*>(b);
+      pl.peer_done[r] = static_cast<unsigned*>(c) + 32;
+    }
+  });
+}
+
+int dsg_session_shard_reset(dsg_session* s, dsg_result* status_out) {
+  std::memset(status_out, 0, sizeof *status_out);
+  return guarded(status_out, [&] {
+    if (!s) throw Fail{DSG_INVALID, "null session"};
+    std::lock_guard<std::mutex> lk(s->ctx->mu);
+    CK(cudaSetDevice(s->ctx->device));
+    const void* dp0 = s->pl.LL.dp;
+    cudaEvent_t ev_start;
+    CK(cudaEventCreate(&ev_start));
+    CK(cudaEventRecord(ev_start, s->ctx->stream));
+    s->ctx->d2h_bytes = 0;
+    phase1(*s->ctx, s->P, s->dg, &s->opt, s->pl);  // recomputed every solve
+    if (s->pl.LL.dp != dp0) throw Fail{DSG_LOGIC, "shard tables moved; re-attach"};
+    reset_tables(*s->ctx, s->P, s->pl);
+    CK(cudaEventRecord(pl_ev_end(*s->ctx), s->ctx->stream));
+    CK(cudaEventSynchronize(pl_ev_end(*s->ctx)));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev_start, pl_ev_end(*s->ctx));
+    cudaEventDestroy(ev_start);
+    status_out->t_device_ms = ms;
+    status_out->t_enumerate_ms = s->pl.t_enum_ms;
+    status_out->t_describe_ms = s->pl.t_desc_ms;
+    status_out->d2h_bytes = s->ctx->d2h_bytes;
+    s->reset_done = true;
+  });
+}
+
+int dsg_session_reload(dsg_session* s, const dsg_graph* graph, const dsg_config* config,
+                       dsg_result* status_out) {
+  std::memset(status_out, 0, sizeof *status_out);
+  return guarded(status_out, [&] {
+    if (!s) throw Fail{DSG_INVALID, "null session"};
+    const auto t0 = Clock::now();
+    Prepared P = prepare(s->P.training ? DSG_MODE_TRAINING : (s->P.repl ? DSG_MODE_REPLICATED
+                                                                          : DSG_MODE_INFERENCE),
+                         graph, config, nullptr, false, s->opt.flags);
+    std::lock_guard<std::mutex> lk(s->ctx->mu);
+    CK(cudaSetDevice(s->ctx->device));
+    s->ctx->h2d_bytes = 0;
+    s->P = std::move(P);
+    s->dg = upload_graph(*s->ctx, s->P, s->pl.pfx);
+    CK(cudaStreamSynchronize(s->ctx->stream));
+    status_out->h2d_bytes = s->ctx->h2d_bytes;
+    status_out->t_prepare_ms = ms_since(t0);
+  });
 }
 
 void dsg_session_destroy(dsg_session* s) {
   if (!s) return;
   if (s->ctx) {
     std::lock_guard<std::mutex> lk(s->ctx->mu);
-    s->ctx->release_prefix(s->prefix);
+    cudaSetDevice(s->ctx->device);
+    for (void* p : s->pl.ipc_opened) cudaIpcCloseMemHandle(p);
+    s->ctx->release_prefix(s->pl.pfx);
   }
   delete s;
 }
@@ -1232,7 +1430,7 @@ int dsg_enumerate_ideals(const dsg_graph* graph, const uint8_t* within, int64_t 
     std::lock_guard<std::mutex> lk(ctx.mu);
     CK(cudaSetDevice(ctx.device));
     DeviceGraph dg = upload_graph(ctx, P, "g.");
-    Lattice lat = enumerate_device(ctx, P, dg, budget, (opt->flags & DSG_FLAG_HASH_ENUM) != 0);
+    Lattice lat = enumerate_device(ctx, P, dg, budget, (opt->flags & DSG_FLAG_HASH_ENUM) != 0, "e.");
     out->count = lat.I;
     out->words = P.W;
     out->bits = (uint64_t*)std::malloc(sizeof(uint64_t) * (size_t)lat.I * P.W + 8);

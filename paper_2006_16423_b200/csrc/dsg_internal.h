@@ -154,6 +154,15 @@ struct PersistPlan {
   uint64_t* trace;           // optional [total_items][4] timestamps (DSG_TRACE_FILE)
   unsigned long long* keys;  // [I][C] packed (value^sign, arg) for mode-0 merges of
                              // 32-bit values; 0xff.. = no candidate
+  // Wavefront sharding over GPUs (one process per GPU): this rank owns the
+  // target units with unit % world == rank; finalized dp/bp rows are stored
+  // into every rank's tables over NVLink (peer pointers from CUDA IPC) and
+  // every rank's level counter is bumped with a system-scope atomic.
+  // world == 1: the tables point at this GPU's own buffers.
+  int rank, world;
+  void* const* peer_dp;        // [world] dp table of each rank
+  int32_t* const* peer_bp;     // [world]
+  unsigned* const* peer_done;  // [world] level counters of each rank
 };
 
 struct PersistInfo {
@@ -167,6 +176,7 @@ void query_persistent(const LevelLaunch& L, PersistInfo* info);
 void launch_persistent(const LevelLaunch& L, const PersistPlan& P, cudaStream_t st,
                        PersistInfo* info);
 void launch_read_globaltimer(uint64_t* out, cudaStream_t st);
+void launch_fill_u32(unsigned* p, int64_t n, unsigned value, cudaStream_t st);
 void launch_finalize(const LevelLaunch& L, cudaStream_t st);
 void launch_init_empty(int value_bits, int K, int L, void* dp, int32_t* bp, cudaStream_t st);
 

@@ -65,8 +65,8 @@ __device__ bool wait_levels(const PersistPlan& p, int j_lo, int j_hi) {
     const uint64_t t0 = globaltimer();
     for (int j = j_lo; j <= j_hi && s_ok; ++j) {
       const unsigned need = (unsigned)(p.level_off[j + 1] - p.level_off[j]);
-      if (ld_relaxed(p.done + j) >= need) continue;
-      while (ld_relaxed(p.done + j) < need) {
+      if (ld_relaxed_sys(p.done + j) >= need) continue;
+      while (ld_relaxed_sys(p.done + j) < need) {
         __nanosleep(100);
         if (ld_relaxed((const unsigned*)p.stop) != 0) {
           s_ok = 0;
@@ -80,7 +80,8 @@ __device__ bool wait_levels(const PersistPlan& p, int j_lo, int j_hi) {
         }
       }
     }
-    __threadfence();  // acquire the finished rows
+    if (p.world == 1) __threadfence();  // acquire the finished rows
+    else __threadfence_system();        // ... including peers' NVLink stores
   }
   __syncthreads();
   return s_ok != 0;
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
     const int64_t units = mode == 0 ? (T + TS - 1) / TS : T;
     const int64_t unit = it % units;
     const int64_t chunk = it / units;
+    if (p.world > 1 && (int)(unit % p.world) != p.rank) continue;  // another GPU's unit
     const int64_t s0 = p.chunk_lo[p.chunk_base[s] + chunk];
     const int64_t s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
     // sources [s0, s1) must be final
@@ -333,9 +335,9 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
       }
       __syncthreads();
       if (warp == 0 && lane < n_act) {
+        // the finished rows go to every rank's table (this GPU's own for
+        // world == 1; NVLink peer stores otherwise)
         const int64_t t = t_lo + tl0 + lane;
-        V* dpt = (V*)a.dp + (size_t)t * C;
-        int32_t* bpt = a.bp + (size_t)t * C;
         if (!kGeneric) {
 #pragma unroll
           for (int c = 0; c < CMAX; ++c) {
@@ -345,25 +347,38 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
             }
           }
           monotone_regs<V, LP1, CMAX>(best, barg, C);
+          for (int r = 0; r < p.world; ++r) {
+            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+            int32_t* bpt = p.peer_bp[r] + (size_t)t * C;
 #pragma unroll
-          for (int c = 0; c < CMAX; ++c) {
-            if (c < C) {
-              dpt[c] = best[c];
-              bpt[c] = barg[c];
+            for (int c = 0; c < CMAX; ++c) {
+              if (c < C) {
+                dpt[c] = best[c];
+                bpt[c] = barg[c];
+              }
             }
           }
         } else {
           monotone_strided(m_val + lane, m_arg + lane, TS, a.K, a.L);
-          for (int c = 0; c < C; ++c) {
-            dpt[c] = m_val[c * TS + lane];
-            bpt[c] = m_arg[c * TS + lane];
+          for (int r = 0; r < p.world; ++r) {
+            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+            int32_t* bpt = p.peer_bp[r] + (size_t)t * C;
+            for (int c = 0; c < C; ++c) {
+              dpt[c] = m_val[c * TS + lane];
+              bpt[c] = m_arg[c * TS + lane];
+            }
           }
         }
       }
       __syncthreads();
       if (tid == 0) {
-        __threadfence();  // release the rows
-        atomicAdd(p.done + s, (unsigned)n_act);
+        if (p.world == 1) {
+          __threadfence();  // release the rows
+          atomicAdd(p.peer_done[0] + s, (unsigned)n_act);
+        } else {
+          __threadfence_system();  // rows reached every peer before its counter moves
+          for (int r = 0; r < p.world; ++r) atomicAdd_system(p.peer_done[r] + s, (unsigned)n_act);
+        }
       }
     }
     __syncthreads();

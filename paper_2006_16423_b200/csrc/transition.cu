@@ -100,6 +100,12 @@ __global__ void init_empty_kernel(int K, int L, V* dp, int32_t* bp) {
 
 __global__ void read_globaltimer_kernel(uint64_t* out) { *out = globaltimer(); }
 
+__global__ void fill_u32_kernel(unsigned* p, int64_t n, unsigned value) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = value;
+}
+
 // Fewest-devices cell + argmin walk (dp_solver.cpp:332-380); one thread.
 template <typename V>
 __global__ void traceback_kernel(int64_t I, int K, int L, int W, const V* dp, const int32_t* bp,
@@ -227,6 +233,11 @@ void launch_finalize(const LevelLaunch& L, cudaStream_t st) {
 void launch_init_empty(int value_bits, int K, int L, void* dp, int32_t* bp, cudaStream_t st) {
   if (value_bits == 32) init_empty_kernel<int32_t><<<1, 128, 0, st>>>(K, L, (int32_t*)dp, bp);
   else init_empty_kernel<int64_t><<<1, 128, 0, st>>>(K, L, (int64_t*)dp, bp);
+  count_launch();
+}
+
+void launch_fill_u32(unsigned* p, int64_t n, unsigned value, cudaStream_t st) {
+  fill_u32_kernel<<<1, 256, 0, st>>>(p, n, value);
   count_launch();
 }
 

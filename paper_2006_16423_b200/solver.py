@@ -43,6 +43,14 @@ def load_library() -> C.CDLL:
     lib.dsg_session_run.restype = C.c_int
     lib.dsg_session_destroy.argtypes = [C.c_void_p]
     lib.dsg_session_destroy.restype = None
+    lib.dsg_session_shard_prepare.argtypes = [C.c_void_p, C.c_int32, C.c_int32,
+                                              C.POINTER(_abi.dsg_shard_handle),
+                                              C.POINTER(_abi.dsg_result)]
+    lib.dsg_session_shard_attach.argtypes = [C.c_void_p, C.POINTER(_abi.dsg_shard_handle),
+                                             C.POINTER(_abi.dsg_result)]
+    lib.dsg_session_shard_reset.argtypes = [C.c_void_p, C.POINTER(_abi.dsg_result)]
+    lib.dsg_session_reload.argtypes = [C.c_void_p, C.POINTER(_abi.dsg_graph),
+                                       C.POINTER(_abi.dsg_config), C.POINTER(_abi.dsg_result)]
     _lib = lib
     return lib
 
@@ -115,9 +123,16 @@ class Session:
         raise_for_status(st.status, st.message, st.budget_limit)
         self.prepare_ms = st.t_prepare_ms
 
-    def set_flags(self, flags: int) -> None:
-        # options are copied at creation; recreate to change them
-        raise NotImplementedError
+    def reload(self, g: Graph, config: DeviceConfig) -> dict:
+        """Re-flatten + re-upload a same-shaped graph (the H2D leg of e2e)."""
+        self._pg = _abi.PodGraph(g)
+        self._cfg = _abi.pod_config(config)
+        self.config = config
+        st = _abi.dsg_result()
+        self._lib.dsg_session_reload(self._h, C.byref(self._pg.struct), C.byref(self._cfg),
+                                     C.byref(st))
+        raise_for_status(st.status, st.message, st.budget_limit)
+        return {"h2d_bytes": st.h2d_bytes, "t_prepare_ms": st.t_prepare_ms}
 
     def run(self) -> RawResult:
         res = _abi.dsg_result()
@@ -138,6 +153,72 @@ class Session:
             self.close()
         except Exception:
             pass
+
+
+class ShardComm:
+    """What a sharded session needs from the process group: an all-gather of
+    small byte strings and a barrier.  `from_torch()` uses torch.distributed
+    (NCCL or gloo); tests can pass any object with the same two methods."""
+
+    def __init__(self, rank: int, world: int, all_gather_bytes, barrier):
+        self.rank, self.world = rank, world
+        self.all_gather_bytes = all_gather_bytes
+        self.barrier = barrier
+
+    @staticmethod
+    def from_torch(group=None) -> "ShardComm":
+        import torch.distributed as dist
+
+        def gather(b: bytes):
+            out = [None] * dist.get_world_size(group)
+            dist.all_gather_object(out, b, group=group)
+            return out
+
+        return ShardComm(dist.get_rank(group), dist.get_world_size(group), gather,
+                         lambda: dist.barrier(group=group))
+
+
+class ShardedSession(Session):
+    """One rank of the multi-GPU wavefront (dsg_session_shard_*, SURVEY
+    §8(e)): target units of every level are split across ranks; finished dp
+    rows travel GPU->GPU over NVLink inside the persistent kernel."""
+
+    def __init__(self, mode: int, g: Graph, config: DeviceConfig, comm: ShardComm,
+                 opt: Optional[SolveOptions] = None):
+        super().__init__(mode, g, config, opt)
+        self.comm = comm
+        mine = _abi.dsg_shard_handle()
+        st = _abi.dsg_result()
+        self._lib.dsg_session_shard_prepare(self._h, comm.rank, comm.world, C.byref(mine),
+                                            C.byref(st))
+        raise_for_status(st.status, st.message, st.budget_limit)
+        blobs = comm.all_gather_bytes(bytes(mine))
+        handles = (_abi.dsg_shard_handle * comm.world)()
+        for r, b in enumerate(blobs):
+            C.memmove(C.byref(handles[r]), b, C.sizeof(_abi.dsg_shard_handle))
+        self._lib.dsg_session_shard_attach(self._h, handles, C.byref(st))
+        raise_for_status(st.status, st.message, st.budget_limit)
+        comm.barrier()
+
+    def run(self) -> RawResult:
+        st = _abi.dsg_result()
+        self._lib.dsg_session_shard_reset(self._h, C.byref(st))
+        raise_for_status(st.status, st.message, st.budget_limit)
+        self.comm.barrier()  # every rank reset before any rank writes into it
+        res = _abi.dsg_result()
+        self._lib.dsg_session_run(self._h, C.byref(res))
+        try:
+            self.comm.barrier()  # every peer finished writing into this rank
+            raise_for_status(res.status, res.message, res.budget_limit)
+            raw = _raw_from(res, self.config)
+            # phase 1 (lattice + descriptors) ran inside the reset call
+            raw.stats["t_reset_device_ms"] = st.t_device_ms
+            raw.stats["t_enumerate_ms"] = st.t_enumerate_ms
+            raw.stats["t_describe_ms"] = st.t_describe_ms
+            raw.stats["t_device_ms"] = st.t_device_ms + res.t_device_ms
+            return raw
+        finally:
+            self._lib.dsg_result_free(C.byref(res))
 
 
 def run_dp(lib: C.CDLL, prefix: str, mode: int, g: Graph, config: DeviceConfig,

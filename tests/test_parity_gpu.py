@@ -270,3 +270,26 @@ def test_repeat_solves_are_deterministic(gpu):
     a = device_solve(1, w.graph, w.config)
     b = device_solve(1, w.graph, w.config)
     assert a.assignment == b.assignment and a.objective_value == b.objective_value
+
+
+def test_sharded_protocol_single_rank(gpu):
+    """dsg_session_shard_{prepare,attach,reset} + run at world 1: the same
+    phase split, reset/run protocol and peer-table indirection as N GPUs."""
+    from paper_2006_16423_b200.solver import ShardComm, ShardedSession
+    comm = ShardComm(0, 1, lambda b: [b], lambda: None)
+    for name in ("C3", "C1"):
+        w = wl.standin(name)
+        ref = device_solve(1 if w.training else 0, w.graph, w.config)
+        s = ShardedSession(1 if w.training else 0, w.graph, w.config, comm)
+        for _ in range(2):
+            raw = s.run()
+            assert raw.objective == ref.objective_value
+            assert raw.n_pairs == ref.stats["n_pairs"]
+        s.close()
+    g, cfg = random_dag(42)
+    s = ShardedSession(0, g, cfg, comm)
+    try:
+        got = s.run().objective
+    except InfeasibleError:
+        got = INF
+    assert got == ob.objective_or_inf("port", 0, g, cfg)
