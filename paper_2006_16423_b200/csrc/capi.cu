@@ -762,6 +762,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   pl.item_base.assign(lat.n_levels + 1, 0);
   std::vector<int64_t> tile_base(lat.n_levels, 0), part_base(lat.n_levels, 0);
   std::vector<int64_t> chunk_lo, chunk_base(lat.n_levels, 0);
+  std::vector<int64_t> n_old(lat.n_levels, 0), crit_base(lat.n_levels + 1, 0),
+      bg_base(lat.n_levels + 1, 0);
   size_t part_elems = 1;
   pl.total_tiles = 0;
   pl.total_items = 0;
@@ -810,6 +812,9 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       chunk_lo.push_back(S);
       chunks = oc + rc;
       pl.chunk_len[s] = 0;
+      n_old[s] = oc;
+      crit_base[s + 1] = crit_base[s] + units * rc;
+      bg_base[s + 1] = bg_base[s] + units * oc;
     } else {
       chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / min_chunk));
       const int64_t len = (S + chunks - 1) / chunks;
@@ -858,6 +863,21 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.item_base = up64("pp.item_base", pl.item_base);
   PP.part_base = up64("pp.part_base", part_base);
   PP.total_items = pl.total_items;
+  // critical / background CTA split (env DSG_CRIT_FRAC, default 1/4)
+  {
+    double frac = 0.25;
+    if (const char* e = std::getenv("DSG_CRIT_FRAC")) frac = std::atof(e);
+    const int blocks = std::max(1, pl.pinfo.blocks);
+    int cb = (int)(blocks * frac + 0.5);
+    if (blocks < 8 || frac <= 0.0) cb = 0;  // tiny grids: one combined list
+    cb = std::min(cb, blocks - 1);
+    PP.crit_blocks = std::max(cb, 0);
+    PP.n_old = up64("pp.n_old", n_old);
+    PP.crit_base = up64("pp.crit_base", crit_base);
+    PP.bg_base = up64("pp.bg_base", bg_base);
+    PP.total_crit = crit_base[lat.n_levels];
+    PP.total_bg = bg_base[lat.n_levels];
+  }
   {
     int32_t* mode_d = ctx.get_t<int32_t>(pfx + "pp.mode", pl.mode.size());
     CK(cudaMemcpyAsync(mode_d, pl.mode.data(), sizeof(int32_t) * pl.mode.size(),

@@ -144,6 +144,12 @@ struct PersistPlan {
   const int64_t* tile_base;  // [n_levels] prefix of arrival counters over levels
   const int64_t* item_base;  // [n_levels + 1] prefix of work items over levels
   const int64_t* part_base;  // [n_levels] offset of each level's partials
+  // critical / background split (crit_blocks == 0: one combined list)
+  int crit_blocks;
+  const int64_t* n_old;      // [n_levels] chunks over levels <= s-2 (background)
+  const int64_t* crit_base;  // [n_levels + 1] prefix of critical items
+  const int64_t* bg_base;    // [n_levels + 1] prefix of background items
+  int64_t total_crit, total_bg;
   const int32_t* level_of;   // [I] level of each ordinal
   int64_t total_items;
   unsigned* tile_count;      // [total counters], zeroed

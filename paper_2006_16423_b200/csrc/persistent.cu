@@ -62,12 +62,18 @@ __device__ bool wait_levels(const PersistPlan& p, int j_lo, int j_hi) {
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
     s_ok = 1;
-    const uint64_t t0 = globaltimer();
+    uint64_t t0 = 0;
     for (int j = j_lo; j <= j_hi && s_ok; ++j) {
       const unsigned need = (unsigned)(p.level_off[j + 1] - p.level_off[j]);
       if (ld_relaxed_sys(p.done + j) >= need) continue;
+      // polite polling: back off up to ~1 us so the spinning warp does not
+      // steal issue slots from the co-resident CTAs doing the real work
+      unsigned ns = 32, polls = 0;
+      if (!t0) t0 = globaltimer();
       while (ld_relaxed_sys(p.done + j) < need) {
-        __nanosleep(100);
+        __nanosleep(ns);
+        ns = ns < 1024 ? ns * 2 : 1024;
+        if ((++polls & 63) != 0) continue;
         if (ld_relaxed((const unsigned*)p.stop) != 0) {
           s_ok = 0;
           break;
@@ -140,18 +146,28 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
   const int32_t* pa = a.part_arg;
   unsigned nested_total = 0;
   int s = 1;  // current level (items are level ordered)
+  // Which list this CTA walks: with a split, the first crit_blocks CTAs take
+  // the critical items (chunks over the newest level, which gate the next
+  // level) and the rest the background items (older sources, ready early),
+  // so the level chain never queues behind a long background item.
+  const bool split = p.crit_blocks > 0;
+  const bool crit = split && (int)blockIdx.x < p.crit_blocks;
+  const int64_t* base = !split ? p.item_base : (crit ? p.crit_base : p.bg_base);
+  const int64_t total = !split ? p.total_items : (crit ? p.total_crit : p.total_bg);
+  const int64_t first = !split ? blockIdx.x : (crit ? blockIdx.x : blockIdx.x - p.crit_blocks);
+  const int64_t stride = !split ? gridDim.x : (crit ? p.crit_blocks : gridDim.x - p.crit_blocks);
 
-  for (int64_t gi = blockIdx.x; gi < p.total_items; gi += gridDim.x) {
-    while (s + 1 < p.n_levels && gi >= p.item_base[s + 1]) ++s;
+  for (int64_t gi = first; gi < total; gi += stride) {
+    while (s + 1 < p.n_levels && gi >= base[s + 1]) ++s;
     const int64_t t_lo = p.level_off[s], t_hi = p.level_off[s + 1];
     const int64_t T = t_hi - t_lo;
     const int64_t chunks = p.n_chunks[s];
     const int mode = p.mode[s];
     const size_t pb = (size_t)p.part_base[s];
-    const int64_t it = gi - p.item_base[s];
+    const int64_t it = gi - base[s];
     const int64_t units = mode == 0 ? (T + TS - 1) / TS : T;
     const int64_t unit = it % units;
-    const int64_t chunk = it / units;
+    const int64_t chunk = it / units + ((split && crit) ? p.n_old[s] : 0);
     if (p.world > 1 && (int)(unit % p.world) != p.rank) continue;  // another GPU's unit
     const int64_t s0 = p.chunk_lo[p.chunk_base[s] + chunk];
     const int64_t s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
@@ -383,7 +399,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
     }
     __syncthreads();
     if (p.trace && tid == 0) {
-      uint64_t* tr = p.trace + gi * 4;
+      uint64_t* tr = p.trace + (gi + ((split && !crit) ? p.total_crit : 0)) * 4;
       tr[0] = tr0;
       tr[1] = tr1;
       tr[2] = tr2;
