@@ -637,6 +637,8 @@ struct Pipeline {
   int rank = 0, world = 1;
   std::vector<void*> peer_dp;
   std::vector<int32_t*> peer_bp;
+  int64_t* level_off_d = nullptr;
+  int32_t* level_of_d = nullptr;
   std::vector<unsigned*> peer_done;
   std::vector<void*> ipc_opened;
   double t_enum_ms = 0, t_desc_ms = 0;
@@ -745,7 +747,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   LL.bw_to = dg.g.bw_to;
   LL.n_nodes = P.n;
   LL.dp = ctx.get(pfx + "dp.values", (size_t)I * C * vsz);
-  LL.bp = ctx.get_t<int32_t>(pfx + "dp.bp", (size_t)I * C);
+  LL.bp = nullptr;  // values only; the traceback re-derives the argmins
   LL.pair_counter = ctx.get_t<unsigned long long>(pfx + "dp.pairs", 1);
 
   // ---- chunk plan
@@ -836,12 +838,27 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     for (int s = 1; s < lat.n_levels; ++s) {
       part_base[s] = (int64_t)part_elems;
       const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
-      const int64_t rows = pl.mode[s] == 0 ? (vb == 32 ? 0 : ((T + 31) / 32) * 32) : T;
+      // mode 0 merges chunks with atomicMin (no partials); mode 1 keeps one
+      // partial per (target, chunk, cell)
+      const int64_t rows = pl.mode[s] == 0 ? 0 : T;
       part_elems += (size_t)(pl.n_chunks[s] * C * rows);
     }
   }
   LL.part_val = ctx.get(pfx + "dp.part_val", part_elems * vsz);
-  LL.part_arg = ctx.get_t<int32_t>(pfx + "dp.part_arg", part_elems);
+  LL.part_arg = nullptr;
+  // level of every ordinal (dependency waits, traceback)
+  {
+    pl.level_off_d = ctx.get_t<int64_t>(pfx + "pp.level_off", lat.level_off.size() + 1);
+    CK(cudaMemcpyAsync(pl.level_off_d, lat.level_off.data(), sizeof(int64_t) * lat.level_off.size(),
+                       cudaMemcpyHostToDevice, st));
+    std::vector<int32_t> lvl_of((size_t)I);
+    for (int s = 0; s < lat.n_levels; ++s)
+      for (int64_t o = lat.level_off[s]; o < lat.level_off[s + 1]; ++o) lvl_of[o] = s;
+    pl.level_of_d = ctx.get_t<int32_t>(pfx + "pp.level_of", (size_t)I);
+    CK(cudaMemcpyAsync(pl.level_of_d, lvl_of.data(), sizeof(int32_t) * I, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // host vectors are temporaries
+    ctx.h2d_bytes += (int64_t)(sizeof(int32_t) * I + sizeof(int64_t) * lat.level_off.size());
+  }
   if (!pl.persistent) return;
 
   // ---- persistent plan (device copies)
@@ -854,7 +871,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     ctx.h2d_bytes += (int64_t)(sizeof(int64_t) * v.size());
     return (const int64_t*)d;
   };
-  PP.level_off = up64("pp.level_off", lat.level_off);
+  PP.level_off = pl.level_off_d;
+  PP.level_of = pl.level_of_d;
   PP.n_chunks = up64("pp.n_chunks", pl.n_chunks);
   PP.chunk_len = up64("pp.chunk_len", pl.chunk_len);
   PP.chunk_lo = up64("pp.chunk_lo", chunk_lo);
@@ -883,13 +901,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     CK(cudaMemcpyAsync(mode_d, pl.mode.data(), sizeof(int32_t) * pl.mode.size(),
                        cudaMemcpyHostToDevice, st));
     PP.mode = mode_d;
-    std::vector<int32_t> lvl_of((size_t)I);
-    for (int s = 0; s < lat.n_levels; ++s)
-      for (int64_t o = lat.level_off[s]; o < lat.level_off[s + 1]; ++o) lvl_of[o] = s;
-    int32_t* lo_d = ctx.get_t<int32_t>(pfx + "pp.level_of", (size_t)I);
-    CK(cudaMemcpyAsync(lo_d, lvl_of.data(), sizeof(int32_t) * I, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));  // host vectors are temporaries
-    PP.level_of = lo_d;
   }
   PP.tile_count = ctx.get_t<unsigned>(pfx + "pp.tile_count", (size_t)pl.total_tiles + 1);
   pl.ctl_words = (size_t)lat.n_levels + 64;
@@ -897,7 +909,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.stop = reinterpret_cast<int*>(pl.ctl);
   PP.err = reinterpret_cast<int*>(pl.ctl + 1);
   PP.done = pl.ctl + 32;
-  PP.keys = ctx.get_t<unsigned long long>(pfx + "pp.keys", vb == 32 ? (size_t)I * C : 1);
+  PP.keys = ctx.get_t<unsigned long long>(pfx + "pp.keys", (size_t)I * C);  // value atomics
   // peer tables: this GPU only, until a sharded session attaches its peers
   if (pl.world == 1) {
     pl.peer_dp.assign(1, LL.dp);
@@ -942,14 +954,13 @@ void reset_tables(DeviceCtx& ctx, const Prepared& P, Pipeline& pl) {
   cudaStream_t st = ctx.stream;
   const int vb = P.value_bits;
   CK(cudaMemsetAsync(pl.LL.pair_counter, 0, sizeof(unsigned long long), st));
-  launch_init_empty(vb, P.K, P.L, pl.LL.dp, pl.LL.bp, st);
+  launch_init_empty(vb, P.K, P.L, pl.LL.dp, st);
   if (pl.persistent) {
     CK(cudaMemsetAsync(pl.PP.tile_count, 0, sizeof(unsigned) * (pl.total_tiles + 1), st));
     CK(cudaMemsetAsync(pl.ctl, 0, sizeof(unsigned) * pl.ctl_words, st));
     // level 0 (the empty ideal) is final before the launch
     launch_fill_u32(pl.PP.done, 1, 1u, st);
-    if (vb == 32)
-      CK(cudaMemsetAsync(pl.PP.keys, 0xff, sizeof(unsigned long long) * pl.I * P.C, st));
+    launch_fill_inf(vb, pl.PP.keys, pl.I * P.C, st);
   }
   CK(cudaStreamSynchronize(st));
 }
@@ -967,7 +978,6 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
   const int vb = P.value_bits;
   LevelLaunch& LL = pl.LL;
   void* dp = LL.dp;
-  int32_t* bp = LL.bp;
 
   cudaEvent_t ev_desc, ev_dp;
   CK(cudaEventCreate(&ev_desc));
@@ -1056,19 +1066,23 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
   D2H(&pairs, LL.pair_counter, sizeof pairs);
   const bool do_traceback = pl.rank == 0;
   const int maxb = K + Lc + 1;
-  TracebackOut tb{};
+  TraceState tb{};
   std::vector<int32_t> cpus(maxb);
   std::vector<uint64_t> bbits((size_t)maxb * W);
   if (do_traceback) {
-    TracebackOut* tb_d = ctx.get_t<TracebackOut>(pl.pfx + "tb.out", 1);
-    int64_t* ords_d = ctx.get_t<int64_t>(pl.pfx + "tb.ords", maxb);
-    int64_t* prevs_d = ctx.get_t<int64_t>(pl.pfx + "tb.prevs", maxb);
-    int32_t* cpus_d = ctx.get_t<int32_t>(pl.pfx + "tb.cpus", maxb);
-    uint64_t* bb_d = ctx.get_t<uint64_t>(pl.pfx + "tb.bits", (size_t)maxb * W);
-    launch_traceback(vb, I, K, Lc, W, dp, bp, pl.D.abits, tb_d, ords_d, prevs_d, cpus_d, bb_d, st);
-    D2H(&tb, tb_d, sizeof tb);
-    D2H(cpus.data(), cpus_d, sizeof(int32_t) * maxb);
-    D2H(bbits.data(), bb_d, sizeof(uint64_t) * maxb * W);
+    TraceBuffers tbuf;
+    tbuf.state = ctx.get_t<TraceState>(pl.pfx + "tb.state", 1);
+    tbuf.n_parts = std::max(1, ctx.sm_count * 2);
+    tbuf.part_v = ctx.get(pl.pfx + "tb.part_v", (size_t)tbuf.n_parts * 8);
+    tbuf.part_g = ctx.get_t<int32_t>(pl.pfx + "tb.part_g", tbuf.n_parts);
+    tbuf.ords = ctx.get_t<int64_t>(pl.pfx + "tb.ords", maxb);
+    tbuf.prevs = ctx.get_t<int64_t>(pl.pfx + "tb.prevs", maxb);
+    tbuf.kinds = ctx.get_t<int32_t>(pl.pfx + "tb.kinds", maxb);
+    tbuf.block_bits = ctx.get_t<uint64_t>(pl.pfx + "tb.bits", (size_t)maxb * W);
+    launch_traceback(LL, pl.level_of_d, pl.level_off_d, I, ctx.sm_count, tbuf, st);
+    D2H(&tb, tbuf.state, sizeof tb);
+    D2H(cpus.data(), tbuf.kinds, sizeof(int32_t) * maxb);
+    D2H(bbits.data(), tbuf.block_bits, sizeof(uint64_t) * maxb * W);
   }
   if (flags & DSG_FLAG_KEEP_TABLES) {
     res->words = W;
@@ -1110,8 +1124,8 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
   res->t_enumerate_ms = pl.t_enum_ms;
   res->t_describe_ms = pl.t_desc_ms;
   if (!do_traceback) return;
-  if (tb.status == 1) throw Fail{DSG_INFEASIBLE, "no feasible assignment exists"};
-  if (tb.status != 0) throw Fail{DSG_LOGIC, "dp reconstruction stuck"};
+  if (tb.status == 2) throw Fail{DSG_INFEASIBLE, "no feasible assignment exists"};
+  if (tb.status != 1) throw Fail{DSG_LOGIC, "dp reconstruction stuck"};
 
   // ---- result
   const int64_t g = gcd64(tb.best_value, P.D);
@@ -1290,7 +1304,6 @@ int dsg_session_shard_prepare(dsg_session* s, int32_t rank, int32_t world,
     handle_out->device = s->ctx->device;
     handle_out->n_ideals = s->pl.I;
     CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out->dp), s->pl.LL.dp));
-    CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out->bp), s->pl.LL.bp));
     CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out->ctl), s->pl.ctl));
   });
 }
@@ -1311,18 +1324,15 @@ int dsg_session_shard_attach(dsg_session* s, const dsg_shard_handle* all, dsg_re
         pl.peer_done[r] = pl.PP.done;
         continue;
       }
-      void *d = nullptr, *b = nullptr, *c = nullptr;
+      void *d = nullptr, *c = nullptr;
       CK(cudaIpcOpenMemHandle(&d, *reinterpret_cast<const cudaIpcMemHandle_t*>(all[r].dp),
-                              cudaIpcMemLazyEnablePeerAccess));
-      CK(cudaIpcOpenMemHandle(&b, *reinterpret_cast<const cudaIpcMemHandle_t*>(all[r].bp),
                               cudaIpcMemLazyEnablePeerAccess));
       CK(cudaIpcOpenMemHandle(&c, *reinterpret_cast<const cudaIpcMemHandle_t*>(all[r].ctl),
                               cudaIpcMemLazyEnablePeerAccess));
       pl.ipc_opened.push_back(d);
-      pl.ipc_opened.push_back(b);
       pl.ipc_opened.push_back(c);
       pl.peer_dp[r] = d;
-      pl.peer_bp[r] = static_cast<int32_t*>(b);
+      pl.peer_bp[r] = nullptr;
       pl.peer_done[r] = static_cast<unsigned*>(c) + 32;
     }
   });

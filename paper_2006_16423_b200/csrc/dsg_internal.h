@@ -184,19 +184,31 @@ void launch_persistent(const LevelLaunch& L, const PersistPlan& P, cudaStream_t 
 void launch_read_globaltimer(uint64_t* out, cudaStream_t st);
 void launch_fill_u32(unsigned* p, int64_t n, unsigned value, cudaStream_t st);
 void launch_finalize(const LevelLaunch& L, cudaStream_t st);
-void launch_init_empty(int value_bits, int K, int L, void* dp, int32_t* bp, cudaStream_t st);
+void launch_init_empty(int value_bits, int K, int L, void* dp, cudaStream_t st);
+void launch_fill_inf(int value_bits, void* p, int64_t n, cudaStream_t st);
 
-struct TracebackOut {
-  int32_t status;   // 0 ok, 1 infeasible, 2 stuck
-  int32_t best_k, best_l;
+// Traceback state on the device (transition.cu).
+struct TraceState {
+  int64_t ord;
+  int32_t k, l;
+  int32_t status;   // 0 walking, 1 done, 2 infeasible, 3 stuck
   int32_t n_blocks;
+  int32_t best_k, best_l;
   int64_t best_value;
 };
 
-// ords/prevs/cpus/block_bits hold up to K+L entries (one per block).
-void launch_traceback(int value_bits, int64_t I, int K, int L, int W, const void* dp,
-                      const int32_t* bp, const uint64_t* abits, TracebackOut* out,
-                      int64_t* ords, int64_t* prevs, int32_t* cpus, uint64_t* block_bits,
-                      cudaStream_t st);
+struct TraceBuffers {
+  TraceState* state;
+  void* part_v;          // [n_parts] per-CTA direct minimum
+  int32_t* part_g;       // [n_parts] its smallest argmin
+  int n_parts;
+  int64_t* ords;         // [K+L+1] one entry per block
+  int64_t* prevs;
+  int32_t* kinds;        // cpu | repl << 1
+  uint64_t* block_bits;  // [K+L+1][W]
+};
+
+void launch_traceback(const LevelLaunch& L, const int32_t* level_of, const int64_t* level_off,
+                      int64_t I, int sm_count, TraceBuffers& b, cudaStream_t st);
 
 }  // namespace dsg

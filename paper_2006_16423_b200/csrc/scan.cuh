@@ -218,22 +218,61 @@ __device__ __forceinline__ V acc_block_cost(const LevelLaunch& a, int64_t s, con
   return combine<V>(cin, proc, cout, a.interleave);
 }
 
-// Scan sources s0, s0+step, ... < s1 for target x.  Cells in registers
-// (LP1 > 0) or in a shared-memory column colv/cola with stride CS (LP1 == 0).
-// Source dp rows use plain (coherent) loads: in the persistent kernel other
-// CTAs wrote them before the last grid barrier.
+// K2+K3 for one (target, source) pair: false when I' ⊄ I (not a
+// transition) — *counted* is set when it is a transition at all (the
+// reference counts gated training pairs too) and *gated* when the training
+// backward gate rejects the block.  On success: accelerator load (INF if
+// infeasible), CPU load, block memory.
+template <typename V, bool TRAIN, int TS>
+__device__ __forceinline__ bool pair_cost(const LevelLaunch& a, const Target<V>& x, int64_t s,
+                                          const uint64_t* tA, const uint64_t* tInt, bool& gated,
+                                          V& acc, V& cpu, V& mem_blk) {
+  constexpr V INF = VTraits<V>::INF;
+  const SrcRec r = load_rec(a.srec + s);
+  gated = false;
+  if (TRAIN && a.has_bw) {
+    const uint64_t* sA = a.abits + (size_t)s * a.W;
+    if (!(a.fastgate && x.up && __ldg(a.upset + s)) && !bw_contiguous<TS>(a, tA, sA)) {
+      gated = true;
+      return true;
+    }
+  }
+  cpu = x.cpu - (V)r.cpu;
+  mem_blk = (V)(x.mem - (V)r.mem);
+  acc = INF;
+  bool acc_ok = a.K > 0 && (x.un - r.unsup) == 0;
+  if (acc_ok && a.memcheck) acc_ok = !(mem_blk > (V)a.mlim);
+  if (acc_ok) acc = acc_block_cost<V, TRAIN, TS>(a, s, r, (V)(x.acc - (V)r.acc), x, tA, tInt);
+  return true;
+}
+
+// replicated_load (dp_solver.cpp:100-108) for r >= 2 on exactly scaled values
+template <typename V>
+__device__ __forceinline__ V replicated(const LevelLaunch& a, V acc, V mem_blk, int rr) {
+  const V divided = acc / (V)rr;
+  const V sync = (V)a.repl_sign * ((mem_blk / (V)a.repl_bn) * (V)a.repl_bd * (V)(rr - 1) / (V)rr);
+  return a.repl_combine == 0 ? (V)(divided + sync) : vmax(divided, sync);
+}
+
+// Scan sources s0, s0+step, ... < s1 for target x: the fused K2+K3+K4 loop.
+// The K4 update is value-only — cell = min(cell, max(dp[I'][k-1][l], acc))
+// and min(cell, max(dp[I'][k][l-1], cpu)), two IMNMX per candidate; the
+// argmin is recovered exactly for the ≤ K+L cells of the optimal path during
+// traceback (traceback_search).  Cells live in registers (LP1 > 0) or in a
+// shared-memory column colv with stride CS (LP1 == 0: large (K+1)(L+1),
+// replication).  Source dp rows are plain (coherent) loads: inside the
+// persistent kernel other CTAs wrote them after this kernel started.
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int CS>
 __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Target<V>& x,
                                                  int64_t s0, int64_t s1, int step,
                                                  const uint64_t* tA, const uint64_t* tInt, V* best,
-                                                 int32_t* barg, V* colv, int32_t* cola) {
+                                                 V* colv) {
   constexpr V INF = VTraits<V>::INF;
   constexpr bool kGeneric = LP1 == 0;
   constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
   const int W = a.W;
   const int C = a.C;
   const V* dp = (const V*)a.dp;
-  const V mlim = (V)a.mlim;
   unsigned nested_cnt = 0;
   for (int64_t s = s0; s < s1; s += step) {
     // K2: I' ⊆ I
@@ -243,45 +282,21 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     if (UNIFORM && !__any_sync(0xffffffffu, nested)) continue;
     if (!nested) continue;
     ++nested_cnt;
-    if (TRAIN && a.has_bw) {
-      if (!(a.fastgate && x.up && __ldg(a.upset + s)) && !bw_contiguous<TS>(a, tA, sA)) continue;
-    }
-    const SrcRec r = load_rec(a.srec + s);
-    // K3: block cost
-    const V cpu = x.cpu - (V)r.cpu;
-    V acc = INF;
-    bool acc_ok = a.K > 0 && (x.un - r.unsup) == 0;
-    if (acc_ok && a.memcheck) acc_ok = !((V)(x.mem - (V)r.mem) > mlim);
-    if (acc_ok) acc = acc_block_cost<V, TRAIN, TS>(a, s, r, (V)(x.acc - (V)r.acc), x, tA, tInt);
-    // K4: min-max update, strict < keeps the smallest argmin.  arg =
-    // src*(K+2) + r for an accelerator block on r replicas, + K+1 for a CPU
-    // block: within one source the reference tries r = 1..k, then the CPU
-    // (dp_solver.cpp:205-230), so the smallest arg is its first improvement.
+    bool gated;
+    V acc, cpu, mem_blk;
+    pair_cost<V, TRAIN, TS>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk);
+    if (gated) continue;
+    // K4: min-max update
     const V* sdp = dp + (size_t)s * C;
-    const int32_t base_arg = (int32_t)(s * (a.K + 2));
-    const int32_t aa = base_arg + 1, ac = base_arg + a.K + 1;
     if (kGeneric && a.repl && acc != INF) {
-      // replication (dp_solver.cpp:100-108, 209-219): values are scaled so
-      // base/r and (r-1)*mem/(r*B) are exact integers (capi.cu)
-      const V mem_blk = (V)(x.mem - (V)r.mem);
       const int lp1 = a.L + 1;
       for (int rr = 1; rr <= a.K; ++rr) {
-        V load = acc;
-        if (rr > 1) {
-          const V divided = acc / (V)rr;
-          const V sync = (V)a.repl_sign * ((mem_blk / (V)a.repl_bn) * (V)a.repl_bd * (V)(rr - 1) / (V)rr);
-          load = a.repl_combine == 0 ? (V)(divided + sync) : vmax(divided, sync);
-        }
-        for (int k = rr; k <= a.K; ++k) {
+        const V load = rr == 1 ? acc : replicated<V>(a, acc, mem_blk, rr);
+        for (int k = rr; k <= a.K; ++k)
           for (int l = 0; l <= a.L; ++l) {
             const int c = k * lp1 + l;
-            const V v = vmax(sdp[c - rr * lp1], load);
-            if (v < colv[c * CS] || (v == colv[c * CS] && base_arg + rr < cola[c * CS])) {
-              colv[c * CS] = v;
-              cola[c * CS] = base_arg + rr;
-            }
+            colv[c * CS] = min(colv[c * CS], vmax(sdp[c - rr * lp1], load));
           }
-        }
       }
       acc = INF;  // accelerator candidates done; the CPU ones below
     }
@@ -291,20 +306,10 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
         const int k = c / (LP1 ? LP1 : 1);
         const int l = c % (LP1 ? LP1 : 1);
         if (c < C) {
-          if (k >= 1) {
-            const V v = vmax(sdp[c - LP1], acc);
-            if (v < best[c]) {
-              best[c] = v;
-              barg[c] = aa;
-            }
-          }
-          if (l >= 1) {
-            const V v = vmax(sdp[c - 1], cpu);
-            if (v < best[c]) {
-              best[c] = v;
-              barg[c] = ac;
-            }
-          }
+          V b = best[c];
+          if (k >= 1) b = min(b, vmax(sdp[c - LP1], acc));
+          if (l >= 1) b = min(b, vmax(sdp[c - 1], cpu));
+          best[c] = b;
         }
       }
     } else {
@@ -323,22 +328,7 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
 #pragma unroll
         for (int i = 0; i < B; ++i) {
           const int c = c0 + i;
-          if (c < C) {
-            V b = colv[c * CS];
-            int32_t g = cola[c * CS];
-            const V v1 = vmax(va[i], acc);
-            if (v1 < b) {
-              b = v1;
-              g = aa;
-            }
-            const V v2 = vmax(vc[i], cpu);
-            if (v2 < b) {
-              b = v2;
-              g = ac;
-            }
-            colv[c * CS] = b;
-            cola[c * CS] = g;
-          }
+          if (c < C) colv[c * CS] = min(colv[c * CS], min(vmax(va[i], acc), vmax(vc[i], cpu)));
         }
       }
     }
@@ -347,20 +337,13 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
 }
 
 template <typename V, int LP1, int KP1MAX, int CS>
-__device__ __forceinline__ void init_cells(int C, V* best, int32_t* barg, V* colv, int32_t* cola) {
+__device__ __forceinline__ void init_cells(int C, V* best, V* colv) {
   constexpr V INF = VTraits<V>::INF;
   constexpr int CMAX = LP1 == 0 ? 1 : LP1 * KP1MAX;
 #pragma unroll
-  for (int c = 0; c < CMAX; ++c) {
-    best[c] = INF;
-    barg[c] = INT_MAX;
-  }
-  if (LP1 == 0) {
-    for (int c = 0; c < C; ++c) {
-      colv[c * CS] = INF;
-      cola[c * CS] = INT_MAX;
-    }
-  }
+  for (int c = 0; c < CMAX; ++c) best[c] = INF;
+  if (LP1 == 0)
+    for (int c = 0; c < C; ++c) colv[c * CS] = INF;
 }
 
 // lexicographic (value, arg) minimum
@@ -375,42 +358,28 @@ __device__ __forceinline__ void vmin_arg(V& v, int32_t& g, V v2, int32_t g2) {
 // monotone_pass, dp_solver.cpp:180-193 (in place, k then l ascending), on
 // register cells with compile-time indices
 template <typename V, int LP1, int CMAX>
-__device__ __forceinline__ void monotone_regs(V* v, int32_t* g, int C) {
+__device__ __forceinline__ void monotone_regs(V* v, int C) {
 #pragma unroll
   for (int c = 0; c < CMAX; ++c) {
     const int k = c / (LP1 ? LP1 : 1), l = c % (LP1 ? LP1 : 1);
     if (c < C) {
-      if (k > 0 && v[c - (LP1 ? LP1 : 1)] < v[c]) {
-        v[c] = v[c - (LP1 ? LP1 : 1)];
-        g[c] = -3;
-      }
-      if (l > 0 && v[c - 1] < v[c]) {
-        v[c] = v[c - 1];
-        g[c] = -4;
-      }
+      if (k > 0) v[c] = min(v[c], v[c - (LP1 ? LP1 : 1)]);
+      if (l > 0) v[c] = min(v[c], v[c - 1]);
     }
   }
 }
 
 // ... and on a strided shared-memory / global column
 template <typename V>
-__device__ __forceinline__ void monotone_strided(V* v, int32_t* g, int stride, int K, int L) {
+__device__ __forceinline__ void monotone_strided(V* v, int stride, int K, int L) {
   const int lp1 = L + 1;
   for (int k = 0; k <= K; ++k) {
     for (int l = 0; l <= L; ++l) {
       const int c = k * lp1 + l;
       V cur = v[c * stride];
-      int32_t ga = g[c * stride];
-      if (k > 0 && v[(c - lp1) * stride] < cur) {
-        cur = v[(c - lp1) * stride];
-        ga = -3;
-      }
-      if (l > 0 && v[(c - 1) * stride] < cur) {
-        cur = v[(c - 1) * stride];
-        ga = -4;
-      }
+      if (k > 0) cur = min(cur, v[(c - lp1) * stride]);
+      if (l > 0) cur = min(cur, v[(c - 1) * stride]);
       v[c * stride] = cur;
-      g[c * stride] = ga;
     }
   }
 }

@@ -1,13 +1,23 @@
 // transition.cu — per-level launches (DSG_FLAG_LEVEL_LAUNCH cross-check
-// path), dp initialisation and traceback.
+// path), dp initialisation and the traceback.
 //
-// One transition_kernel launch per level: a CTA owns a tile of 128 target
-// ideals (one per thread) and a contiguous chunk of source ordinals; all
-// 32 lanes walk the same source (broadcast loads) through the fused scan of
-// scan.cuh; per-chunk (value, arg) partials are reduced in chunk order by
-// finalize_kernel, which then applies monotone_pass (dp_solver.cpp:180-193).
-// The default driver is the persistent cooperative kernel (persistent.cu);
-// this path shares the scan but nothing else, so the parity tests run both.
+// Per-level path: one transition_kernel launch per level; a CTA owns a tile
+// of 128 target ideals (one per thread) and a contiguous chunk of source
+// ordinals; all 32 lanes walk the same source (broadcast loads) through the
+// fused scan of scan.cuh; finalize_kernel reduces the per-chunk minima and
+// applies monotone_pass (dp_solver.cpp:180-193).  The default driver is the
+// persistent dataflow kernel (persistent.cu); this path shares the scan but
+// nothing else, so the parity tests run both.
+//
+// Traceback (dp_solver.cpp:332-380).  The DP kernels keep values only; the
+// traceback re-derives the argmin of the ≤ K+L cells on the optimal path:
+// for cell (ord, k, l), traceback_search scans every source of `ord` on the
+// whole GPU and keeps the lexicographically smallest (value, src*(K+2)+code)
+// — code r for an accelerator block on r replicas, K+1 for a CPU block —
+// which is the reference's first-found improvement when sources are walked
+// in ordinal order (dp_solver.cpp:205-230); traceback_decide then replays
+// monotone_pass's strict tests to tell a block from a waste move (kinds
+// 3/4) and steps to the predecessor.
 #include <climits>
 #include <cstdint>
 
@@ -29,35 +39,25 @@ __global__ void __launch_bounds__(kTileTargets) transition_kernel(const LevelLau
   uint64_t* s_tgt = reinterpret_cast<uint64_t*>(smem);
   uint64_t* s_int = s_tgt + (size_t)W * TS;
   V* s_best = reinterpret_cast<V*>(s_int + (TRAIN ? (size_t)W * TS : 0));
-  int32_t* s_arg = reinterpret_cast<int32_t*>(s_best + (kGeneric ? (size_t)C * TS : 0));
   const int tid = threadIdx.x;
   const int64_t T = a.t_hi - a.t_lo;
   const Target<V> x = load_target<V, TRAIN, TS>(a, a.t_lo, a.t_hi, blockIdx.x, tid, s_tgt + tid,
                                                 s_int + tid);
   V best[CMAX];
-  int32_t barg[CMAX];
-  init_cells<V, LP1, KP1MAX, TS>(C, best, barg, s_best + tid, s_arg + tid);
+  init_cells<V, LP1, KP1MAX, TS>(C, best, s_best + tid);
   __syncwarp();
   const int64_t s0 = (int64_t)blockIdx.y * a.chunk_len;
   const int64_t s1 = min(s0 + a.chunk_len, a.s_hi);
   unsigned nested = scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS>(
-      a, x, s0, s1, 1, s_tgt + tid, s_int + tid, best, barg, s_best + tid, s_arg + tid);
+      a, x, s0, s1, 1, s_tgt + tid, s_int + tid, best, s_best + tid);
   if (x.active) {
     V* pv = (V*)a.part_val;
     const size_t base = (size_t)blockIdx.y * C;
 #pragma unroll
-    for (int c = 0; c < (kGeneric ? 0 : CMAX); ++c) {
-      if (c < C) {
-        pv[(base + c) * T + x.tl] = best[c];
-        a.part_arg[(base + c) * T + x.tl] = barg[c];
-      }
-    }
-    if (kGeneric) {
-      for (int c = 0; c < C; ++c) {
-        pv[(base + c) * T + x.tl] = s_best[c * TS + tid];
-        a.part_arg[(base + c) * T + x.tl] = s_arg[c * TS + tid];
-      }
-    }
+    for (int c = 0; c < (kGeneric ? 0 : CMAX); ++c)
+      if (c < C) pv[(base + c) * T + x.tl] = best[c];
+    if (kGeneric)
+      for (int c = 0; c < C; ++c) pv[(base + c) * T + x.tl] = s_best[c * TS + tid];
   }
   for (int off = 16; off > 0; off >>= 1) nested += __shfl_xor_sync(0xffffffffu, nested, off);
   if ((tid & 31) == 0 && nested) atomicAdd(a.pair_counter, (unsigned long long)nested);
@@ -72,30 +72,26 @@ __global__ void finalize_kernel(const LevelLaunch a) {
   const int64_t t = a.t_lo + tl;
   const int C = a.C;
   V* dpt = (V*)a.dp + (size_t)t * C;
-  int32_t* bpt = a.bp + (size_t)t * C;
   const V* pv = (const V*)a.part_val;
   for (int c = 0; c < C; ++c) {
     V v = INF;
-    int32_t g = INT_MAX;
-    for (int64_t ch = 0; ch < a.n_chunks; ++ch) {
-      const size_t i = ((size_t)ch * C + c) * T + tl;
-      vmin_arg(v, g, pv[i], a.part_arg[i]);
-    }
+    for (int64_t ch = 0; ch < a.n_chunks; ++ch) v = min(v, pv[((size_t)ch * C + c) * T + tl]);
     dpt[c] = v;
-    bpt[c] = v == INF ? -1 : g;
   }
-  monotone_strided(dpt, bpt, 1, a.K, a.L);
+  monotone_strided(dpt, 1, a.K, a.L);
 }
 
 // dp[∅][0][0] = 0 followed by monotone_pass(0) (dp_solver.cpp:325-326)
 template <typename V>
-__global__ void init_empty_kernel(int K, int L, V* dp, int32_t* bp) {
-  const int C = (K + 1) * (L + 1);
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    const int k = c / (L + 1), l = c % (L + 1);
-    dp[c] = 0;
-    bp[c] = (k == 0 && l == 0) ? -1 : (k > 0 ? -3 : -4);
-  }
+__global__ void init_empty_kernel(int C, V* dp) {
+  for (int c = threadIdx.x; c < C; c += blockDim.x) dp[c] = 0;
+}
+
+template <typename V>
+__global__ void fill_inf_kernel(V* p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = VTraits<V>::INF;
 }
 
 __global__ void read_globaltimer_kernel(uint64_t* out) { *out = globaltimer(); }
@@ -106,20 +102,19 @@ __global__ void fill_u32_kernel(unsigned* p, int64_t n, unsigned value) {
     p[i] = value;
 }
 
-// Fewest-devices cell + argmin walk (dp_solver.cpp:332-380); one thread.
+// ---------------------------------------------------------------- traceback
+
+// Fewest-devices cell (dp_solver.cpp:337-351); one thread.
 template <typename V>
-__global__ void traceback_kernel(int64_t I, int K, int L, int W, const V* dp, const int32_t* bp,
-                                 const uint64_t* abits, TracebackOut* out, int64_t* ords,
-                                 int64_t* prevs, int32_t* cpus, uint64_t* block_bits) {
+__global__ void traceback_init_kernel(int64_t I, int K, int L, const V* dp, TraceState* st) {
   constexpr V INF = VTraits<V>::INF;
   const int lp1 = L + 1, C = (K + 1) * lp1;
-  const int64_t full = I - 1;
-  const V* row = dp + (size_t)full * C;
+  const V* row = dp + (size_t)(I - 1) * C;
   const V best = row[K * lp1 + L];
-  out->best_value = (int64_t)best;
-  out->n_blocks = 0;
+  st->best_value = (int64_t)best;
+  st->n_blocks = 0;
   if (best == INF) {
-    out->status = 1;
+    st->status = 2;  // infeasible
     return;
   }
   int bk = K, bl = L;
@@ -135,56 +130,143 @@ __global__ void traceback_kernel(int64_t I, int K, int L, int W, const V* dp, co
       }
     }
   }
-  out->best_k = bk;
-  out->best_l = bl;
-  int64_t ord = full;
-  int k = bk, l = bl, nb = 0;
-  int guard = 2 * (K + L) + 2;
-  while (!(ord == 0 && k == 0 && l == 0)) {
-    if (--guard < 0 || k < 0 || l < 0) {
-      out->status = 2;
-      return;
+  st->best_k = bk;
+  st->best_l = bl;
+  st->ord = I - 1;
+  st->k = bk;
+  st->l = bl;
+  st->status = (I - 1 == 0 && bk == 0 && bl == 0) ? 1 : 0;
+}
+
+// The direct (pre-monotone) minimum of cell (ord, k, l) and its smallest
+// argmin, one partial per CTA; sources are spread over the whole grid.
+template <typename V, bool TRAIN>
+__global__ void __launch_bounds__(256) traceback_search_kernel(const LevelLaunch a,
+                                                               const TraceState* st,
+                                                               const int32_t* level_of,
+                                                               const int64_t* level_off,
+                                                               V* part_v, int32_t* part_g) {
+  constexpr V INF = VTraits<V>::INF;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ V red_v[256];
+  __shared__ int32_t red_g[256];
+  if (st->status != 0) return;
+  const int W = a.W, K = a.K, lp1 = a.L + 1;
+  const int64_t ord = st->ord;
+  const int k = st->k, l = st->l;
+  uint64_t* tA = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* tInt = tA + W;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) {
+    tA[w] = a.abits[(size_t)ord * W + w];
+    if (TRAIN) tInt[w] = a.intbits[(size_t)ord * W + w];
+  }
+  __syncthreads();
+  const Target<V> x = target_scalars<V, TRAIN>(a, ord, 0, true);
+  const int64_t S = level_off[level_of[ord]];
+  const V* dp = (const V*)a.dp;
+  V bv = INF;
+  int32_t bg = INT_MAX;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t* sA = a.abits + (size_t)s * W;
+    bool nested = true;
+    for (int w = 0; w < W && nested; ++w) nested = (sA[w] & ~tA[w]) == 0ull;
+    if (!nested) continue;
+    bool gated;
+    V acc, cpu, mem_blk;
+    pair_cost<V, TRAIN, 1>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk);
+    if (gated) continue;
+    const V* sdp = dp + (size_t)s * a.C;
+    const int32_t base = (int32_t)(s * (K + 2));
+    if (k >= 1 && acc != INF) {
+      const int rmax = a.repl ? k : 1;
+      for (int rr = 1; rr <= rmax; ++rr) {
+        const V load = rr == 1 ? acc : replicated<V>(a, acc, mem_blk, rr);
+        vmin_arg(bv, bg, vmax(sdp[(k - rr) * lp1 + l], load), base + rr);
+      }
     }
-    const int32_t b = bp[(size_t)ord * C + k * lp1 + l];
-    if (b == -1 || b < -4) {
-      out->status = 2;
-      return;
+    if (l >= 1) vmin_arg(bv, bg, vmax(sdp[k * lp1 + l - 1], cpu), base + K + 1);
+  }
+  red_v[threadIdx.x] = bv;
+  red_g[threadIdx.x] = bg;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      V v = red_v[threadIdx.x];
+      int32_t g = red_g[threadIdx.x];
+      vmin_arg(v, g, red_v[threadIdx.x + off], red_g[threadIdx.x + off]);
+      red_v[threadIdx.x] = v;
+      red_g[threadIdx.x] = g;
     }
-    if (b == -3) {
-      --k;
-      continue;
-    }
-    if (b == -4) {
-      --l;
-      continue;
-    }
-    // arg = prev*(K+2) + r (accelerator block on r replicas) or + K+1 (CPU)
-    const int64_t prev = (int64_t)(b / (K + 2));
-    const int code = b % (K + 2);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part_v[blockIdx.x] = red_v[0];
+    part_g[blockIdx.x] = red_g[0];
+  }
+}
+
+// Replay monotone_pass's strict tests for cell (ord, k, l) and step.
+template <typename V>
+__global__ void traceback_decide_kernel(int K, int L, int W, const V* dp, const uint64_t* abits,
+                                        const V* part_v, const int32_t* part_g, int n_parts,
+                                        TraceState* st, int64_t* ords, int64_t* prevs,
+                                        int32_t* kinds, uint64_t* block_bits) {
+  constexpr V INF = VTraits<V>::INF;
+  if (st->status != 0 || threadIdx.x != 0) return;
+  V dv = INF;
+  int32_t dg = INT_MAX;
+  for (int i = 0; i < n_parts; ++i) vmin_arg(dv, dg, part_v[i], part_g[i]);
+  const int lp1 = L + 1, C = (K + 1) * lp1;
+  const int64_t ord = st->ord;
+  int k = st->k, l = st->l;
+  const V* row = dp + (size_t)ord * C;
+  const int c = k * lp1 + l;
+  V w = dv;
+  int kind = 0;  // 0 block, 3 waste accelerator, 4 waste CPU
+  if (k > 0 && row[c - lp1] < w) {
+    w = row[c - lp1];
+    kind = 3;
+  }
+  if (l > 0 && row[c - 1] < w) {
+    w = row[c - 1];
+    kind = 4;
+  }
+  if (w != row[c] || w == INF) {
+    st->status = 3;  // dp reconstruction stuck (dp_solver.cpp:357)
+    return;
+  }
+  int64_t next = ord;
+  if (kind == 3) {
+    --k;
+  } else if (kind == 4) {
+    --l;
+  } else {
+    const int64_t prev = dg / (K + 2);
+    const int code = dg % (K + 2);
     const int cpu = code == K + 1;
     const int repl = cpu ? 1 : code;
-    if ((!cpu && repl > k) || prev >= ord) {
-      out->status = 2;
-      return;
-    }
+    const int nb = st->n_blocks;
     ords[nb] = ord;
     prevs[nb] = prev;
-    cpus[nb] = cpu | (repl << 1);
-    for (int w = 0; w < W; ++w)
-      block_bits[(size_t)nb * W + w] = abits[(size_t)ord * W + w] & ~abits[(size_t)prev * W + w];
-    ++nb;
+    kinds[nb] = cpu | (repl << 1);
+    for (int x = 0; x < W; ++x)
+      block_bits[(size_t)nb * W + x] = abits[(size_t)ord * W + x] & ~abits[(size_t)prev * W + x];
+    st->n_blocks = nb + 1;
     if (cpu) --l;
     else k -= repl;
-    ord = prev;
+    next = prev;
   }
-  out->n_blocks = nb;
-  out->status = 0;
+  st->ord = next;
+  st->k = k;
+  st->l = l;
+  if (next == 0 && k == 0 && l == 0) st->status = 1;
 }
 
 template <typename V, int LP1, int KP1MAX, bool TRAIN>
 void launch_tile(const LevelLaunch& L, dim3 grid, cudaStream_t st) {
   size_t smem = (size_t)L.W * kTileTargets * sizeof(uint64_t) * (TRAIN ? 2 : 1);
-  if (LP1 == 0) smem += (size_t)L.C * kTileTargets * (sizeof(V) + sizeof(int32_t));
+  if (LP1 == 0) smem += (size_t)L.C * kTileTargets * sizeof(V);
   auto kern = transition_kernel<V, LP1, KP1MAX, TRAIN>;
   static bool configured = false;
   if (!configured) {
@@ -202,8 +284,31 @@ void dispatch_tile(const LevelLaunch& L, dim3 grid, cudaStream_t st) {
   if (lp1 == 1 && kp1 <= 17) return launch_tile<V, 1, 17, TRAIN>(L, grid, st);
   if (lp1 == 2 && kp1 <= 9) return launch_tile<V, 2, 9, TRAIN>(L, grid, st);
   if (lp1 == 3 && kp1 <= 9) return launch_tile<V, 3, 9, TRAIN>(L, grid, st);
-  if (lp1 == 5 && kp1 <= 9 && sizeof(V) == 4) return launch_tile<V, 5, 9, TRAIN>(L, grid, st);
+  if (lp1 == 5 && kp1 <= 9) return launch_tile<V, 5, 9, TRAIN>(L, grid, st);
   return launch_tile<V, 0, 0, TRAIN>(L, grid, st);
+}
+
+template <typename V>
+void traceback_t(const LevelLaunch& L, const int32_t* level_of, const int64_t* level_off,
+                 int64_t I, int sm_count, TraceBuffers& b, cudaStream_t st) {
+  traceback_init_kernel<V><<<1, 1, 0, st>>>(I, L.K, L.L, (const V*)L.dp, b.state);
+  count_launch();
+  const int grid = b.n_parts;
+  const size_t smem = (size_t)L.W * sizeof(uint64_t) * 2;
+  for (int step = 0; step <= L.K + L.L; ++step) {
+    if (L.training)
+      traceback_search_kernel<V, true><<<grid, 256, smem, st>>>(
+          L, b.state, level_of, level_off, (V*)b.part_v, b.part_g);
+    else
+      traceback_search_kernel<V, false><<<grid, 256, smem, st>>>(
+          L, b.state, level_of, level_off, (V*)b.part_v, b.part_g);
+    traceback_decide_kernel<V><<<1, 32, 0, st>>>(L.K, L.L, L.W, (const V*)L.dp, L.abits,
+                                                 (const V*)b.part_v, b.part_g, grid, b.state,
+                                                 b.ords, b.prevs, b.kinds, b.block_bits);
+    count_launch();
+    count_launch();
+  }
+  (void)sm_count;
 }
 
 }  // namespace
@@ -230,9 +335,17 @@ void launch_finalize(const LevelLaunch& L, cudaStream_t st) {
   count_launch();
 }
 
-void launch_init_empty(int value_bits, int K, int L, void* dp, int32_t* bp, cudaStream_t st) {
-  if (value_bits == 32) init_empty_kernel<int32_t><<<1, 128, 0, st>>>(K, L, (int32_t*)dp, bp);
-  else init_empty_kernel<int64_t><<<1, 128, 0, st>>>(K, L, (int64_t*)dp, bp);
+void launch_init_empty(int value_bits, int K, int L, void* dp, cudaStream_t st) {
+  const int C = (K + 1) * (L + 1);
+  if (value_bits == 32) init_empty_kernel<int32_t><<<1, 128, 0, st>>>(C, (int32_t*)dp);
+  else init_empty_kernel<int64_t><<<1, 128, 0, st>>>(C, (int64_t*)dp);
+  count_launch();
+}
+
+void launch_fill_inf(int value_bits, void* p, int64_t n, cudaStream_t st) {
+  const int blocks = (int)std::min<int64_t>(1024, (n + 255) / 256 + 1);
+  if (value_bits == 32) fill_inf_kernel<int32_t><<<blocks, 256, 0, st>>>((int32_t*)p, n);
+  else fill_inf_kernel<int64_t><<<blocks, 256, 0, st>>>((int64_t*)p, n);
   count_launch();
 }
 
@@ -246,17 +359,10 @@ void launch_read_globaltimer(uint64_t* out, cudaStream_t st) {
   count_launch();
 }
 
-void launch_traceback(int value_bits, int64_t I, int K, int L, int W, const void* dp,
-                      const int32_t* bp, const uint64_t* abits, TracebackOut* out,
-                      int64_t* ords, int64_t* prevs, int32_t* cpus, uint64_t* block_bits,
-                      cudaStream_t st) {
-  if (value_bits == 32)
-    traceback_kernel<int32_t><<<1, 1, 0, st>>>(I, K, L, W, (const int32_t*)dp, bp, abits, out, ords,
-                                               prevs, cpus, block_bits);
-  else
-    traceback_kernel<int64_t><<<1, 1, 0, st>>>(I, K, L, W, (const int64_t*)dp, bp, abits, out, ords,
-                                               prevs, cpus, block_bits);
-  count_launch();
+void launch_traceback(const LevelLaunch& L, const int32_t* level_of, const int64_t* level_off,
+                      int64_t I, int sm_count, TraceBuffers& b, cudaStream_t st) {
+  if (L.value_bits == 32) traceback_t<int32_t>(L, level_of, level_off, I, sm_count, b, st);
+  else traceback_t<int64_t>(L, level_of, level_off, I, sm_count, b, st);
 }
 
 }  // namespace dsg
