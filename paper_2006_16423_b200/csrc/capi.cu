@@ -197,6 +197,7 @@ struct Prepared {
   std::vector<uint64_t> succ_real, pred_real, pred_u, succ_u, twins, bw_succ, bw_from, bw_to,
       bwset;
   std::vector<int32_t> out_off, out_adj, in_off, in_adj;
+  std::vector<int32_t> pu_off, pu_adj, su_off, su_adj;  // universe CSR, unique
   int64_t D = 1;
   int value_bits = 64;
   int64_t mlim = 0;
@@ -442,6 +443,21 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
   }
   if (P.out_adj.empty()) P.out_adj.push_back(0);
   if (P.in_adj.empty()) P.in_adj.push_back(0);
+  // the same universe adjacency as lists (from the bitsets: unique entries)
+  auto to_csr = [&](const std::vector<uint64_t>& bs, std::vector<int32_t>& off,
+                    std::vector<int32_t>& adj) {
+    off.assign(n + 1, 0);
+    adj.clear();
+    for (int v = 0; v < n; ++v) {
+      for (int k = 0; k < W; ++k)
+        for (uint64_t s = bs[(size_t)v * W + k]; s; s &= s - 1)
+          adj.push_back((k << 6) | __builtin_ctzll(s));
+      off[v + 1] = (int32_t)adj.size();
+    }
+    if (adj.empty()) adj.push_back(0);
+  };
+  to_csr(P.pred_u, P.pu_off, P.pu_adj);
+  to_csr(P.succ_u, P.su_off, P.su_adj);
 
   // reachability_within(g, backward) for the general training gate
   // (graph.cpp:291-345): rows in reverse topological order
@@ -495,6 +511,7 @@ T* upload(DeviceCtx& ctx, const std::string& name, const std::vector<T>& v) {
 struct DeviceGraph {
   DevGraph g;
   uint8_t* in_universe;
+  int32_t *pu_off, *pu_adj, *su_off, *su_adj;
 };
 
 DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P, const std::string& prefix) {
@@ -522,6 +539,10 @@ DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P, const std::string& p
   g.in_real_off = upload(ctx, prefix + "in_off", P.in_off);
   g.in_real_adj = upload(ctx, prefix + "in_adj", P.in_adj);
   d.in_universe = upload(ctx, prefix + "in_universe", P.in_universe);
+  d.pu_off = upload(ctx, prefix + "pu_off", P.pu_off);
+  d.pu_adj = upload(ctx, prefix + "pu_adj", P.pu_adj);
+  d.su_off = upload(ctx, prefix + "su_off", P.su_off);
+  d.su_adj = upload(ctx, prefix + "su_adj", P.su_adj);
   return d;
 }
 
@@ -548,10 +569,18 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
     L.pred_u = dg.g.pred_u;
     L.succ_u = dg.g.succ_u;
     L.in_universe = dg.in_universe;
+    L.pu_off = dg.pu_off;
+    L.pu_adj = dg.pu_adj;
+    L.su_off = dg.su_off;
+    L.su_adj = dg.su_adj;
+    L.n_pu = (int)P.pu_off[P.n];
+    L.n_su = (int)P.su_off[P.n];
     L.bits = ctx.get_t<uint64_t>("enum.bits", (size_t)cap * W);
     L.maxm = ctx.get_t<uint64_t>("enum.maxm", (size_t)cap * W);
     L.addm = ctx.get_t<uint64_t>("enum.addm", (size_t)cap * W);
     L.level_of = ctx.get_t<int32_t>("enum.level_of", (size_t)cap);
+    L.spill_par = ctx.get_t<int32_t>("enum.spill_par", (size_t)cap);
+    L.spill_v = ctx.get_t<int32_t>("enum.spill_v", (size_t)cap);
     L.cap = cap;
     L.budget = budget_eff;
     L.level_off = lvl_d;

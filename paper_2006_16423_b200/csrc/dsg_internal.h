@@ -24,6 +24,14 @@ struct EnumLaunch {
   const uint64_t* pred_u;
   const uint64_t* succ_u;
   const uint8_t* in_universe;
+  // universe-restricted adjacency, unique entries (nullptr: bitset path)
+  const int32_t* pu_off;  // [n + 1] predecessors
+  const int32_t* pu_adj;
+  const int32_t* su_off;  // [n + 1] successors
+  const int32_t* su_adj;
+  int n_pu, n_su;
+  int32_t* spill_par;  // [cap] scratch
+  int32_t* spill_v;
   uint64_t* bits;
   uint64_t* maxm;
   uint64_t* addm;

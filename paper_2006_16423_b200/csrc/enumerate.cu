@@ -21,6 +21,8 @@
 // Levels are tiny compared with the DP (< 1 % of the work),
 // so the level loop runs inside ONE persistent CTA with __syncthreads()
 // between levels: no host round trip and no grid barrier per level.
+#include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
 #include <cstdint>
 
 #include "dsg_device.cuh"
@@ -29,6 +31,8 @@
 namespace dsg {
 
 namespace {
+
+namespace cg = cooperative_groups;
 
 constexpr int kEnumThreads = 1024;
 
@@ -85,6 +89,14 @@ struct EnumArgs {
   const uint64_t* pred_u;
   const uint64_t* succ_u;
   const uint8_t* in_universe;
+  const int32_t* pu_off;
+  const int32_t* pu_adj;
+  const int32_t* su_off;
+  const int32_t* su_adj;
+  int n_pu, n_su;      // adjacency list lengths
+  int32_t* spill_par;  // [cap] warp mode: accepted pairs beyond kAccCap
+  int32_t* spill_v;
+  int csr_in_smem;     // stage the adjacency in shared memory
   uint64_t* bits;      // [cap][W]
   uint64_t* maxm;      // [cap][W]
   uint64_t* addm;      // [cap][W]
@@ -103,12 +115,307 @@ struct EnumArgs {
   int64_t table_cap;
 };
 
+// Warp-resident mode for narrow levels: the frontier (parents and children,
+// bits / maximal / addable words each) lives in shared memory, up to
+// small_cap(W) ideals per level; accepted (parent, node) pairs beyond
+// kAccCap spill to global scratch.
+constexpr int kAccCap = 512;
+
+__host__ __device__ __forceinline__ int small_cap(int W) {
+  const int c = (96 * 1024) / (2 * 3 * W * (int)sizeof(uint64_t));
+  return c < 64 ? c : 64;
+}
+
+__host__ __device__ __forceinline__ size_t enum_warp_bytes(int W) {
+  return (size_t)2 * small_cap(W) * 3 * W * sizeof(uint64_t) +
+         (size_t)(kAccCap * 2 + 2 * 64) * sizeof(int32_t);
+}
+
+__host__ __device__ __forceinline__ size_t enum_csr_bytes(int n, int n_pu, int n_su) {
+  return (size_t)(2 * (n + 1) + n_pu + n_su) * sizeof(int32_t);
+}
+
+// Universe adjacency (unique entries); staged in shared memory when it fits.
+struct Adj {
+  const int32_t* pu_off;
+  const int32_t* pu_adj;
+  const int32_t* su_off;
+  const int32_t* su_adj;
+};
+
+__device__ __forceinline__ bool bit_of(const uint64_t* s, int u) {
+  return (s[u >> 6] >> (u & 63)) & 1ull;
+}
+
+// Canonical-parent expansion of one level [lo, hi) (ideals.cpp:38-48
+// restated as set algebra on the parent's masks):
+//   canonical  ⇔ #(maximal ∩ above(v)) == #(pred(v) ∩ maximal ∩ above(v))
+//   max(J∪v)   = (max(J) \ pred(v)) ∪ {v}
+//   add(J∪v)   = (add(J) \ {v}) ∪ {y ∈ succ(v) : pred(y) ⊆ J ∪ {v}}
+//
+// Wide levels: one thread per parent, masks in local memory.
+__device__ void expand_thread(const EnumArgs& a, const Adj& g, int64_t lo, int64_t hi, int level,
+                              unsigned long long* s_next) {
+  const int W = a.W;
+  for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+    uint64_t J[kMaxWords], M[kMaxWords], A[kMaxWords], T[kMaxWords];
+    for (int w = 0; w < W; ++w) {
+      J[w] = a.bits[(size_t)p * W + w];
+      M[w] = a.maxm[(size_t)p * W + w];
+      A[w] = a.addm[(size_t)p * W + w];
+    }
+    for (int w = 0; w < W; ++w) {
+      uint64_t cand = A[w];
+      while (cand) {
+        const int b = __ffsll((long long)cand) - 1;
+        cand &= cand - 1;
+        const int v = (w << 6) | b;
+        const int p0 = g.pu_off[v], p1 = g.pu_off[v + 1];
+        int above = 0;
+        for (int x = w; x < W; ++x) above += __popcll(M[x] & above_mask(v, x));
+        if (above) {
+          int covered = 0;
+          for (int e = p0; e < p1; ++e) {
+            const int u = g.pu_adj[e];
+            covered += (u > v && bit_of(M, u)) ? 1 : 0;
+          }
+          if (covered != above) continue;
+        }
+        const unsigned long long slot = atomicAdd(s_next, 1ull);
+        if ((int64_t)slot >= a.cap) continue;
+        const uint64_t vb = 1ull << b;
+        for (int x = 0; x < W; ++x) T[x] = M[x];
+        for (int e = p0; e < p1; ++e) {
+          const int u = g.pu_adj[e];
+          T[u >> 6] &= ~(1ull << (u & 63));
+        }
+        T[w] |= vb;
+        for (int x = 0; x < W; ++x) {
+          a.bits[slot * W + x] = J[x] | (x == w ? vb : 0ull);
+          a.maxm[slot * W + x] = T[x];
+        }
+        for (int x = 0; x < W; ++x) T[x] = A[x];
+        T[w] &= ~vb;
+        const int s1 = g.su_off[v + 1];
+        for (int e = g.su_off[v]; e < s1; ++e) {
+          const int y = g.su_adj[e];
+          bool ok = true;
+          const int f1 = g.pu_off[y + 1];
+          for (int f = g.pu_off[y]; f < f1 && ok; ++f) {
+            const int u = g.pu_adj[f];
+            ok = u == v || bit_of(J, u);
+          }
+          if (ok) T[y >> 6] |= 1ull << (y & 63);
+        }
+        for (int x = 0; x < W; ++x) a.addm[slot * W + x] = T[x];
+        a.level_of[slot] = level + 1;
+      }
+    }
+  }
+}
+
+// Highest set bit of s strictly below bit t and strictly above bit v, or -1.
+__device__ __forceinline__ int prev_bit(const uint64_t* s, int t, int v) {
+  for (int w = (t - 1) >> 6; w >= 0 && w >= (v >> 6); --w) {
+    uint64_t x = s[w];
+    if (w == (t >> 6)) x &= (t & 63) ? (~0ull >> (64 - (t & 63))) : 0ull;
+    if (x) {
+      const int u = (w << 6) | (63 - __clzll((long long)x));
+      return u > v ? u : -1;
+    }
+  }
+  return -1;
+}
+
+// Narrow levels, run by warp 0 alone: level after level while the frontier
+// stays within small_cap(W), without a CTA barrier or an L2 round trip on
+// the dependency chain.  Phase A: lanes over (parent, word) find the
+// canonical candidates; phase B: lanes over (child, word) build the child
+// rows into global memory and into the next shared frontier.  The canonical
+// test walks the parent's maximal elements above v from the top (kept per
+// cached ideal) while they are predecessors of v.  Returns after expanding a
+// level whose successor does not qualify; *s_next then holds the new end and
+// (lo, hi, level) describe the level just expanded, exactly as after one
+// CTA-wide step.  The adjacency lists must be staged in shared memory.
+__device__ void expand_warp(const EnumArgs& a, int64_t* lo_io, int64_t* hi_io, int* level_io,
+                            unsigned long long* s_next, uint64_t* smem, int* s_nc) {
+  const int W = a.W;
+  const int lane = threadIdx.x & 31;
+  const int cap_small = small_cap(W);
+  const int R = 3 * W;  // words per cached ideal: J | M | A
+  uint64_t* par = smem;
+  uint64_t* chi = smem + (size_t)cap_small * R;
+  int32_t* acc_i = reinterpret_cast<int32_t*>(smem + (size_t)2 * cap_small * R);
+  int32_t* acc_v = acc_i + kAccCap;
+  int32_t* top_p = acc_v + kAccCap;
+  int32_t* top_c = top_p + 64;
+  const int32_t* pu_off = reinterpret_cast<const int32_t*>(smem + enum_warp_bytes(W) / sizeof(uint64_t));
+  const int32_t* su_off = pu_off + (a.n + 1);
+  const int32_t* pu_adj = su_off + (a.n + 1);
+  const int32_t* su_adj = pu_adj + a.n_pu;
+  // lane items (i, x) over a [count][W] grid: start (lane / W, lane % W),
+  // step 32 = (di, dx)
+  const int i0 = lane / W, x0 = lane % W, di = 32 / W, dx = 32 % W;
+  int64_t lo = *lo_io, hi = *hi_io;
+  int level = *level_io;
+  {
+    const int nP0 = (int)(hi - lo);
+    for (int j = lane; j < nP0; j += 32) top_p[j] = -1;
+    __syncwarp();
+    for (int i = i0, x = x0; i < nP0;) {
+      const size_t src = (size_t)(lo + i) * W + x;
+      const uint64_t m = a.maxm[src];
+      par[(size_t)i * R + x] = a.bits[src];
+      par[(size_t)i * R + W + x] = m;
+      par[(size_t)i * R + 2 * W + x] = a.addm[src];
+      if (m) atomicMax(&top_p[i], (x << 6) | (63 - __clzll((long long)m)));
+      x += dx;
+      i += di;
+      if (x >= W) {
+        x -= W;
+        ++i;
+      }
+    }
+    __syncwarp();
+  }
+  while (true) {
+    const int nP = (int)(hi - lo);
+    if (lane == 0) *s_nc = 0;
+    __syncwarp();
+    // phase A: canonical candidates
+    for (int i = i0, x = x0; i < nP;) {
+      uint64_t cand = par[(size_t)i * R + 2 * W + x];
+      if (cand) {
+        const uint64_t* M = par + (size_t)i * R + W;
+        const int top = top_p[i];
+        do {
+          const int b = __ffsll((long long)cand) - 1;
+          cand &= cand - 1;
+          const int v = (x << 6) | b;
+          const int p0 = pu_off[v], p1 = pu_off[v + 1];
+          bool canon = true;
+          for (int t = top; t > v && canon; t = prev_bit(M, t, v)) {
+            bool is_pred = false;
+            for (int e = p0; e < p1; ++e) is_pred |= pu_adj[e] == t;
+            canon = is_pred;
+          }
+          if (!canon) continue;
+          const int k = atomicAdd(s_nc, 1);
+          const int64_t slot = hi + k;
+          if (k < kAccCap) {
+            acc_i[k] = i;
+            acc_v[k] = v;
+          } else if (slot < a.cap) {
+            a.spill_par[slot] = i;
+            a.spill_v[slot] = v;
+          }
+        } while (cand);
+      }
+      x += dx;
+      i += di;
+      if (x >= W) {
+        x -= W;
+        ++i;
+      }
+    }
+    for (int j = lane; j < cap_small; j += 32) top_c[j] = -1;
+    __syncwarp();
+    const int nC = *s_nc;
+    // phase B: child rows
+    for (int k = i0, x = x0; k < nC;) {
+      const int64_t slot = hi + k;
+      if (slot >= a.cap) break;
+      const int i = k < kAccCap ? acc_i[k] : a.spill_par[slot];
+      const int v = k < kAccCap ? acc_v[k] : a.spill_v[slot];
+      const uint64_t* J = par + (size_t)i * R;
+      const uint64_t bx = (v >> 6) == x ? 1ull << (v & 63) : 0ull;
+      uint64_t m = J[W + x];
+      const int p1 = pu_off[v + 1];
+      for (int e = pu_off[v]; e < p1; ++e) {
+        const int u = pu_adj[e];
+        if ((u >> 6) == x) m &= ~(1ull << (u & 63));
+      }
+      m |= bx;
+      uint64_t ad = J[2 * W + x] & ~bx;
+      const int s1 = su_off[v + 1];
+      for (int e = su_off[v]; e < s1; ++e) {
+        const int y = su_adj[e];
+        if ((y >> 6) != x) continue;
+        bool ok = true;
+        const int f1 = pu_off[y + 1];
+        for (int f = pu_off[y]; f < f1 && ok; ++f) {
+          const int u = pu_adj[f];
+          ok = u == v || bit_of(J, u);
+        }
+        if (ok) ad |= 1ull << (y & 63);
+      }
+      const uint64_t jb = J[x] | bx;
+      a.bits[slot * W + x] = jb;
+      a.maxm[slot * W + x] = m;
+      a.addm[slot * W + x] = ad;
+      if (k < cap_small) {
+        chi[(size_t)k * R + x] = jb;
+        chi[(size_t)k * R + W + x] = m;
+        chi[(size_t)k * R + 2 * W + x] = ad;
+        if (m) atomicMax(&top_c[k], (x << 6) | (63 - __clzll((long long)m)));
+      }
+      if (x == 0) a.level_of[slot] = level + 1;
+      x += dx;
+      k += di;
+      if (x >= W) {
+        x -= W;
+        ++k;
+      }
+    }
+    __syncwarp();
+    const int64_t new_hi = hi + nC;
+    if (lane == 0) *s_next = (unsigned long long)new_hi;
+    __syncwarp();
+    if (nC == 0 || nC > cap_small || new_hi > a.budget || new_hi > a.cap) break;
+    // advance without leaving the warp (the CTA step's bookkeeping)
+    lo = hi;
+    hi = new_hi;
+    ++level;
+    if (lane == 0) a.level_off[level + 1] = hi;
+    uint64_t* t = par;
+    par = chi;
+    chi = t;
+    int32_t* tt = top_p;
+    top_p = top_c;
+    top_c = tt;
+  }
+  *lo_io = lo;
+  *hi_io = hi;
+  *level_io = level;
+}
+
 __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs a) {
   const int W = a.W;
+  extern __shared__ uint64_t s_dyn[];
   __shared__ unsigned long long s_next;
   __shared__ unsigned long long s_cand;
   __shared__ int s_stop;
+  __shared__ int s_nc;
+  __shared__ int64_t s_lo, s_hi;
+  __shared__ int s_level;
   const int tid = threadIdx.x;
+
+  // adjacency: shared-memory copy behind the group staging when it fits
+  Adj adj{a.pu_off, a.pu_adj, a.su_off, a.su_adj};
+  if (a.csr_in_smem && !a.hash_mode) {
+    int32_t* c = reinterpret_cast<int32_t*>(s_dyn + enum_warp_bytes(W) / sizeof(uint64_t));
+    int32_t* pu_off = c;
+    int32_t* su_off = pu_off + (a.n + 1);
+    int32_t* pu_adj = su_off + (a.n + 1);
+    int32_t* su_adj = pu_adj + a.n_pu;
+    for (int i = tid; i <= a.n; i += blockDim.x) {
+      pu_off[i] = a.pu_off[i];
+      su_off[i] = a.su_off[i];
+    }
+    for (int i = tid; i < a.n_pu; i += blockDim.x) pu_adj[i] = a.pu_adj[i];
+    for (int i = tid; i < a.n_su; i += blockDim.x) su_adj[i] = a.su_adj[i];
+    adj = Adj{pu_off, pu_adj, su_off, su_adj};
+  }
 
   // the empty ideal, ideals.cpp:23-24
   for (int w = tid; w < W; w += blockDim.x) {
@@ -140,28 +447,21 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs
     }
     __syncthreads();
     if (!a.hash_mode) {
-      for (int64_t p = lo + tid; p < hi; p += blockDim.x) {
-        const uint64_t* pj = a.bits + (size_t)p * W;
-        const uint64_t* pm = a.maxm + (size_t)p * W;
-        const uint64_t* pa = a.addm + (size_t)p * W;
-        for (int w = 0; w < W; ++w) {
-          uint64_t s = pa[w];
-          while (s) {
-            int b = __ffsll((long long)s) - 1;
-            s &= s - 1;
-            int v = (w << 6) | b;
-            // canonical parent: no maximal element above v survives
-            const uint64_t* pv = a.pred_u + (size_t)v * W;
-            bool canon = true;
-            for (int k = 0; k < W && canon; ++k) canon = (pm[k] & ~pv[k] & above_mask(v, k)) == 0ull;
-            if (!canon) continue;
-            unsigned long long slot = atomicAdd(&s_next, 1ull);
-            if ((int64_t)slot >= a.cap) continue;
-            write_child(W, v, pj, pm, pa, a.pred_u, a.succ_u, a.bits + slot * W,
-                        a.maxm + slot * W, a.addm + slot * W);
-            a.level_of[slot] = level + 1;
+      if (a.csr_in_smem && hi - lo <= small_cap(W)) {
+        if (tid < 32) {
+          expand_warp(a, &lo, &hi, &level, &s_next, s_dyn, &s_nc);
+          if (tid == 0) {
+            s_lo = lo;
+            s_hi = hi;
+            s_level = level;
           }
         }
+        __syncthreads();
+        lo = s_lo;
+        hi = s_hi;
+        level = s_level;
+      } else {
+        expand_thread(a, adj, lo, hi, level, &s_next);
       }
     } else {
       // phase 1: every parent writes every child into the candidate buffer
@@ -281,6 +581,10 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
   a.pred_u = L.pred_u;
   a.succ_u = L.succ_u;
   a.in_universe = L.in_universe;
+  a.pu_off = L.pu_off;
+  a.pu_adj = L.pu_adj;
+  a.su_off = L.su_off;
+  a.su_adj = L.su_adj;
   a.bits = L.bits;
   a.maxm = L.maxm;
   a.addm = L.addm;
@@ -296,7 +600,18 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
   a.cand_cap = L.cand_cap;
   a.table = L.table;
   a.table_cap = L.table_cap;
-  enumerate_levels_kernel<<<1, kEnumThreads, 0, st>>>(a);
+  a.n_pu = L.n_pu;
+  a.n_su = L.n_su;
+  a.spill_par = L.spill_par;
+  a.spill_v = L.spill_v;
+  size_t smem = enum_warp_bytes(a.W);
+  const size_t csr = enum_csr_bytes(a.n, a.n_pu, a.n_su);
+  a.csr_in_smem = (!a.hash_mode && smem + csr <= 200 * 1024) ? 1 : 0;
+  if (a.csr_in_smem) smem += csr;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(enumerate_levels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  enumerate_levels_kernel<<<1, kEnumThreads, smem, st>>>(a);
   count_launch();
 }
 
