@@ -659,6 +659,8 @@ struct Pipeline {
   PersistInfo pinfo{};
   bool persistent = true;
   std::vector<int64_t> n_chunks, chunk_len, item_base;
+  int4* items_d = nullptr;  // readiness-ordered work items (device)
+  ItemBuild item_build{};
   std::vector<int32_t> mode;
   int64_t total_tiles = 0, total_items = 0;
   unsigned* ctl = nullptr;  // [0] stop, [1] err, [32 + s] level s done
@@ -699,7 +701,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   D.value_bits = vb;
   D.I = I;
   D.sbits = lat.sbits;
-  D.abits = ctx.get_t<uint64_t>(pfx + "d.abits", (size_t)I * W);
+  D.AW = (W + 1) & ~1;
+  D.abits = ctx.get_t<uint64_t>(pfx + "d.abits", (size_t)I * D.AW);
   D.intbits = ctx.get_t<uint64_t>(pfx + "d.intbits", P.training ? (size_t)I * W : 1);
   D.pfx_cpu = ctx.get(pfx + "d.cpu", I * vsz);
   D.pfx_acc = ctx.get(pfx + "d.acc", I * vsz);
@@ -753,6 +756,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   if ((i128)I * (K + 2) >= ((i128)1 << 31))
     throw Fail{DSG_UNSUPPORTED, "ideal count x (accelerators + 2) exceeds the 31-bit argmin"};
   LL.abits = D.abits;
+  LL.AW = D.AW;
   LL.intbits = D.intbits;
   LL.pfx_cpu = D.pfx_cpu;
   LL.pfx_acc = D.pfx_acc;
@@ -793,19 +797,21 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   pl.item_base.assign(lat.n_levels + 1, 0);
   std::vector<int64_t> tile_base(lat.n_levels, 0), part_base(lat.n_levels, 0);
   std::vector<int64_t> chunk_lo, chunk_base(lat.n_levels, 0);
-  std::vector<int64_t> n_old(lat.n_levels, 0), crit_base(lat.n_levels + 1, 0),
-      bg_base(lat.n_levels + 1, 0);
   size_t part_elems = 1;
   pl.total_tiles = 0;
   pl.total_items = 0;
   // persistent, mode 0 (>= 16 targets): (32-target group, chunk) CTA items
   // whose 4 warps split the chunk; mode 1 (< 16 targets): (target, chunk)
-  // items with one source per thread.  Old sources [0, R) in cost-balanced
-  // chunks (no CTA falls behind the wavefront); the newest level's sources
-  // [R, S) in short chunks, ordered last, because only they wait for level
-  // s-1 and so sit on the critical path.  Per-level path: 128-target tiles
-  // x uniform chunks of >= 16 sources.
+  // items with one source per thread.  Items are claimed in readiness order
+  // (see the item list below).  Per-level path: 128-target tiles x uniform
+  // chunks of >= 16 sources.
   const int64_t kSmallLevel = 16;
+  // mode 0: every chunk short and implicit (chunk c = sources [c*len,
+  // (c+1)*len)) — with readiness-ordered claims the scan stays balanced and
+  // no long item sits on the critical path; mode 1: older sources in long
+  // cost-balanced chunks, the newest level in 128s (explicit boundaries)
+  int64_t chunk_len0 = 32;
+  if (const char* e = std::getenv("DSG_CHUNK_LEN")) chunk_len0 = std::max(4, std::atoi(e));
   for (int s = 1; s < lat.n_levels; ++s) {
     const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
     const int64_t S = lat.level_off[s];
@@ -822,30 +828,22 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       min_chunk = 4;
     }
     int64_t chunks = std::max<int64_t>(1, (target_items + units - 1) / units);
-    if (pl.persistent) {
+    if (pl.persistent && pl.mode[s] == 0) {
+      chunks = (S + chunk_len0 - 1) / chunk_len0;
+      chunk_base[s] = -1;
+      pl.chunk_len[s] = chunk_len0;
+    } else if (pl.persistent) {
       const int64_t R = s >= 2 ? lat.level_off[s - 1] : 0;
-      int64_t rlen, olen;
-      if (pl.mode[s] == 0) {
-        const int64_t pairs = S * T;
-        const int64_t p_item = std::max<int64_t>(8192, pairs / std::max<int64_t>(1, 2 * target_items));
-        rlen = 16;
-        olen = std::max<int64_t>(16, p_item / 32);
-      } else {
-        rlen = kTileTargets;
-        olen = kTileTargets;
-      }
+      const int64_t rlen = kTileTargets;
       const int64_t rc = (S - R + rlen - 1) / rlen;
-      const int64_t oc = (R + olen - 1) / olen;
-      olen = oc ? (R + oc - 1) / oc : 1;
+      int64_t oc = (R + kTileTargets - 1) / kTileTargets;
+      const int64_t olen = oc ? (R + oc - 1) / oc : 1;
       chunk_base[s] = (int64_t)chunk_lo.size();
       for (int64_t c = 0; c < oc; ++c) chunk_lo.push_back(std::min(R, c * olen));
       for (int64_t c = 0; c < rc; ++c) chunk_lo.push_back(R + c * rlen);
       chunk_lo.push_back(S);
       chunks = oc + rc;
       pl.chunk_len[s] = 0;
-      n_old[s] = oc;
-      crit_base[s + 1] = crit_base[s] + units * rc;
-      bg_base[s + 1] = bg_base[s] + units * oc;
     } else {
       chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / min_chunk));
       const int64_t len = (S + chunks - 1) / chunks;
@@ -880,13 +878,10 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     pl.level_off_d = ctx.get_t<int64_t>(pfx + "pp.level_off", lat.level_off.size() + 1);
     CK(cudaMemcpyAsync(pl.level_off_d, lat.level_off.data(), sizeof(int64_t) * lat.level_off.size(),
                        cudaMemcpyHostToDevice, st));
-    std::vector<int32_t> lvl_of((size_t)I);
-    for (int s = 0; s < lat.n_levels; ++s)
-      for (int64_t o = lat.level_off[s]; o < lat.level_off[s + 1]; ++o) lvl_of[o] = s;
     pl.level_of_d = ctx.get_t<int32_t>(pfx + "pp.level_of", (size_t)I);
-    CK(cudaMemcpyAsync(pl.level_of_d, lvl_of.data(), sizeof(int32_t) * I, cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));  // host vectors are temporaries
-    ctx.h2d_bytes += (int64_t)(sizeof(int32_t) * I + sizeof(int64_t) * lat.level_off.size());
+    launch_level_of(pl.level_off_d, lat.n_levels, I, pl.level_of_d, st);
+    CK(cudaStreamSynchronize(st));  // the host vector is a temporary
+    ctx.h2d_bytes += (int64_t)(sizeof(int64_t) * lat.level_off.size());
   }
   if (!pl.persistent) return;
 
@@ -907,29 +902,42 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.chunk_lo = up64("pp.chunk_lo", chunk_lo);
   PP.chunk_base = up64("pp.chunk_base", chunk_base);
   PP.tile_base = up64("pp.tile_base", tile_base);
-  PP.item_base = up64("pp.item_base", pl.item_base);
   PP.part_base = up64("pp.part_base", part_base);
-  PP.total_items = pl.total_items;
-  // critical / background CTA split (env DSG_CRIT_FRAC, default 1/4)
+  PP.chunk_len0 = (int)chunk_len0;
+  // work items in readiness order, built on the device (launch_build_items):
+  // buckets by dep = level of the chunk's last source, critical items first;
+  // a sharded solve lists only this rank's units
   {
-    double frac = 0.25;
-    if (const char* e = std::getenv("DSG_CRIT_FRAC")) frac = std::atof(e);
-    const int blocks = std::max(1, pl.pinfo.blocks);
-    int cb = (int)(blocks * frac + 0.5);
-    if (blocks < 8 || frac <= 0.0) cb = 0;  // tiny grids: one combined list
-    cb = std::min(cb, blocks - 1);
-    PP.crit_blocks = std::max(cb, 0);
-    PP.n_old = up64("pp.n_old", n_old);
-    PP.crit_base = up64("pp.crit_base", crit_base);
-    PP.bg_base = up64("pp.bg_base", bg_base);
-    PP.total_crit = crit_base[lat.n_levels];
-    PP.total_bg = bg_base[lat.n_levels];
+    std::vector<int64_t> pair_off(lat.n_levels + 1, 0);
+    pl.total_items = 0;
+    for (int l = 1; l < lat.n_levels; ++l) {
+      pair_off[l + 1] = pair_off[l] + pl.n_chunks[l];
+      const int64_t T = lat.level_off[l + 1] - lat.level_off[l];
+      const int64_t units = pl.mode[l] == 0 ? (T + 31) / 32 : T;
+      const int64_t units_r =
+          pl.world > 1 ? (units > pl.rank ? (units - pl.rank + pl.world - 1) / pl.world : 0) : units;
+      pl.total_items += units_r * pl.n_chunks[l];
+    }
+    ItemBuild B{};
+    B.n_levels = lat.n_levels;
+    B.pair_off = up64("pp.pair_off", pair_off);
+    B.n_pairs = pair_off[lat.n_levels];
+    B.cnt = ctx.get_t<unsigned long long>(pfx + "pp.item_cnt", 2 * (size_t)lat.n_levels + 1);
+    B.items = ctx.get_t<int4>(pfx + "pp.items", (size_t)pl.total_items + 1);
+    B.rank = pl.rank;
+    B.world = pl.world;
+    PP.items = B.items;
+    PP.total_items = pl.total_items;
+    pl.items_d = B.items;
+    pl.item_build = B;  // launched after the mode table is on the device
   }
   {
     int32_t* mode_d = ctx.get_t<int32_t>(pfx + "pp.mode", pl.mode.size());
     CK(cudaMemcpyAsync(mode_d, pl.mode.data(), sizeof(int32_t) * pl.mode.size(),
                        cudaMemcpyHostToDevice, st));
     PP.mode = mode_d;
+    launch_build_items(PP, pl.item_build, st);
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));  // host vectors are temporaries
   }
   PP.tile_count = ctx.get_t<unsigned>(pfx + "pp.tile_count", (size_t)pl.total_tiles + 1);
@@ -937,6 +945,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   pl.ctl = ctx.get_t<unsigned>(pfx + "pp.ctl", pl.ctl_words);
   PP.stop = reinterpret_cast<int*>(pl.ctl);
   PP.err = reinterpret_cast<int*>(pl.ctl + 1);
+  PP.next = reinterpret_cast<unsigned long long*>(pl.ctl + 2);  // ctl[2..3], zeroed per solve
   PP.done = pl.ctl + 32;
   PP.keys = ctx.get_t<unsigned long long>(pfx + "pp.keys", (size_t)I * C);  // value atomics
   // peer tables: this GPU only, until a sharded session attaches its peers
@@ -970,6 +979,9 @@ void write_trace(DeviceCtx& ctx, const Pipeline& pl, const char* path) {
     std::fwrite(hdr, sizeof hdr, 1, f);
     std::fwrite(pl.lat.level_off.data(), sizeof(int64_t), pl.lat.level_off.size(), f);
     std::fwrite(pl.item_base.data(), sizeof(int64_t), pl.item_base.size(), f);
+    std::vector<int4> items((size_t)pl.total_items);
+    CK(cudaMemcpy(items.data(), pl.items_d, sizeof(int4) * items.size(), cudaMemcpyDeviceToHost));
+    std::fwrite(items.data(), sizeof(int4), items.size(), f);
     std::fwrite(pl.n_chunks.data(), sizeof(int64_t), pl.n_chunks.size(), f);
     std::vector<int64_t> m64(pl.mode.begin(), pl.mode.end());
     std::fwrite(m64.data(), sizeof(int64_t), m64.size(), f);

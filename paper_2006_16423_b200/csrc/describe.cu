@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(128) describe_kernel(DescribeLaunch a) {
     cnt[kCntLItems * stride + o] = nLI;
     return;
   }
-  for (int w = 0; w < W; ++w) a.abits[(size_t)o * W + w] = A[w];
+  for (int w = 0; w < a.AW; ++w) a.abits[(size_t)o * a.AW + w] = w < W ? A[w] : 0ull;
   if (a.training) {
     for (int w = 0; w < W; ++w) a.intbits[(size_t)o * W + w] = A[w] & ~F[w];
     a.upset[o] = up;

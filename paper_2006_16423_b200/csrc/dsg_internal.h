@@ -62,9 +62,10 @@ struct DescribeLaunch {
   int has_bw;        // graph has backward nodes (bw_reach exists)
   int value_bits;    // 32 or 64
   int64_t I;
+  int AW;            // abits row stride: W rounded up to even (16-byte rows)
   const uint64_t* sbits;  // sorted ideal bitsets [I][W]
   // outputs
-  uint64_t* abits;   // [I][W]
+  uint64_t* abits;   // [I][AW]
   uint64_t* intbits; // [I][W] training
   void* pfx_cpu;     // V[I]
   void* pfx_acc;
@@ -94,6 +95,7 @@ struct LevelLaunch {
   int has_bw;
   int fastgate;
   int K, L, C, W;
+  int AW;              // abits row stride (even: 16-byte vector loads)
   int64_t mlim;        // fixed point (clamped)
   int memcheck;
   int interleave;
@@ -147,17 +149,21 @@ struct PersistPlan {
   const int32_t* mode;       // [n_levels] 0: lanes own targets, 1: lanes own sources
   const int64_t* n_chunks;   // [n_levels] source chunks per target (group)
   const int64_t* chunk_len;  // [n_levels] (unused by the dataflow kernel)
-  const int64_t* chunk_lo;   // chunk boundaries: level s chunk c covers
-  const int64_t* chunk_base; //   [chunk_lo[b+c], chunk_lo[b+c+1]), b = chunk_base[s]
+  // chunk c of a mode-0 level covers sources [c*chunk_len0, min(.. + chunk_len0, S));
+  // mode-1 levels list their boundaries: [chunk_lo[b+c], chunk_lo[b+c+1]),
+  // b = chunk_base[s]
+  int chunk_len0;
+  const int64_t* chunk_lo;
+  const int64_t* chunk_base;
   const int64_t* tile_base;  // [n_levels] prefix of arrival counters over levels
-  const int64_t* item_base;  // [n_levels + 1] prefix of work items over levels
+  // Work items (s, unit, chunk, dep) sorted by readiness: dep = the level
+  // of the chunk's last source (the only level the item waits for — levels
+  // complete in order), then target level s.  CTAs claim them in this order
+  // from one atomic counter, so a CTA never sits on an unready item while
+  // ready ones are queued behind it.
   const int64_t* part_base;  // [n_levels] offset of each level's partials
-  // critical / background split (crit_blocks == 0: one combined list)
-  int crit_blocks;
-  const int64_t* n_old;      // [n_levels] chunks over levels <= s-2 (background)
-  const int64_t* crit_base;  // [n_levels + 1] prefix of critical items
-  const int64_t* bg_base;    // [n_levels + 1] prefix of background items
-  int64_t total_crit, total_bg;
+  const int4* items;         // [total_items]
+  unsigned long long* next;  // claim counter, zeroed per solve
   const int32_t* level_of;   // [I] level of each ordinal
   int64_t total_items;
   unsigned* tile_count;      // [total counters], zeroed
@@ -186,6 +192,19 @@ struct PersistInfo {
   int launch_error;
 };
 
+// Device-side item list (persistent.cu): counting sort of every (level,
+// chunk) pair's units by dependency level, the critical items (target level
+// = dep + 1) first inside each bucket.
+struct ItemBuild {
+  int n_levels;
+  const int64_t* pair_off;   // [n_levels + 1] prefix of chunks over levels
+  int64_t n_pairs;
+  unsigned long long* cnt;   // [2 * n_levels + 1] scratch
+  int4* items;               // [total_items] out
+  int rank, world;
+};
+void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t st);
+
 void query_persistent(const LevelLaunch& L, PersistInfo* info);
 void launch_persistent(const LevelLaunch& L, const PersistPlan& P, cudaStream_t st,
                        PersistInfo* info);
@@ -194,6 +213,8 @@ void launch_fill_u32(unsigned* p, int64_t n, unsigned value, cudaStream_t st);
 void launch_finalize(const LevelLaunch& L, cudaStream_t st);
 void launch_init_empty(int value_bits, int K, int L, void* dp, cudaStream_t st);
 void launch_fill_inf(int value_bits, void* p, int64_t n, cudaStream_t st);
+void launch_level_of(const int64_t* level_off, int n_levels, int64_t I, int32_t* level_of,
+                     cudaStream_t st);
 
 // Traceback state on the device (transition.cu).
 struct TraceState {

@@ -5,13 +5,13 @@
 // /root/reference/proj/src/dp_solver.cpp:319-330).  dp[I] depends only on
 // dp[I'] for I' ⊊ I, all in earlier levels, so:
 //
-//   * the work is a static, level-ordered list of items (host plan,
-//     capi.cu); CTA b takes items b, b+G, b+2G, ... in order (optionally two
-//     lists: critical newest-level chunks and background older chunks);
+//   * the work is a list of items (host plan, capi.cu) sorted by readiness;
+//     CTAs claim the next item from one atomic counter;
 //   * an item scans one chunk of source ordinals for a unit of targets of
-//     level s and first waits (spin on per-level completion counters) only
-//     until the levels its chunk covers are finished — the chunks that cover
-//     old levels start long before level s-1 is done, so levels overlap;
+//     level s and first waits (spin on the per-level completion counter)
+//     only until the last level its chunk covers is finished — levels
+//     complete in order, and the chunks that cover old levels start long
+//     before level s-1 is done, so levels overlap;
 //   * every item merges its per-target cell minima (value-only: the argmin
 //     is recovered for the optimal path during traceback); the item that
 //     arrives last for a unit (atomic arrival counter) applies monotone_pass
@@ -59,19 +59,18 @@ __device__ __forceinline__ void atomic_min_v(int64_t* p, int64_t v) {
   atomicMin(reinterpret_cast<long long*>(p), (long long)v);
 }
 
-// Wait until levels [j_lo, j_hi] are complete.  Returns false on stop/err.
-__device__ bool wait_levels(const PersistPlan& p, int j_lo, int j_hi) {
+// Wait until level j is complete (then so are all levels below it: every
+// unit of level j consumes all of level j-1).  Returns false on stop/err.
+__device__ bool wait_level(const PersistPlan& p, int j) {
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
     s_ok = 1;
-    uint64_t t0 = 0;
-    for (int j = j_lo; j <= j_hi && s_ok; ++j) {
-      const unsigned need = (unsigned)(p.level_off[j + 1] - p.level_off[j]);
-      if (ld_relaxed_sys(p.done + j) >= need) continue;
+    const unsigned need = (unsigned)(p.level_off[j + 1] - p.level_off[j]);
+    if (ld_relaxed_sys(p.done + j) < need) {
       // polite polling: back off up to ~1 us so the spinning warp does not
       // steal issue slots from the co-resident CTAs doing the real work
       unsigned ns = 32, polls = 0;
-      if (!t0) t0 = globaltimer();
+      const uint64_t t0 = globaltimer();
       while (ld_relaxed_sys(p.done + j) < need) {
         __nanosleep(ns);
         ns = ns < 1024 ? ns * 2 : 1024;
@@ -95,7 +94,7 @@ __device__ bool wait_levels(const PersistPlan& p, int j_lo, int j_hi) {
   return s_ok != 0;
 }
 
-template <typename V, int LP1, int KP1MAX, bool TRAIN>
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT>
 __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const LevelLaunch a,
                                                                          const PersistPlan p) {
   constexpr V INF = VTraits<V>::INF;
@@ -115,34 +114,36 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
   V* colv = g_val + (size_t)warp * C * TS + lane;
   V* keys = reinterpret_cast<V*>(p.keys);
   unsigned nested_total = 0;
-  int s = 1;  // current level (items are level ordered)
-  // Which list this CTA walks: with a split, the first crit_blocks CTAs take
-  // the critical items (chunks over the newest level, which gate the next
-  // level) and the rest the background items (older sources, ready early).
-  const bool split = p.crit_blocks > 0;
-  const bool crit = split && (int)blockIdx.x < p.crit_blocks;
-  const int64_t* base = !split ? p.item_base : (crit ? p.crit_base : p.bg_base);
-  const int64_t total = !split ? p.total_items : (crit ? p.total_crit : p.total_bg);
-  const int64_t first = !split ? blockIdx.x : (crit ? blockIdx.x : blockIdx.x - p.crit_blocks);
-  const int64_t stride = !split ? gridDim.x : (crit ? p.crit_blocks : gridDim.x - p.crit_blocks);
+  __shared__ long long s_gi;
+  if (tid == 0) s_gi = (long long)atomicAdd(p.next, 1ull);
+  __syncthreads();
 
-  for (int64_t gi = first; gi < total; gi += stride) {
-    while (s + 1 < p.n_levels && gi >= base[s + 1]) ++s;
+  while (true) {
+    const int64_t gi = s_gi;
+    if (gi >= p.total_items) break;
+    const int4 item = __ldg(p.items + gi);
+    // claim the next item now; its latency hides behind this one
+    unsigned long long next_gi = 0;
+    if (tid == 0) next_gi = atomicAdd(p.next, 1ull);
+    const int s = item.x;
+    const int64_t unit = item.y;
+    const int64_t chunk = item.z;
     const int64_t t_lo = p.level_off[s], t_hi = p.level_off[s + 1];
     const int64_t T = t_hi - t_lo;
     const int64_t chunks = p.n_chunks[s];
     const int mode = p.mode[s];
     const size_t pb = (size_t)p.part_base[s];
-    const int64_t it = gi - base[s];
-    const int64_t units = mode == 0 ? (T + TS - 1) / TS : T;
-    const int64_t unit = it % units;
-    const int64_t chunk = it / units + ((split && crit) ? p.n_old[s] : 0);
-    if (p.world > 1 && (int)(unit % p.world) != p.rank) continue;  // another GPU's unit
-    const int64_t s0 = p.chunk_lo[p.chunk_base[s] + chunk];
-    const int64_t s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
+    int64_t s0, s1;
+    if (mode == 0) {
+      s0 = chunk * p.chunk_len0;
+      s1 = min(s0 + p.chunk_len0, t_lo);
+    } else {
+      s0 = p.chunk_lo[p.chunk_base[s] + chunk];
+      s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
+    }
     // sources [s0, s1) must be final
     const uint64_t tr0 = p.trace ? globaltimer() : 0;
-    if (!wait_levels(p, p.level_of[s0], p.level_of[s1 - 1])) break;
+    if (!wait_level(p, item.w)) break;
     const uint64_t tr1 = p.trace ? globaltimer() : 0;
     if (blockIdx.x == 0 && tid == 0 && p.deadline_ns && globaltimer() > (uint64_t)p.deadline_ns)
       atomicExch(p.stop, 1);
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
       const Target<V> x = load_target<V, TRAIN, TS>(a, t_lo, t_hi, unit, lane, s_tgt + lane,
                                                     s_int + lane, warp == 0);
       __syncthreads();
-      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS>(
+      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT>(
           a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv);
       // merge the 4 warps into warp 0 through the merge buffer
       for (int src = 1; src < kWarps; ++src) {
@@ -197,12 +198,12 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
       // ------------------------------------ lanes own sources
       const int64_t t = t_lo + unit;
       for (int w = tid; w < W; w += kTileTargets) {
-        s_tgt[w] = __ldg(a.abits + (size_t)t * W + w);
+        s_tgt[w] = __ldg(a.abits + (size_t)t * a.AW + w);
         if (TRAIN) s_int[w] = __ldg(a.intbits + (size_t)t * W + w);
       }
       __syncthreads();
       const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
-      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, 1, false, TS>(
+      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, 1, false, TS, WT>(
           a, x, s0 + tid, s1, kTileTargets, s_tgt, s_int, best, colv);
       // lanes -> warp (shuffle min) -> CTA (shared memory) -> one partial
       if (!kGeneric) {
@@ -292,12 +293,14 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
     }
     __syncthreads();
     if (p.trace && tid == 0) {
-      uint64_t* tr = p.trace + (gi + ((split && !crit) ? p.total_crit : 0)) * 4;
+      uint64_t* tr = p.trace + gi * 4;
       tr[0] = tr0;
       tr[1] = tr1;
       tr[2] = tr2;
       tr[3] = globaltimer() | (s_last ? (1ull << 63) : 0ull);
     }
+    if (tid == 0) s_gi = (long long)next_gi;
+    __syncthreads();
   }
   for (int off = 16; off > 0; off >>= 1)
     nested_total += __shfl_xor_sync(0xffffffffu, nested_total, off);
@@ -312,10 +315,10 @@ size_t persist_smem(const LevelLaunch& L, bool generic, size_t vsz) {
   return s;
 }
 
-template <typename V, int LP1, int KP1MAX, bool TRAIN>
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT = 0>
 void run_variant(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
   const size_t smem = persist_smem(L, LP1 == 0, sizeof(V));
-  auto kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN>;
+  auto kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN, WT>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -347,6 +350,14 @@ template <typename V, bool TRAIN>
 void dispatch_cells(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
   const int lp1 = L.L + 1, kp1 = L.K + 1;
   if (L.repl) return run_variant<V, 0, 0, TRAIN>(L, P, st, info);  // replication: generic cells
+  // small bitsets: target words in registers (32-bit values, the common case)
+  if constexpr (sizeof(V) == 4) {
+    if (L.W <= 8) {
+      if (lp1 == 1 && kp1 <= 9) return run_variant<V, 1, 9, TRAIN, 8>(L, P, st, info);
+      if (lp1 == 1 && kp1 <= 17) return run_variant<V, 1, 17, TRAIN, 8>(L, P, st, info);
+      if (lp1 == 2 && kp1 <= 9) return run_variant<V, 2, 9, TRAIN, 8>(L, P, st, info);
+    }
+  }
   if (lp1 == 1 && kp1 <= 9) return run_variant<V, 1, 9, TRAIN>(L, P, st, info);
   if (lp1 == 1 && kp1 <= 17) return run_variant<V, 1, 17, TRAIN>(L, P, st, info);
   if (lp1 == 2 && kp1 <= 9) return run_variant<V, 2, 9, TRAIN>(L, P, st, info);
@@ -365,7 +376,98 @@ void dispatch(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, Persi
   }
 }
 
+// ---- item list on the device
+struct PairInfo {
+  int s, dep;
+  int64_t c, units_r;
+};
+
+__device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t q) {
+  int lo = 1, hi = b.n_levels - 1;  // largest s with pair_off[s] <= q
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (b.pair_off[mid] <= q) lo = mid;
+    else hi = mid - 1;
+  }
+  PairInfo r;
+  r.s = lo;
+  r.c = q - b.pair_off[lo];
+  const int64_t S = p.level_off[lo], T = p.level_off[lo + 1] - S;
+  const int mode = p.mode[lo];
+  const int64_t s1 = mode == 0 ? min((r.c + 1) * p.chunk_len0, S)
+                               : p.chunk_lo[p.chunk_base[lo] + r.c + 1];
+  r.dep = p.level_of[s1 - 1];
+  const int64_t units = mode == 0 ? (T + kGroup - 1) / kGroup : T;
+  r.units_r = b.world > 1 ? (units > b.rank ? (units - b.rank + b.world - 1) / b.world : 0) : units;
+  return r;
+}
+
+__global__ void item_count_kernel(const PersistPlan p, const ItemBuild b) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= b.n_pairs) return;
+  const PairInfo r = pair_info(p, b, q);
+  if (r.units_r) atomicAdd(b.cnt + 2 * r.dep + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.units_r);
+}
+
+// exclusive scan of cnt[0, n) in place, one CTA
+__global__ void __launch_bounds__(1024) item_scan_kernel(unsigned long long* cnt, int n) {
+  __shared__ unsigned long long warp_sum[32];
+  const int tid = threadIdx.x, per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  unsigned long long local = 0;
+  for (int i = lo; i < hi; ++i) local += cnt[i];
+  unsigned long long incl = local;
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, off);
+    if ((tid & 31) >= off) incl += t;
+  }
+  if ((tid & 31) == 31) warp_sum[tid >> 5] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    unsigned long long w = tid < (int)(blockDim.x >> 5) ? warp_sum[tid] : 0ull;
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, w, off);
+      if (tid >= off) w += t;
+    }
+    warp_sum[tid] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  unsigned long long run = incl - local + ((tid >> 5) ? warp_sum[(tid >> 5) - 1] : 0ull);
+  for (int i = lo; i < hi; ++i) {
+    const unsigned long long v = cnt[i];
+    cnt[i] = run;
+    run += v;
+  }
+}
+
+__global__ void item_fill_kernel(const PersistPlan p, const ItemBuild b) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= b.n_pairs) return;
+  const PairInfo r = pair_info(p, b, q);
+  if (!r.units_r) return;
+  const unsigned long long pos =
+      atomicAdd(b.cnt + 2 * r.dep + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.units_r);
+  for (int64_t k = 0; k < r.units_r; ++k) {
+    const int64_t u = b.world > 1 ? b.rank + k * b.world : k;
+    b.items[pos + k] = make_int4(r.s, (int)u, (int)r.c, r.dep);
+  }
+}
+
 }  // namespace
+
+void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t st) {
+  const int n = 2 * B.n_levels;
+  cudaMemsetAsync(B.cnt, 0, sizeof(unsigned long long) * (n + 1), st);
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((B.n_pairs + threads - 1) / threads);
+  if (blocks == 0) return;
+  item_count_kernel<<<blocks, threads, 0, st>>>(P, B);
+  item_scan_kernel<<<1, 1024, 0, st>>>(B.cnt, n);
+  item_fill_kernel<<<blocks, threads, 0, st>>>(P, B);
+  count_launch();
+  count_launch();
+  count_launch();
+}
 
 void query_persistent(const LevelLaunch& L, PersistInfo* info) {
   info->query_only = 1;

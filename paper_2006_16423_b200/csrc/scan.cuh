@@ -163,7 +163,7 @@ __device__ __forceinline__ Target<V> load_target(const LevelLaunch& a, int64_t t
   const int64_t t = active ? t_lo + tl : t_lo;
   if (stage) {
     for (int w = 0; w < W; ++w) {
-      colA[w * TS] = active ? __ldg(a.abits + (size_t)t * W + w) : 0ull;
+      colA[w * TS] = active ? __ldg(a.abits + (size_t)t * a.AW + w) : 0ull;
       if (TRAIN) colInt[w * TS] = active ? __ldg(a.intbits + (size_t)t * W + w) : 0ull;
     }
   }
@@ -202,7 +202,7 @@ __device__ __forceinline__ V acc_block_cost(const LevelLaunch& a, int64_t s, con
       cout += in ? (V)__ldg(&pi->weight) : (V)0;
       cout_inf += (in && __ldg(&pi->inf)) ? 1 : 0;
     }
-    const uint64_t* sA = a.abits + (size_t)s * a.W;
+    const uint64_t* sA = a.abits + (size_t)s * a.AW;
     for (int64_t e = x.l_lo; e < x.l_hi; ++e) {
       const LEntry le = a.lentries[e];
       bool charged = false;
@@ -231,7 +231,7 @@ __device__ __forceinline__ bool pair_cost(const LevelLaunch& a, const Target<V>&
   const SrcRec r = load_rec(a.srec + s);
   gated = false;
   if (TRAIN && a.has_bw) {
-    const uint64_t* sA = a.abits + (size_t)s * a.W;
+    const uint64_t* sA = a.abits + (size_t)s * a.AW;
     if (!(a.fastgate && x.up && __ldg(a.upset + s)) && !bw_contiguous<TS>(a, tA, sA)) {
       gated = true;
       return true;
@@ -262,7 +262,10 @@ __device__ __forceinline__ V replicated(const LevelLaunch& a, V acc, V mem_blk, 
 // shared-memory column colv with stride CS (LP1 == 0: large (K+1)(L+1),
 // replication).  Source dp rows are plain (coherent) loads: inside the
 // persistent kernel other CTAs wrote them after this kernel started.
-template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int CS>
+//
+// WT > 0: W <= WT: the subset test is fully unrolled (WT/2 predicated
+// 16-byte source loads, one LOP3 per word against the shared target column).
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int CS, int WT = 0>
 __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Target<V>& x,
                                                  int64_t s0, int64_t s1, int step,
                                                  const uint64_t* tA, const uint64_t* tInt, V* best,
@@ -276,9 +279,29 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
   unsigned nested_cnt = 0;
   for (int64_t s = s0; s < s1; s += step) {
     // K2: I' ⊆ I
-    const uint64_t* __restrict__ sA = a.abits + (size_t)s * W;
-    bool nested = x.active;
-    for (int w = 0; w < W; ++w) nested &= (__ldg(sA + w) & ~tA[w * TS]) == 0ull;
+    // 16-byte source words (rows padded to even length, pad word 0); the
+    // target's pad column is never read past W
+    const ulonglong2* __restrict__ sA2 =
+        reinterpret_cast<const ulonglong2*>(a.abits + (size_t)s * a.AW);
+    uint64_t stray = 0;
+    if constexpr (WT > 0) {
+#pragma unroll
+      for (int j = 0; j < WT / 2; ++j) {
+        if (2 * j < W) {
+          const ulonglong2 v = __ldg(sA2 + j);
+          stray |= v.x & ~tA[2 * j * TS];
+          if (2 * j + 1 < W) stray |= v.y & ~tA[(2 * j + 1) * TS];
+        }
+      }
+    } else {
+#pragma unroll 4
+      for (int w = 0; w < W; w += 2) {
+        const ulonglong2 v = __ldg(sA2 + (w >> 1));
+        stray |= v.x & ~tA[w * TS];
+        if (w + 1 < W) stray |= v.y & ~tA[(w + 1) * TS];
+      }
+    }
+    const bool nested = x.active && stray == 0ull;
     if (UNIFORM && !__any_sync(0xffffffffu, nested)) continue;
     if (!nested) continue;
     ++nested_cnt;

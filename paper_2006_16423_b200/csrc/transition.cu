@@ -87,6 +87,20 @@ __global__ void init_empty_kernel(int C, V* dp) {
   for (int c = threadIdx.x; c < C; c += blockDim.x) dp[c] = 0;
 }
 
+// level of every ordinal: largest s with level_off[s] <= o
+__global__ void level_of_kernel(const int64_t* __restrict__ level_off, int n_levels, int64_t I,
+                                int32_t* __restrict__ level_of) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= I) return;
+  int lo = 0, hi = n_levels - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (level_off[mid] <= o) lo = mid;
+    else hi = mid - 1;
+  }
+  level_of[o] = lo;
+}
+
 template <typename V>
 __global__ void fill_inf_kernel(V* p, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -157,7 +171,7 @@ __global__ void __launch_bounds__(256) traceback_search_kernel(const LevelLaunch
   uint64_t* tA = reinterpret_cast<uint64_t*>(smem);
   uint64_t* tInt = tA + W;
   for (int w = threadIdx.x; w < W; w += blockDim.x) {
-    tA[w] = a.abits[(size_t)ord * W + w];
+    tA[w] = a.abits[(size_t)ord * a.AW + w];
     if (TRAIN) tInt[w] = a.intbits[(size_t)ord * W + w];
   }
   __syncthreads();
@@ -168,7 +182,7 @@ __global__ void __launch_bounds__(256) traceback_search_kernel(const LevelLaunch
   int32_t bg = INT_MAX;
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S;
        s += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t* sA = a.abits + (size_t)s * W;
+    const uint64_t* sA = a.abits + (size_t)s * a.AW;
     bool nested = true;
     for (int w = 0; w < W && nested; ++w) nested = (sA[w] & ~tA[w]) == 0ull;
     if (!nested) continue;
@@ -208,7 +222,8 @@ __global__ void __launch_bounds__(256) traceback_search_kernel(const LevelLaunch
 
 // Replay monotone_pass's strict tests for cell (ord, k, l) and step.
 template <typename V>
-__global__ void traceback_decide_kernel(int K, int L, int W, const V* dp, const uint64_t* abits,
+__global__ void traceback_decide_kernel(int K, int L, int W, int AW, const V* dp,
+                                        const uint64_t* abits,
                                         const V* part_v, const int32_t* part_g, int n_parts,
                                         TraceState* st, int64_t* ords, int64_t* prevs,
                                         int32_t* kinds, uint64_t* block_bits) {
@@ -251,7 +266,7 @@ __global__ void traceback_decide_kernel(int K, int L, int W, const V* dp, const 
     prevs[nb] = prev;
     kinds[nb] = cpu | (repl << 1);
     for (int x = 0; x < W; ++x)
-      block_bits[(size_t)nb * W + x] = abits[(size_t)ord * W + x] & ~abits[(size_t)prev * W + x];
+      block_bits[(size_t)nb * W + x] = abits[(size_t)ord * AW + x] & ~abits[(size_t)prev * AW + x];
     st->n_blocks = nb + 1;
     if (cpu) --l;
     else k -= repl;
@@ -302,7 +317,7 @@ void traceback_t(const LevelLaunch& L, const int32_t* level_of, const int64_t* l
     else
       traceback_search_kernel<V, false><<<grid, 256, smem, st>>>(
           L, b.state, level_of, level_off, (V*)b.part_v, b.part_g);
-    traceback_decide_kernel<V><<<1, 32, 0, st>>>(L.K, L.L, L.W, (const V*)L.dp, L.abits,
+    traceback_decide_kernel<V><<<1, 32, 0, st>>>(L.K, L.L, L.W, L.AW, (const V*)L.dp, L.abits,
                                                  (const V*)b.part_v, b.part_g, grid, b.state,
                                                  b.ords, b.prevs, b.kinds, b.block_bits);
     count_launch();
@@ -346,6 +361,13 @@ void launch_fill_inf(int value_bits, void* p, int64_t n, cudaStream_t st) {
   const int blocks = (int)std::min<int64_t>(1024, (n + 255) / 256 + 1);
   if (value_bits == 32) fill_inf_kernel<int32_t><<<blocks, 256, 0, st>>>((int32_t*)p, n);
   else fill_inf_kernel<int64_t><<<blocks, 256, 0, st>>>((int64_t*)p, n);
+  count_launch();
+}
+
+void launch_level_of(const int64_t* level_off, int n_levels, int64_t I, int32_t* level_of,
+                     cudaStream_t st) {
+  if (I <= 0) return;
+  level_of_kernel<<<(unsigned)((I + 255) / 256), 256, 0, st>>>(level_off, n_levels, I, level_of);
   count_launch();
 }
 

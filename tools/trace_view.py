@@ -24,6 +24,8 @@ def take(n, dt=np.int64):
 
 level_off = take(n_levels + 1)
 item_base = take(n_levels + 1)
+items = np.frombuffer(buf[off:off + 16 * total_items], dtype=np.int32).reshape(total_items, 4)
+off += 16 * total_items
 n_chunks = take(n_levels)
 mode = take(n_levels)
 tr = take(total_items * 4, np.uint64).reshape(total_items, 4)
@@ -41,13 +43,13 @@ print(f"item scan  mean {scan.mean():.2f} us  p99 {np.percentile(scan, 99):.2f} 
 print(f"item fin   mean {fin.mean():.2f} us  (finalizers {last.sum()}, mean {fin[last].mean():.2f} us)")
 rows = []
 for s in range(1, n_levels):
-    a, b = item_base[s], item_base[s + 1]
-    if b <= a:
+    sel = np.nonzero(items[:, 0] == s)[0]
+    if len(sel) == 0:
         continue
-    r = rel[a:b]
-    done = r[last[a:b], 3].max() if last[a:b].any() else float("nan")
-    rows.append((s, level_off[s + 1] - level_off[s], b - a, n_chunks[s], mode[s], r[:, 0].min(),
-                 done, scan[a:b].max()))
+    r = rel[sel]
+    done = r[last[sel], 3].max() if last[sel].any() else float("nan")
+    rows.append((s, level_off[s + 1] - level_off[s], len(sel), n_chunks[s], mode[s], r[:, 0].min(),
+                 done, scan[sel].max()))
 rows = np.array(rows)
 lat = np.diff(np.concatenate([[0], rows[:, 6]]))
 print("per-level completion gaps (us): mean %.2f  p50 %.2f  p90 %.2f  max %.2f" %
