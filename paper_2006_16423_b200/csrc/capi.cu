@@ -807,11 +807,15 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   // chunks of >= 16 sources.
   const int64_t kSmallLevel = 16;
   // mode 0: every chunk short and implicit (chunk c = sources [c*len,
-  // (c+1)*len)) — with readiness-ordered claims the scan stays balanced and
-  // no long item sits on the critical path; mode 1: older sources in long
-  // cost-balanced chunks, the newest level in 128s (explicit boundaries)
-  int64_t chunk_len0 = 32;
+  // (c+1)*len), len 48: measured best on C2/C3) — with readiness-ordered
+  // claims the scan stays balanced and no long item sits on the critical
+  // path; mode 1: older sources in long cost-balanced chunks, the newest
+  // level in 128s (explicit boundaries)
+  int64_t chunk_len0 = 48, chunk_len1 = 16;
+  unsigned poll_ns_max = 256;  // measured: 256 ns beats 1 us on C2/C3
   if (const char* e = std::getenv("DSG_CHUNK_LEN")) chunk_len0 = std::max(4, std::atoi(e));
+  if (const char* e = std::getenv("DSG_CHUNK_LEN1")) chunk_len1 = std::max(4, std::atoi(e));
+  if (const char* e = std::getenv("DSG_POLL_NS")) poll_ns_max = (unsigned)std::max(32, std::atoi(e));
   for (int s = 1; s < lat.n_levels; ++s) {
     const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
     const int64_t S = lat.level_off[s];
@@ -829,7 +833,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     }
     int64_t chunks = std::max<int64_t>(1, (target_items + units - 1) / units);
     if (pl.persistent && pl.mode[s] == 0) {
-      chunks = (S + chunk_len0 - 1) / chunk_len0;
+      const int64_t R = lat.level_off[s - 1];
+      chunks = (R + chunk_len0 - 1) / chunk_len0 + (S - R + chunk_len1 - 1) / chunk_len1;
       chunk_base[s] = -1;
       pl.chunk_len[s] = chunk_len0;
     } else if (pl.persistent) {
@@ -904,6 +909,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.tile_base = up64("pp.tile_base", tile_base);
   PP.part_base = up64("pp.part_base", part_base);
   PP.chunk_len0 = (int)chunk_len0;
+  PP.chunk_len1 = (int)chunk_len1;
+  PP.poll_ns_max = poll_ns_max;
   // work items in readiness order, built on the device (launch_build_items):
   // buckets by dep = level of the chunk's last source, critical items first;
   // a sharded solve lists only this rank's units

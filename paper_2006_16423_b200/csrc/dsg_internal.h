@@ -149,10 +149,14 @@ struct PersistPlan {
   const int32_t* mode;       // [n_levels] 0: lanes own targets, 1: lanes own sources
   const int64_t* n_chunks;   // [n_levels] source chunks per target (group)
   const int64_t* chunk_len;  // [n_levels] (unused by the dataflow kernel)
-  // chunk c of a mode-0 level covers sources [c*chunk_len0, min(.. + chunk_len0, S));
-  // mode-1 levels list their boundaries: [chunk_lo[b+c], chunk_lo[b+c+1]),
-  // b = chunk_base[s]
-  int chunk_len0;
+  // mode-0 chunks are implicit: with R = level_off[s-1] (start of the
+  // newest source level) and n_old = ceil(R / chunk_len0), chunk c < n_old
+  // covers [c*chunk_len0, min(.. + chunk_len0, R)) and chunk n_old + j the
+  // newest level's [R + j*chunk_len1, min(.. + chunk_len1, S)) — short,
+  // because those items gate level s.  Mode-1 levels list their
+  // boundaries: [chunk_lo[b+c], chunk_lo[b+c+1]), b = chunk_base[s].
+  int chunk_len0, chunk_len1;
+  unsigned poll_ns_max;      // dependency-wait backoff cap
   const int64_t* chunk_lo;
   const int64_t* chunk_base;
   const int64_t* tile_base;  // [n_levels] prefix of arrival counters over levels

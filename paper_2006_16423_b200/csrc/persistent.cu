@@ -59,6 +59,20 @@ __device__ __forceinline__ void atomic_min_v(int64_t* p, int64_t v) {
   atomicMin(reinterpret_cast<long long*>(p), (long long)v);
 }
 
+// Implicit mode-0 chunk boundaries (see PersistPlan::chunk_len0).
+__device__ __forceinline__ void mode0_chunk(const PersistPlan& p, int s, int64_t c, int64_t& s0,
+                                            int64_t& s1) {
+  const int64_t R = p.level_off[s - 1], S = p.level_off[s];
+  const int64_t n_old = (R + p.chunk_len0 - 1) / p.chunk_len0;
+  if (c < n_old) {
+    s0 = c * p.chunk_len0;
+    s1 = min(s0 + p.chunk_len0, R);
+  } else {
+    s0 = R + (c - n_old) * p.chunk_len1;
+    s1 = min(s0 + p.chunk_len1, S);
+  }
+}
+
 // Wait until level j is complete (then so are all levels below it: every
 // unit of level j consumes all of level j-1).  Returns false on stop/err.
 __device__ bool wait_level(const PersistPlan& p, int j) {
@@ -73,7 +87,7 @@ __device__ bool wait_level(const PersistPlan& p, int j) {
       const uint64_t t0 = globaltimer();
       while (ld_relaxed_sys(p.done + j) < need) {
         __nanosleep(ns);
-        ns = ns < 1024 ? ns * 2 : 1024;
+        ns = ns < p.poll_ns_max ? ns * 2 : p.poll_ns_max;
         if ((++polls & 63) != 0) continue;
         if (ld_relaxed((const unsigned*)p.stop) != 0) {
           s_ok = 0;
@@ -94,7 +108,7 @@ __device__ bool wait_level(const PersistPlan& p, int j) {
   return s_ok != 0;
 }
 
-template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT>
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
 __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const LevelLaunch a,
                                                                          const PersistPlan p) {
   constexpr V INF = VTraits<V>::INF;
@@ -103,7 +117,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
   constexpr int TS = kGroup;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_last;
-  const int W = a.W, C = a.C;
+  const int W = a.W, C = CX ? CMAX : a.C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // shared: target group [W][32] (+ interior) — mode 1 uses column 0 —,
   // merge buffer [C][32], generic cells [4 warps][C][32]
@@ -135,8 +149,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
     const size_t pb = (size_t)p.part_base[s];
     int64_t s0, s1;
     if (mode == 0) {
-      s0 = chunk * p.chunk_len0;
-      s1 = min(s0 + p.chunk_len0, t_lo);
+      mode0_chunk(p, s, chunk, s0, s1);
     } else {
       s0 = p.chunk_lo[p.chunk_base[s] + chunk];
       s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
@@ -155,8 +168,18 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
       // ------------------------------------ lanes own targets
       const Target<V> x = load_target<V, TRAIN, TS>(a, t_lo, t_hi, unit, lane, s_tgt + lane,
                                                     s_int + lane, warp == 0);
+      // start from the unit's merged minimum so far (other chunks' atomicMin
+      // merges): a valid upper bound that lets the scan prune early
+      if constexpr (!kGeneric) {
+        if (x.active) {
+          const V* key = keys + (size_t)x.t * C;
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c)
+            if (c < C) best[c] = __ldcg(key + c);
+        }
+      }
       __syncthreads();
-      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT>(
+      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
           a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv);
       // merge the 4 warps into warp 0 through the merge buffer
       for (int src = 1; src < kWarps; ++src) {
@@ -203,7 +226,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
       }
       __syncthreads();
       const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
-      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, 1, false, TS, WT>(
+      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, 1, false, TS, WT, CX>(
           a, x, s0 + tid, s1, kTileTargets, s_tgt, s_int, best, colv);
       // lanes -> warp (shuffle min) -> CTA (shared memory) -> one partial
       if (!kGeneric) {
@@ -315,10 +338,10 @@ size_t persist_smem(const LevelLaunch& L, bool generic, size_t vsz) {
   return s;
 }
 
-template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT = 0>
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT = 0, bool CX = false>
 void run_variant(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
   const size_t smem = persist_smem(L, LP1 == 0, sizeof(V));
-  auto kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN, WT>;
+  auto kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN, WT, CX>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -353,6 +376,7 @@ void dispatch_cells(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st,
   // small bitsets: target words in registers (32-bit values, the common case)
   if constexpr (sizeof(V) == 4) {
     if (L.W <= 8) {
+      if (lp1 == 1 && kp1 == 9) return run_variant<V, 1, 9, TRAIN, 8, true>(L, P, st, info);
       if (lp1 == 1 && kp1 <= 9) return run_variant<V, 1, 9, TRAIN, 8>(L, P, st, info);
       if (lp1 == 1 && kp1 <= 17) return run_variant<V, 1, 17, TRAIN, 8>(L, P, st, info);
       if (lp1 == 2 && kp1 <= 9) return run_variant<V, 2, 9, TRAIN, 8>(L, P, st, info);
@@ -394,8 +418,12 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
   r.c = q - b.pair_off[lo];
   const int64_t S = p.level_off[lo], T = p.level_off[lo + 1] - S;
   const int mode = p.mode[lo];
-  const int64_t s1 = mode == 0 ? min((r.c + 1) * p.chunk_len0, S)
-                               : p.chunk_lo[p.chunk_base[lo] + r.c + 1];
+  int64_t s0, s1;
+  if (mode == 0) {
+    mode0_chunk(p, lo, r.c, s0, s1);
+  } else {
+    s1 = p.chunk_lo[p.chunk_base[lo] + r.c + 1];
+  }
   r.dep = p.level_of[s1 - 1];
   const int64_t units = mode == 0 ? (T + kGroup - 1) / kGroup : T;
   r.units_r = b.world > 1 ? (units > b.rank ? (units - b.rank + b.world - 1) / b.world : 0) : units;

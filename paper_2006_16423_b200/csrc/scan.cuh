@@ -218,15 +218,28 @@ __device__ __forceinline__ V acc_block_cost(const LevelLaunch& a, int64_t s, con
   return combine<V>(cin, proc, cout, a.interleave);
 }
 
+struct AlwaysNeeded {
+  template <typename V>
+  __device__ __forceinline__ bool operator()(V) const {
+    return true;
+  }
+};
+
 // K2+K3 for one (target, source) pair: false when I' ⊄ I (not a
 // transition) — *counted* is set when it is a transition at all (the
 // reference counts gated training pairs too) and *gated* when the training
 // backward gate rejects the block.  On success: accelerator load (INF if
 // infeasible), CPU load, block memory.
-template <typename V, bool TRAIN, int TS>
+//
+// need(proc): whether an accelerator load >= proc could still improve a
+// cell.  acc(B) >= proc(B) in every interleaving mode (the comm terms are
+// non-negative, graph.cpp:457-467), so when it cannot the frontier walk is
+// skipped (by the whole warp when no lane needs it) and acc = INF — the
+// cell minima are unchanged.
+template <typename V, bool TRAIN, int TS, class Need = AlwaysNeeded>
 __device__ __forceinline__ bool pair_cost(const LevelLaunch& a, const Target<V>& x, int64_t s,
                                           const uint64_t* tA, const uint64_t* tInt, bool& gated,
-                                          V& acc, V& cpu, V& mem_blk) {
+                                          V& acc, V& cpu, V& mem_blk, Need need = Need()) {
   constexpr V INF = VTraits<V>::INF;
   const SrcRec r = load_rec(a.srec + s);
   gated = false;
@@ -242,7 +255,8 @@ __device__ __forceinline__ bool pair_cost(const LevelLaunch& a, const Target<V>&
   acc = INF;
   bool acc_ok = a.K > 0 && (x.un - r.unsup) == 0;
   if (acc_ok && a.memcheck) acc_ok = !(mem_blk > (V)a.mlim);
-  if (acc_ok) acc = acc_block_cost<V, TRAIN, TS>(a, s, r, (V)(x.acc - (V)r.acc), x, tA, tInt);
+  const V proc = (V)(x.acc - (V)r.acc);
+  if (acc_ok && need(proc)) acc = acc_block_cost<V, TRAIN, TS>(a, s, r, proc, x, tA, tInt);
   return true;
 }
 
@@ -265,7 +279,9 @@ __device__ __forceinline__ V replicated(const LevelLaunch& a, V acc, V mem_blk, 
 //
 // WT > 0: W <= WT: the subset test is fully unrolled (WT/2 predicated
 // 16-byte source loads, one LOP3 per word against the shared target column).
-template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int CS, int WT = 0>
+// CX: C == LP1 * KP1MAX exactly (no per-cell predicates).
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int CS, int WT = 0,
+          bool CX = false>
 __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Target<V>& x,
                                                  int64_t s0, int64_t s1, int step,
                                                  const uint64_t* tA, const uint64_t* tInt, V* best,
@@ -273,8 +289,9 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
   constexpr V INF = VTraits<V>::INF;
   constexpr bool kGeneric = LP1 == 0;
   constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
+  constexpr V NEG = (V)(-INF - 1);
   const int W = a.W;
-  const int C = a.C;
+  const int C = CX ? CMAX : a.C;
   const V* dp = (const V*)a.dp;
   unsigned nested_cnt = 0;
   for (int64_t s = s0; s < s1; s += step) {
@@ -307,10 +324,27 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     ++nested_cnt;
     bool gated;
     V acc, cpu, mem_blk;
-    pair_cost<V, TRAIN, TS>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk);
+    const V* sdp = dp + (size_t)s * C;
+    // the source row cells the update reads (indices <= C-2), loaded once
+    V row[CMAX > 1 ? CMAX - 1 : 1];
+    if constexpr (!kGeneric) {
+#pragma unroll
+      for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? sdp[c] : INF;
+      // prune: the accelerator cost matters only if max(dp[I'][k-1][l], proc)
+      // beats the running minimum of some cell, i.e. proc < thr
+      auto need = [&](V proc) {
+        V thr = NEG;
+#pragma unroll
+        for (int c = LP1; c < CMAX; ++c)
+          if (c < C) thr = vmax(thr, row[c - LP1] < best[c] ? best[c] : NEG);
+        return proc < thr;
+      };
+      pair_cost<V, TRAIN, TS>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk, need);
+    } else {
+      pair_cost<V, TRAIN, TS>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk);
+    }
     if (gated) continue;
     // K4: min-max update
-    const V* sdp = dp + (size_t)s * C;
     if (kGeneric && a.repl && acc != INF) {
       const int lp1 = a.L + 1;
       for (int rr = 1; rr <= a.K; ++rr) {
@@ -330,8 +364,8 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
         const int l = c % (LP1 ? LP1 : 1);
         if (c < C) {
           V b = best[c];
-          if (k >= 1) b = min(b, vmax(sdp[c - LP1], acc));
-          if (l >= 1) b = min(b, vmax(sdp[c - 1], cpu));
+          if (k >= 1) b = min(b, vmax(row[c - LP1], acc));
+          if (l >= 1) b = min(b, vmax(row[c - 1], cpu));
           best[c] = b;
         }
       }

@@ -54,8 +54,9 @@ rows = np.array(rows)
 lat = np.diff(np.concatenate([[0], rows[:, 6]]))
 print("per-level completion gaps (us): mean %.2f  p50 %.2f  p90 %.2f  max %.2f" %
       (lat.mean(), np.median(lat), np.percentile(lat, 90), lat.max()))
-step = max(1, len(rows) // 25)
+step = int(sys.argv[2]) if len(sys.argv) > 2 else max(1, len(rows) // 25)
+lim = int(sys.argv[3]) if len(sys.argv) > 3 else len(rows)
 print(" level   T  items chunks mode   start_us    done_us  gap_us  max_scan_us")
-for i in range(0, len(rows), step):
+for i in range(0, min(lim, len(rows)), step):
     s, T, it, ch, md, st, dn, ms = rows[i]
     print(f"{int(s):6d} {int(T):4d} {int(it):6d} {int(ch):6d} {int(md):4d} {st:10.1f} {dn:10.1f} {lat[i]:7.2f} {ms:10.2f}")
