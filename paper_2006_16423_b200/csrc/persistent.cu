@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
   // shared: target group [W][32] (+ interior) — mode 1 uses column 0 —,
   // merge buffer [C][32], generic cells [4 warps][C][32]
   uint64_t* s_tgt = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* s_int = s_tgt + (size_t)W * TS;
+  uint64_t* s_int = s_tgt + (size_t)a.AW * TS;  // target column padded to AW (pad 0)
   V* m_val = reinterpret_cast<V*>(s_int + (TRAIN ? (size_t)W * TS : 0));
   V* g_val = m_val + (size_t)C * TS;
   V* colv = g_val + (size_t)warp * C * TS + lane;
@@ -220,9 +220,9 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
     } else {
       // ------------------------------------ lanes own sources
       const int64_t t = t_lo + unit;
-      for (int w = tid; w < W; w += kTileTargets) {
+      for (int w = tid; w < a.AW; w += kTileTargets) {
         s_tgt[w] = __ldg(a.abits + (size_t)t * a.AW + w);
-        if (TRAIN) s_int[w] = __ldg(a.intbits + (size_t)t * W + w);
+        if (TRAIN && w < W) s_int[w] = __ldg(a.intbits + (size_t)t * W + w);
       }
       __syncthreads();
       const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
 
 size_t persist_smem(const LevelLaunch& L, bool generic, size_t vsz) {
   const int tr = L.training ? 2 : 1;
-  size_t s = (size_t)L.W * kGroup * sizeof(uint64_t) * tr;  // targets
+  size_t s = (size_t)L.AW * kGroup * sizeof(uint64_t) * tr;  // targets
   s += (size_t)L.C * kGroup * vsz;                           // merge buffer
   if (generic) s += (size_t)kWarps * L.C * kGroup * vsz;
   return s;
@@ -375,8 +375,14 @@ void dispatch_cells(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st,
   if (L.repl) return run_variant<V, 0, 0, TRAIN>(L, P, st, info);  // replication: generic cells
   // small bitsets: target words in registers (32-bit values, the common case)
   if constexpr (sizeof(V) == 4) {
+    if (lp1 == 1 && kp1 == 9) {
+      // exact words and cells: no predicates in the hot loop
+      if (L.AW == 2) return run_variant<V, 1, 9, TRAIN, 2, true>(L, P, st, info);
+      if (L.AW == 4) return run_variant<V, 1, 9, TRAIN, 4, true>(L, P, st, info);
+      if (L.AW == 6) return run_variant<V, 1, 9, TRAIN, 6, true>(L, P, st, info);
+      if (L.AW == 8) return run_variant<V, 1, 9, TRAIN, 8, true>(L, P, st, info);
+    }
     if (L.W <= 8) {
-      if (lp1 == 1 && kp1 == 9) return run_variant<V, 1, 9, TRAIN, 8, true>(L, P, st, info);
       if (lp1 == 1 && kp1 <= 9) return run_variant<V, 1, 9, TRAIN, 8>(L, P, st, info);
       if (lp1 == 1 && kp1 <= 17) return run_variant<V, 1, 17, TRAIN, 8>(L, P, st, info);
       if (lp1 == 2 && kp1 <= 9) return run_variant<V, 2, 9, TRAIN, 8>(L, P, st, info);

@@ -162,8 +162,8 @@ __device__ __forceinline__ Target<V> load_target(const LevelLaunch& a, int64_t t
   const bool active = t_lo + tl < t_hi;
   const int64_t t = active ? t_lo + tl : t_lo;
   if (stage) {
+    for (int w = 0; w < a.AW; ++w) colA[w * TS] = active ? __ldg(a.abits + (size_t)t * a.AW + w) : 0ull;
     for (int w = 0; w < W; ++w) {
-      colA[w * TS] = active ? __ldg(a.abits + (size_t)t * a.AW + w) : 0ull;
       if (TRAIN) colInt[w * TS] = active ? __ldg(a.intbits + (size_t)t * W + w) : 0ull;
     }
   }
@@ -279,7 +279,8 @@ __device__ __forceinline__ V replicated(const LevelLaunch& a, V acc, V mem_blk, 
 //
 // WT > 0: W <= WT: the subset test is fully unrolled (WT/2 predicated
 // 16-byte source loads, one LOP3 per word against the shared target column).
-// CX: C == LP1 * KP1MAX exactly (no per-cell predicates).
+// CX: C == LP1 * KP1MAX exactly (no per-cell predicates); with CX, the
+// padded row length a.AW == WT exactly as well (no per-word predicates).
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int CS, int WT = 0,
           bool CX = false>
 __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Target<V>& x,
@@ -290,7 +291,7 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
   constexpr bool kGeneric = LP1 == 0;
   constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
   constexpr V NEG = (V)(-INF - 1);
-  const int W = a.W;
+  const int W = (CX && WT > 0) ? WT : a.W;  // exact: W rounded up, pad word 0
   const int C = CX ? CMAX : a.C;
   const V* dp = (const V*)a.dp;
   unsigned nested_cnt = 0;

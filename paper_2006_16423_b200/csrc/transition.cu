@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kTileTargets) transition_kernel(const LevelLau
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = a.W, C = a.C;
   uint64_t* s_tgt = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* s_int = s_tgt + (size_t)W * TS;
+  uint64_t* s_int = s_tgt + (size_t)a.AW * TS;  // target column padded to AW
   V* s_best = reinterpret_cast<V*>(s_int + (TRAIN ? (size_t)W * TS : 0));
   const int tid = threadIdx.x;
   const int64_t T = a.t_hi - a.t_lo;
@@ -280,7 +280,7 @@ __global__ void traceback_decide_kernel(int K, int L, int W, int AW, const V* dp
 
 template <typename V, int LP1, int KP1MAX, bool TRAIN>
 void launch_tile(const LevelLaunch& L, dim3 grid, cudaStream_t st) {
-  size_t smem = (size_t)L.W * kTileTargets * sizeof(uint64_t) * (TRAIN ? 2 : 1);
+  size_t smem = (size_t)(L.AW + (TRAIN ? L.W : 0)) * kTileTargets * sizeof(uint64_t);
   if (LP1 == 0) smem += (size_t)L.C * kTileTargets * sizeof(V);
   auto kern = transition_kernel<V, LP1, KP1MAX, TRAIN>;
   static bool configured = false;
