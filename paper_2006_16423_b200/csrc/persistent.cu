@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
       }
       __syncthreads();
       const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
-      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, 1, false, TS, WT, CX>(
+      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, 1, false, TS, WT, CX, 1>(
           a, x, s0 + tid, s1, kTileTargets, s_tgt, s_int, best, colv);
       // lanes -> warp (shuffle min) -> CTA (shared memory) -> one partial
       if (!kGeneric) {

@@ -31,6 +31,10 @@
 namespace dsg {
 namespace scan {
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 template <typename V>
 __device__ __forceinline__ V vmax(V a, V b) {
   return a > b ? a : b;
@@ -281,8 +285,11 @@ __device__ __forceinline__ V replicated(const LevelLaunch& a, V acc, V mem_blk, 
 // 16-byte source loads, one LOP3 per word against the shared target column).
 // CX: C == LP1 * KP1MAX exactly (no per-cell predicates); with CX, the
 // padded row length a.AW == WT exactly as well (no per-word predicates).
+// PF > 0: prefetch (L1) the rows of the source PF steps ahead — pays off
+// when each thread walks its own sources (lanes own sources), not when the
+// warp shares them.
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int CS, int WT = 0,
-          bool CX = false>
+          bool CX = false, int PF = 0>
 __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Target<V>& x,
                                                  int64_t s0, int64_t s1, int step,
                                                  const uint64_t* tA, const uint64_t* tInt, V* best,
@@ -296,6 +303,13 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
   const V* dp = (const V*)a.dp;
   unsigned nested_cnt = 0;
   for (int64_t s = s0; s < s1; s += step) {
+    if (PF > 0 && s + PF * step < s1) {
+      // pull a later source's rows into L1 while this one is evaluated
+      const int64_t sn = s + PF * step;
+      prefetch_l1(a.abits + (size_t)sn * a.AW);
+      prefetch_l1(a.srec + sn);
+      prefetch_l1((const V*)a.dp + (size_t)sn * C);
+    }
     // K2: I' ⊆ I
     // 16-byte source words (rows padded to even length, pad word 0); the
     // target's pad column is never read past W

@@ -92,6 +92,25 @@ def main():
         data = json.load(open(tj)) if os.path.exists(tj) else {}
         data[workload] = traffic
         json.dump(data, open(tj, "w"), indent=1)
+        mj = os.path.join(ROOT, "profiles", "ncu_metrics.json")
+        mdata = json.load(open(mj)) if os.path.exists(mj) else {}
+
+        def num(m):
+            return float(d[m][0].replace(",", "")) if m in d else None
+
+        mdata[workload] = {
+            "kernel_ms": num("gpu__time_duration.sum"),
+            "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "alu_pipe_pct": num("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+            "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
+            "dram_throughput_pct": num("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "l2_throughput_pct": num("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "l1_hit_pct": num("l1tex__t_sector_hit_rate.pct"),
+            "warp_instructions": num("smsp__inst_executed.sum"),
+            "registers": num("launch__registers_per_thread"),
+            "source": f"profiles/{tag}_ncu.md",
+        }
+        json.dump(mdata, open(mj, "w"), indent=1)
         md.append(f"DRAM traffic per launch (read + write): **{traffic / 1e6:.2f} MB**.")
         md.append("")
     if lpath:
