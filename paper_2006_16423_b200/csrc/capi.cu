@@ -916,6 +916,9 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   // a sharded solve lists only this rank's units
   {
     std::vector<int64_t> pair_off(lat.n_levels + 1, 0);
+    const bool grouped = grouping_enabled(LL);
+    int group_slack = 8;
+    if (const char* e = std::getenv("DSG_GROUP_SLACK")) group_slack = std::max(1, std::atoi(e));
     pl.total_items = 0;
     for (int l = 1; l < lat.n_levels; ++l) {
       pair_off[l + 1] = pair_off[l] + pl.n_chunks[l];
@@ -923,9 +926,22 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       const int64_t units = pl.mode[l] == 0 ? (T + 31) / 32 : T;
       const int64_t units_r =
           pl.world > 1 ? (units > pl.rank ? (units - pl.rank + pl.world - 1) / pl.world : 0) : units;
-      pl.total_items += units_r * pl.n_chunks[l];
+      // old mode-0 chunks (their last source below level l-1) are grouped
+      // (grouped: last source level < l - slack; chunk c < n_old ends at
+      // min((c+1)*len, R) - 1, R = level_off[l-1])
+      int64_t n_grp = 0;
+      if (grouped && pl.mode[l] == 0 && l - group_slack >= 1) {
+        const int64_t R = lat.level_off[l - 1];
+        const int64_t n_old = (R + chunk_len0 - 1) / chunk_len0;
+        n_grp = group_slack == 1 ? n_old
+                                 : std::min<int64_t>(n_old, lat.level_off[l - group_slack] / chunk_len0);
+      }
+      pl.total_items += n_grp * ((units_r + 3) / 4) + (pl.n_chunks[l] - n_grp) * units_r;
     }
     ItemBuild B{};
+    B.grouped = grouped ? 1 : 0;
+    PP.grouped = B.grouped;
+    B.group_slack = group_slack;
     B.n_levels = lat.n_levels;
     B.pair_off = up64("pp.pair_off", pair_off);
     B.n_pairs = pair_off[lat.n_levels];

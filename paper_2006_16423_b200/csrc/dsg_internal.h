@@ -167,6 +167,7 @@ struct PersistPlan {
   // ready ones are queued behind it.
   const int64_t* part_base;  // [n_levels] offset of each level's partials
   const int4* items;         // [total_items]
+  int grouped;               // grouped items present (4 target column sets)
   unsigned long long* next;  // claim counter, zeroed per solve
   const int32_t* level_of;   // [I] level of each ordinal
   int64_t total_items;
@@ -201,6 +202,8 @@ struct PersistInfo {
 // = dep + 1) first inside each bucket.
 struct ItemBuild {
   int n_levels;
+  int grouped;               // old mode-0 chunks: one item per 4 units
+  int group_slack;           //   ... when their last source level < s - slack
   const int64_t* pair_off;   // [n_levels + 1] prefix of chunks over levels
   int64_t n_pairs;
   unsigned long long* cnt;   // [2 * n_levels + 1] scratch
@@ -208,6 +211,8 @@ struct ItemBuild {
   int rank, world;
 };
 void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t st);
+// mode-0 chunks over old levels become one item per 4 units (a warp each)
+bool grouping_enabled(const LevelLaunch& L);
 
 void query_persistent(const LevelLaunch& L, PersistInfo* info);
 void launch_persistent(const LevelLaunch& L, const PersistPlan& P, cudaStream_t st,

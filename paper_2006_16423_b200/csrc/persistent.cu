@@ -34,6 +34,7 @@
 // aborts (flag) instead of hanging.
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "scan.cuh"
 
@@ -45,6 +46,7 @@ using namespace scan;
 
 constexpr int kWarps = kTileTargets / 32;  // warps per CTA (4)
 constexpr int kGroup = 32;                 // targets per mode-0 item
+constexpr int kGroupMaxAW = 16;            // grouped items (a column set per warp) up to this
 constexpr uint64_t kWatchdogNs = 20000000000ull;
 
 template <typename V>
@@ -108,6 +110,67 @@ __device__ bool wait_level(const PersistPlan& p, int j) {
   return s_ok != 0;
 }
 
+// Level s gained n finished targets: release their rows, bump the level
+// counter on every rank (system scope when peers read it over NVLink).
+__device__ __forceinline__ void release_done(const PersistPlan& p, int s, unsigned n) {
+  if (p.world == 1) {
+    __threadfence();  // release the rows
+    atomicAdd(p.peer_done[0] + s, n);
+  } else {
+    __threadfence_system();  // rows reached every peer before its counter moves
+    for (int r = 0; r < p.world; ++r) atomicAdd_system(p.peer_done[r] + s, n);
+  }
+}
+
+// Mode 0, one warp: this chunk of `unit` has merged its minima into the
+// keys; count the arrival, and if it is the unit's last chunk apply
+// monotone_pass (dp_solver.cpp:180-193) to the merged cells, store the rows
+// into every rank's table and release them.  Returns whether it finalized.
+template <typename V, int LP1, int CMAX>
+__device__ bool arrive_finalize_unit(const LevelLaunch& a, const PersistPlan& p, int s,
+                                     int64_t unit, int64_t t_lo, int64_t T, int64_t chunks,
+                                     int lane, V* best, V* colv, const V* keys, int C) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr bool kGeneric = LP1 == 0;
+  constexpr int TS = kGroup;
+  unsigned last = 0;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();  // cumulative release of this warp's merges
+    last = atomicAdd(p.tile_count + p.tile_base[s] + unit, 1u) == chunks - 1;
+    if (last) __threadfence();  // acquire the other chunks' merges
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return false;
+  const int64_t n_act = min((int64_t)TS, T - unit * TS);
+  if (lane < n_act) {
+    const int64_t t = t_lo + unit * TS + lane;
+    const V* key = keys + (size_t)t * C;
+    if (!kGeneric) {
+#pragma unroll
+      for (int c = 0; c < CMAX; ++c)
+        if (c < C) best[c] = __ldcg(key + c);
+      monotone_regs<V, LP1, CMAX>(best, C);
+      for (int r = 0; r < p.world; ++r) {
+        V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c)
+          if (c < C) dpt[c] = best[c];
+      }
+    } else {
+      for (int c = 0; c < C; ++c) colv[c * TS] = __ldcg(key + c);
+      monotone_strided(colv, TS, a.K, a.L);
+      for (int r = 0; r < p.world; ++r) {
+        V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+        for (int c = 0; c < C; ++c) dpt[c] = colv[c * TS];
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) release_done(p, s, (unsigned)n_act);
+  return true;
+}
+
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
 __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const LevelLaunch a,
                                                                          const PersistPlan p) {
@@ -116,20 +179,26 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
   constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
   constexpr int TS = kGroup;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int s_last;
+  __shared__ int s_last, s_any_last;
   const int W = a.W, C = CX ? CMAX : a.C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // shared: target group [W][32] (+ interior) — mode 1 uses column 0 —,
-  // merge buffer [C][32], generic cells [4 warps][C][32]
+  // shared: target columns [G][AW][32] (padded, pad word 0) + interior
+  // [G][W][32] — G = 4 when grouped items exist (one column set per warp),
+  // else 1; mode 1 uses column 0 —, merge buffer [C][32], generic cells
+  // [4 warps][C][32]
+  const int G = p.grouped ? kWarps : 1;  // == grouping_enabled(a)
   uint64_t* s_tgt = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* s_int = s_tgt + (size_t)a.AW * TS;  // target column padded to AW (pad 0)
-  V* m_val = reinterpret_cast<V*>(s_int + (TRAIN ? (size_t)W * TS : 0));
+  uint64_t* s_int = s_tgt + (size_t)G * a.AW * TS;
+  V* m_val = reinterpret_cast<V*>(s_int + (TRAIN ? (size_t)G * W * TS : 0));
   V* g_val = m_val + (size_t)C * TS;
   V* colv = g_val + (size_t)warp * C * TS + lane;
   V* keys = reinterpret_cast<V*>(p.keys);
   unsigned nested_total = 0;
   __shared__ long long s_gi;
-  if (tid == 0) s_gi = (long long)atomicAdd(p.next, 1ull);
+  if (tid == 0) {
+    s_gi = (long long)atomicAdd(p.next, 1ull);
+    s_any_last = 0;
+  }
   __syncthreads();
 
   while (true) {
@@ -141,7 +210,7 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
     if (tid == 0) next_gi = atomicAdd(p.next, 1ull);
     const int s = item.x;
     const int64_t unit = item.y;
-    const int64_t chunk = item.z;
+    const int64_t chunk = item.z & ((1 << 30) - 1);
     const int64_t t_lo = p.level_off[s], t_hi = p.level_off[s + 1];
     const int64_t T = t_hi - t_lo;
     const int64_t chunks = p.n_chunks[s];
@@ -162,12 +231,33 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
       atomicExch(p.stop, 1);
 
     V best[CMAX];
-    init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
-    int64_t n_act;  // targets of this unit
+    bool any_last = false;  // trace: some unit of this item finalized
     if (mode == 0) {
       // ------------------------------------ lanes own targets
-      const Target<V> x = load_target<V, TRAIN, TS>(a, t_lo, t_hi, unit, lane, s_tgt + lane,
-                                                    s_int + lane, warp == 0);
+      const bool grouped = ((item.z >> 30) & 1) != 0;
+      // grouped (chunks over old levels): warp w owns its own 32-target
+      // unit and scans the whole chunk — the four warps read the same
+      // sources, so three of four reads hit L1, and no cross-warp merge;
+      // split (newest-level chunks, latency-critical): the four warps share
+      // one unit and split the chunk's sources
+      int64_t unit_w = unit;
+      bool wact = true;
+      uint64_t* tcol = s_tgt;
+      uint64_t* icol = s_int;
+      if (grouped) {
+        const int64_t k = unit + warp;  // own-unit index
+        const int64_t units = (T + TS - 1) / TS;
+        const int64_t units_r =
+            p.world > 1 ? (units > p.rank ? (units - p.rank + p.world - 1) / p.world : 0) : units;
+        wact = k < units_r;
+        unit_w = p.world > 1 ? p.rank + (int64_t)p.world * k : k;
+        tcol = s_tgt + (size_t)warp * a.AW * TS;
+        icol = s_int + (size_t)warp * W * TS;
+      }
+      init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
+      Target<V> x = load_target<V, TRAIN, TS>(a, t_lo, t_hi, wact ? unit_w : 0, lane, tcol + lane,
+                                              icol + lane, grouped ? wact : warp == 0);
+      x.active = x.active && wact;
       // start from the unit's merged minimum so far (other chunks' atomicMin
       // merges): a valid upper bound that lets the scan prune early
       if constexpr (!kGeneric) {
@@ -178,47 +268,60 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
             if (c < C) best[c] = __ldcg(key + c);
         }
       }
-      __syncthreads();
-      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
-          a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv);
-      // merge the 4 warps into warp 0 through the merge buffer
-      for (int src = 1; src < kWarps; ++src) {
+      if (grouped) {
+        __syncwarp();
+        if (wact)
+          nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
+              a, x, s0, s1, 1, tcol + lane, icol + lane, best, colv);
+      } else {
         __syncthreads();
-        if (warp == src) {
-          if (!kGeneric) {
+        nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
+            a, x, s0 + warp, s1, kWarps, tcol + lane, icol + lane, best, colv);
+        // merge the 4 warps into warp 0 through the merge buffer
+        for (int src = 1; src < kWarps; ++src) {
+          __syncthreads();
+          if (warp == src) {
+            if (!kGeneric) {
 #pragma unroll
-            for (int c = 0; c < CMAX; ++c)
-              if (c < C) m_val[c * TS + lane] = best[c];
-          } else {
-            for (int c = 0; c < C; ++c) m_val[c * TS + lane] = colv[c * TS];
+              for (int c = 0; c < CMAX; ++c)
+                if (c < C) m_val[c * TS + lane] = best[c];
+            } else {
+              for (int c = 0; c < C; ++c) m_val[c * TS + lane] = colv[c * TS];
+            }
           }
-        }
-        __syncthreads();
-        if (warp == 0) {
-          if (!kGeneric) {
+          __syncthreads();
+          if (warp == 0) {
+            if (!kGeneric) {
 #pragma unroll
-            for (int c = 0; c < CMAX; ++c)
-              if (c < C) best[c] = min(best[c], m_val[c * TS + lane]);
-          } else {
-            for (int c = 0; c < C; ++c) colv[c * TS] = min(colv[c * TS], m_val[c * TS + lane]);
+              for (int c = 0; c < CMAX; ++c)
+                if (c < C) best[c] = min(best[c], m_val[c * TS + lane]);
+            } else {
+              for (int c = 0; c < C; ++c) colv[c * TS] = min(colv[c * TS], m_val[c * TS + lane]);
+            }
           }
         }
       }
-      // chunks of a unit merge in L2 with a value atomicMin
-      if (warp == 0 && x.active) {
-        V* key = keys + (size_t)x.t * C;
-        if (!kGeneric) {
+      if (grouped ? wact : warp == 0) {
+        // chunks of a unit merge in L2 with a value atomicMin; the last
+        // arriving chunk finalizes the unit (this warp alone)
+        if (x.active) {
+          V* key = keys + (size_t)x.t * C;
+          if (!kGeneric) {
 #pragma unroll
-          for (int c = 0; c < CMAX; ++c)
-            if (c < C && best[c] != INF) atomic_min_v(key + c, best[c]);
-        } else {
-          for (int c = 0; c < C; ++c)
-            if (colv[c * TS] != INF) atomic_min_v(key + c, colv[c * TS]);
+            for (int c = 0; c < CMAX; ++c)
+              if (c < C && best[c] != INF) atomic_min_v(key + c, best[c]);
+          } else {
+            for (int c = 0; c < C; ++c)
+              if (colv[c * TS] != INF) atomic_min_v(key + c, colv[c * TS]);
+          }
         }
+        any_last = arrive_finalize_unit<V, LP1, CMAX>(a, p, s, unit_w, t_lo, T, chunks, lane, best,
+                                                      colv, keys, C);
       }
-      n_act = min((int64_t)TS, T - unit * TS);
+      if (any_last) s_any_last = 1;
     } else {
       // ------------------------------------ lanes own sources
+      init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
       const int64_t t = t_lo + unit;
       for (int w = tid; w < a.AW; w += kTileTargets) {
         s_tgt[w] = __ldg(a.abits + (size_t)t * a.AW + w);
@@ -250,78 +353,59 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
         for (int w = 1; w < kWarps; ++w) v = min(v, m_val[c * TS + w]);
         pv[((size_t)unit * chunks + chunk) * C + c] = v;
       }
-      n_act = 1;
-    }
-    // arrival: the last chunk of this unit finalizes its targets
-    __syncthreads();
-    const uint64_t tr2 = p.trace ? globaltimer() : 0;
-    if (tid == 0) {
-      __threadfence();  // cumulative release of this CTA's merges
-      s_last = atomicAdd(p.tile_count + p.tile_base[s] + unit, 1u) == chunks - 1;
-      if (s_last) __threadfence();  // acquire the other chunks' merges
-    }
-    __syncthreads();
-    if (s_last) {
-      const int64_t tl0 = mode == 0 ? unit * TS : unit;
-      if (mode == 0) {
-        for (int r = tid; r < C * TS; r += kTileTargets) {
-          const int c = r / TS, tl_local = r % TS;
-          m_val[r] = tl_local < n_act ? __ldcg(keys + (size_t)(t_lo + tl0 + tl_local) * C + c) : INF;
-        }
-      } else {
+      // arrival: the last chunk of this target finalizes it
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();  // cumulative release of this CTA's partials
+        s_last = atomicAdd(p.tile_count + p.tile_base[s] + unit, 1u) == chunks - 1;
+        if (s_last) __threadfence();  // acquire the other chunks' partials
+      }
+      __syncthreads();
+      if (s_last) {
         // one target: warps over cells, lanes over chunks, shuffle min
-        const V* pv = (const V*)a.part_val + pb;
+        const V* pvr = (const V*)a.part_val + pb;
         for (int c = warp; c < C; c += kWarps) {
           V v = INF;
           for (int64_t ch = lane; ch < chunks; ch += 32)
-            v = min(v, __ldcg(pv + ((size_t)unit * chunks + ch) * C + c));
+            v = min(v, __ldcg(pvr + ((size_t)unit * chunks + ch) * C + c));
           v = warp_min(v);
           if (lane == 0) m_val[c * TS] = v;
         }
-      }
-      __syncthreads();
-      if (warp == 0 && lane < n_act) {
-        // the finished rows go to every rank's table (this GPU's own for
-        // world == 1; NVLink peer stores otherwise)
-        const int64_t t = t_lo + tl0 + lane;
-        if (!kGeneric) {
-#pragma unroll
-          for (int c = 0; c < CMAX; ++c)
-            if (c < C) best[c] = m_val[c * TS + lane];
-          monotone_regs<V, LP1, CMAX>(best, C);
-          for (int r = 0; r < p.world; ++r) {
-            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+        __syncthreads();
+        if (tid == 0) {
+          if (!kGeneric) {
 #pragma unroll
             for (int c = 0; c < CMAX; ++c)
-              if (c < C) dpt[c] = best[c];
+              if (c < C) best[c] = m_val[c * TS];
+            monotone_regs<V, LP1, CMAX>(best, C);
+            for (int r = 0; r < p.world; ++r) {
+              V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+#pragma unroll
+              for (int c = 0; c < CMAX; ++c)
+                if (c < C) dpt[c] = best[c];
+            }
+          } else {
+            monotone_strided(m_val, TS, a.K, a.L);
+            for (int r = 0; r < p.world; ++r) {
+              V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+              for (int c = 0; c < C; ++c) dpt[c] = m_val[c * TS];
+            }
           }
-        } else {
-          monotone_strided(m_val + lane, TS, a.K, a.L);
-          for (int r = 0; r < p.world; ++r) {
-            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
-            for (int c = 0; c < C; ++c) dpt[c] = m_val[c * TS + lane];
-          }
+          release_done(p, s, 1u);
         }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        if (p.world == 1) {
-          __threadfence();  // release the rows
-          atomicAdd(p.peer_done[0] + s, (unsigned)n_act);
-        } else {
-          __threadfence_system();  // rows reached every peer before its counter moves
-          for (int r = 0; r < p.world; ++r) atomicAdd_system(p.peer_done[r] + s, (unsigned)n_act);
-        }
+        if (tid == 0) s_any_last = 1;
       }
     }
     __syncthreads();
+    const uint64_t tr2 = p.trace ? globaltimer() : 0;
     if (p.trace && tid == 0) {
       uint64_t* tr = p.trace + gi * 4;
       tr[0] = tr0;
       tr[1] = tr1;
       tr[2] = tr2;
-      tr[3] = globaltimer() | (s_last ? (1ull << 63) : 0ull);
+      tr[3] = globaltimer() | (s_any_last ? (1ull << 63) : 0ull);
     }
+    if (tid == 0) s_any_last = 0;
     if (tid == 0) s_gi = (long long)next_gi;
     __syncthreads();
   }
@@ -330,17 +414,29 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
   if (lane == 0 && nested_total) atomicAdd(a.pair_counter, (unsigned long long)nested_total);
 }
 
-size_t persist_smem(const LevelLaunch& L, bool generic, size_t vsz) {
-  const int tr = L.training ? 2 : 1;
-  size_t s = (size_t)L.AW * kGroup * sizeof(uint64_t) * tr;  // targets
-  s += (size_t)L.C * kGroup * vsz;                           // merge buffer
+}  // namespace
+
+// Grouped items (experimental, env DSG_GROUPING=1): measured slower than
+// split items on C2/C3 — the 4x longer items delay the start of the
+// critical items when a level completes — so off by default.
+bool grouping_enabled(const LevelLaunch& L) {
+  const char* e = std::getenv("DSG_GROUPING");
+  return L.AW <= kGroupMaxAW && e && std::atoi(e) != 0;
+}
+
+namespace {
+
+size_t persist_smem(const LevelLaunch& L, bool generic, size_t vsz, bool grouped) {
+  const size_t G = grouped ? kWarps : 1;
+  size_t s = G * kGroup * sizeof(uint64_t) * (L.AW + (L.training ? L.W : 0));  // targets
+  s += (size_t)L.C * kGroup * vsz;                                           // merge buffer
   if (generic) s += (size_t)kWarps * L.C * kGroup * vsz;
   return s;
 }
 
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT = 0, bool CX = false>
 void run_variant(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
-  const size_t smem = persist_smem(L, LP1 == 0, sizeof(V));
+  const size_t smem = persist_smem(L, LP1 == 0, sizeof(V), grouping_enabled(L));
   auto kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN, WT, CX>;
   static bool configured = false;
   if (!configured) {
@@ -409,7 +505,8 @@ void dispatch(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, Persi
 // ---- item list on the device
 struct PairInfo {
   int s, dep;
-  int64_t c, units_r;
+  bool grouped;    // one item per 4 units (old mode-0 chunk)
+  int64_t c, units_r, n_items;
 };
 
 __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t q) {
@@ -433,6 +530,8 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
   r.dep = p.level_of[s1 - 1];
   const int64_t units = mode == 0 ? (T + kGroup - 1) / kGroup : T;
   r.units_r = b.world > 1 ? (units > b.rank ? (units - b.rank + b.world - 1) / b.world : 0) : units;
+  r.grouped = b.grouped && mode == 0 && r.dep < lo - b.group_slack;
+  r.n_items = r.grouped ? (r.units_r + kWarps - 1) / kWarps : r.units_r;
   return r;
 }
 
@@ -440,7 +539,7 @@ __global__ void item_count_kernel(const PersistPlan p, const ItemBuild b) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= b.n_pairs) return;
   const PairInfo r = pair_info(p, b, q);
-  if (r.units_r) atomicAdd(b.cnt + 2 * r.dep + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.units_r);
+  if (r.n_items) atomicAdd(b.cnt + 2 * r.dep + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.n_items);
 }
 
 // exclusive scan of cnt[0, n) in place, one CTA
@@ -478,12 +577,17 @@ __global__ void item_fill_kernel(const PersistPlan p, const ItemBuild b) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= b.n_pairs) return;
   const PairInfo r = pair_info(p, b, q);
-  if (!r.units_r) return;
+  if (!r.n_items) return;
   const unsigned long long pos =
-      atomicAdd(b.cnt + 2 * r.dep + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.units_r);
-  for (int64_t k = 0; k < r.units_r; ++k) {
-    const int64_t u = b.world > 1 ? b.rank + k * b.world : k;
-    b.items[pos + k] = make_int4(r.s, (int)u, (int)r.c, r.dep);
+      atomicAdd(b.cnt + 2 * r.dep + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.n_items);
+  for (int64_t k = 0; k < r.n_items; ++k) {
+    if (r.grouped) {
+      // own-unit indices [4k, 4k+4): warp w takes 4k + w
+      b.items[pos + k] = make_int4(r.s, (int)(k * kWarps), (int)r.c | (1 << 30), r.dep);
+    } else {
+      const int64_t u = b.world > 1 ? b.rank + k * b.world : k;
+      b.items[pos + k] = make_int4(r.s, (int)u, (int)r.c, r.dep);
+    }
   }
 }
 

@@ -74,6 +74,29 @@ def test_driver_variants_match_golden(gpu, flags, max_blocks):
         assert got == rat_from_json(case["objective"]), case["name"]
 
 
+@pytest.mark.parametrize("max_blocks", [0, 2])
+def test_grouped_items_match_golden(gpu, monkeypatch, max_blocks):
+    """The experimental grouped items (DSG_GROUPING=1: one CTA item per four
+    32-target units over old chunks, one warp each) agree with the goldens."""
+    monkeypatch.setenv("DSG_GROUPING", "1")
+    monkeypatch.setenv("DSG_GROUP_SLACK", "2")
+    for case in CORPUS[::4]:
+        g = graph_from_json(case["graph"])
+        cfg = config_from_case(case)
+        f = solver.solve_maxload_training if case["mode"] == 1 else solver.solve_maxload_inference
+        try:
+            got = f(g, cfg, solver.SolveOptions(max_blocks=max_blocks)).objective_value
+        except InfeasibleError:
+            got = INF
+        assert got == rat_from_json(case["objective"]), case["name"]
+    w = wl.standin("C1")
+    base = device_solve(1, w.graph, w.config)
+    monkeypatch.delenv("DSG_GROUPING")
+    again = device_solve(1, w.graph, w.config)
+    assert base.objective_value == again.objective_value
+    assert base.stats["n_pairs"] == again.stats["n_pairs"]
+
+
 def test_standin_driver_variants_agree(gpu):
     w = wl.standin("C3")
     base = device_solve(1, w.graph, w.config)
