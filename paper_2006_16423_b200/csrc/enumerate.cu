@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 #include <cooperative_groups/reduce.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "dsg_device.cuh"
 #include "dsg_internal.h"
@@ -97,6 +98,7 @@ struct EnumArgs {
   int32_t* spill_par;  // [cap] warp mode: accepted pairs beyond kAccCap
   int32_t* spill_v;
   int csr_in_smem;     // stage the adjacency in shared memory
+  int warp_items;      // warp mode while parents x words <= this
   uint64_t* bits;      // [cap][W]
   uint64_t* maxm;      // [cap][W]
   uint64_t* addm;      // [cap][W]
@@ -115,20 +117,28 @@ struct EnumArgs {
   int64_t table_cap;
 };
 
-// Warp-resident mode for narrow levels: the frontier (parents and children,
-// bits / maximal / addable words each) lives in shared memory, up to
-// small_cap(W) ideals per level; accepted (parent, node) pairs beyond
-// kAccCap spill to global scratch.
-constexpr int kAccCap = 512;
+// Resident modes: the frontier (parents and children, bits / maximal /
+// addable words each) lives in shared memory — up to small_cap(W) ideals
+// per level when warp 0 runs alone (tiny levels), up to cta_cap(W) when the
+// whole CTA runs; accepted (parent, node) pairs beyond kAccCap spill to
+// global scratch.
+constexpr int kAccCap = 2048;
+
+__host__ __device__ __forceinline__ int cta_cap(int W) {
+  const int c = (144 * 1024) / (2 * 3 * W * (int)sizeof(uint64_t));
+  return c < 4096 ? c : 4096;
+}
 
 __host__ __device__ __forceinline__ int small_cap(int W) {
-  const int c = (96 * 1024) / (2 * 3 * W * (int)sizeof(uint64_t));
+  const int c = cta_cap(W);
   return c < 64 ? c : 64;
 }
 
+// frontier buffers [2][cta_cap][3W] u64, accepted pairs [2][kAccCap] i32,
+// top maximal element [2][cta_cap] i32
 __host__ __device__ __forceinline__ size_t enum_warp_bytes(int W) {
-  return (size_t)2 * small_cap(W) * 3 * W * sizeof(uint64_t) +
-         (size_t)(kAccCap * 2 + 2 * 64) * sizeof(int32_t);
+  return (size_t)2 * cta_cap(W) * 3 * W * sizeof(uint64_t) +
+         (size_t)(kAccCap * 2 + 2 * cta_cap(W)) * sizeof(int32_t);
 }
 
 __host__ __device__ __forceinline__ size_t enum_csr_bytes(int n, int n_pu, int n_su) {
@@ -153,7 +163,96 @@ __device__ __forceinline__ bool bit_of(const uint64_t* s, int u) {
 //   max(J∪v)   = (max(J) \ pred(v)) ∪ {v}
 //   add(J∪v)   = (add(J) \ {v}) ∪ {y ∈ succ(v) : pred(y) ⊆ J ∪ {v}}
 //
-// Wide levels: one thread per parent, masks in local memory.
+// Wide levels, the whole CTA in two phases (a barrier between): phase A,
+// threads over (parent, word) pairs test the candidates of that word and
+// record each canonical child (parent, node) at its slot; phase B, threads
+// over (child, word) pairs build the child rows.  Parent rows are read
+// from global memory (L1 after the first touch).
+__device__ void expand_cta(const EnumArgs& a, const Adj& g, int64_t lo, int64_t hi, int level,
+                           unsigned long long* s_next) {
+  const int W = a.W;
+  const int nt = blockDim.x;
+  const int i0 = threadIdx.x / W, x0 = threadIdx.x % W, di = nt / W, dx = nt % W;
+  const int64_t nP = hi - lo;
+  // phase A
+  for (int64_t i = i0, x = x0; i < nP;) {
+    const size_t row = (size_t)(lo + i) * W;
+    uint64_t cand = a.addm[row + x];
+    if (cand) {
+      const uint64_t* M = a.maxm + row;
+      int upper = 0;  // maximal elements in the words above x
+      for (int y = (int)x + 1; y < W; ++y) upper += __popcll(M[y]);
+      const uint64_t mx = M[x];
+      do {
+        const int b = __ffsll((long long)cand) - 1;
+        cand &= cand - 1;
+        const int v = ((int)x << 6) | b;
+        const int above = upper + __popcll(mx & above_mask(v, (int)x));
+        if (above) {
+          int covered = 0;
+          const int p1 = g.pu_off[v + 1];
+          for (int e = g.pu_off[v]; e < p1; ++e) {
+            const int u = g.pu_adj[e];
+            covered += (u > v && bit_of(M, u)) ? 1 : 0;
+          }
+          if (covered != above) continue;
+        }
+        const unsigned long long slot = atomicAdd(s_next, 1ull);
+        if ((int64_t)slot >= a.cap) continue;
+        a.spill_par[slot] = (int32_t)(lo + i);
+        a.spill_v[slot] = v;
+      } while (cand);
+    }
+    x += dx;
+    i += di;
+    if (x >= W) {
+      x -= W;
+      ++i;
+    }
+  }
+  __syncthreads();
+  const int64_t end = min((int64_t)*s_next, a.cap);
+  // phase B
+  for (int64_t k = i0, x = x0; hi + k < end;) {
+    const int64_t slot = hi + k;
+    const int64_t par = a.spill_par[slot];
+    const int v = a.spill_v[slot];
+    const uint64_t* J = a.bits + (size_t)par * W;
+    const uint64_t bx = (v >> 6) == x ? 1ull << (v & 63) : 0ull;
+    uint64_t m = a.maxm[(size_t)par * W + x];
+    const int p1 = g.pu_off[v + 1];
+    for (int e = g.pu_off[v]; e < p1; ++e) {
+      const int u = g.pu_adj[e];
+      if ((u >> 6) == x) m &= ~(1ull << (u & 63));
+    }
+    m |= bx;
+    uint64_t ad = a.addm[(size_t)par * W + x] & ~bx;
+    const int s1 = g.su_off[v + 1];
+    for (int e = g.su_off[v]; e < s1; ++e) {
+      const int y = g.su_adj[e];
+      if ((y >> 6) != x) continue;
+      bool ok = true;
+      const int f1 = g.pu_off[y + 1];
+      for (int f = g.pu_off[y]; f < f1 && ok; ++f) {
+        const int u = g.pu_adj[f];
+        ok = u == v || bit_of(J, u);
+      }
+      if (ok) ad |= 1ull << (y & 63);
+    }
+    a.bits[slot * W + x] = J[x] | bx;
+    a.maxm[slot * W + x] = m;
+    a.addm[slot * W + x] = ad;
+    if (x == 0) a.level_of[slot] = level + 1;
+    x += dx;
+    k += di;
+    if (x >= W) {
+      x -= W;
+      ++k;
+    }
+  }
+}
+
+// Wide levels (alternative): one thread per parent, masks in local memory.
 __device__ void expand_thread(const EnumArgs& a, const Adj& g, int64_t lo, int64_t hi, int level,
                               unsigned long long* s_next) {
   const int W = a.W;
@@ -227,41 +326,50 @@ __device__ __forceinline__ int prev_bit(const uint64_t* s, int t, int v) {
   return -1;
 }
 
-// Narrow levels, run by warp 0 alone: level after level while the frontier
-// stays within small_cap(W), without a CTA barrier or an L2 round trip on
-// the dependency chain.  Phase A: lanes over (parent, word) find the
-// canonical candidates; phase B: lanes over (child, word) build the child
-// rows into global memory and into the next shared frontier.  The canonical
-// test walks the parent's maximal elements above v from the top (kept per
-// cached ideal) while they are predecessors of v.  Returns after expanding a
-// level whose successor does not qualify; *s_next then holds the new end and
-// (lo, hi, level) describe the level just expanded, exactly as after one
+// Resident levels, run by a team — warp 0 alone (TEAM = 32, tiny levels,
+// no CTA barrier) or the whole CTA (TEAM = kEnumThreads) — level after level
+// while the frontier stays in shared memory, without an L2 round trip on the
+// dependency chain.  Phase A: threads over (parent, word) find the canonical
+// candidates; phase B: threads over (child, word) build the child rows into
+// global memory and into the next shared frontier.  The canonical test walks
+// the parent's maximal elements above v from the top (kept per cached ideal)
+// while they are predecessors of v.  Returns after expanding a level whose
+// successor does not qualify for this team; *s_next then holds the new end
+// and (lo, hi, level) describe the level just expanded, exactly as after one
 // CTA-wide step.  The adjacency lists must be staged in shared memory.
-__device__ void expand_warp(const EnumArgs& a, int64_t* lo_io, int64_t* hi_io, int* level_io,
-                            unsigned long long* s_next, uint64_t* smem, int* s_nc) {
+template <int TEAM>
+__device__ __forceinline__ void team_sync() {
+  if (TEAM == 32) __syncwarp();
+  else __syncthreads();
+}
+
+template <int TEAM>
+__device__ void expand_resident(const EnumArgs& a, int64_t* lo_io, int64_t* hi_io, int* level_io,
+                                unsigned long long* s_next, uint64_t* smem, int* s_nc) {
   const int W = a.W;
-  const int lane = threadIdx.x & 31;
-  const int cap_small = small_cap(W);
+  const int r = TEAM == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  const int cap_buf = cta_cap(W);
+  const int cap = TEAM == 32 ? small_cap(W) : cap_buf;
   const int R = 3 * W;  // words per cached ideal: J | M | A
   uint64_t* par = smem;
-  uint64_t* chi = smem + (size_t)cap_small * R;
-  int32_t* acc_i = reinterpret_cast<int32_t*>(smem + (size_t)2 * cap_small * R);
+  uint64_t* chi = smem + (size_t)cap_buf * R;
+  int32_t* acc_i = reinterpret_cast<int32_t*>(smem + (size_t)2 * cap_buf * R);
   int32_t* acc_v = acc_i + kAccCap;
   int32_t* top_p = acc_v + kAccCap;
-  int32_t* top_c = top_p + 64;
+  int32_t* top_c = top_p + cap_buf;
   const int32_t* pu_off = reinterpret_cast<const int32_t*>(smem + enum_warp_bytes(W) / sizeof(uint64_t));
   const int32_t* su_off = pu_off + (a.n + 1);
   const int32_t* pu_adj = su_off + (a.n + 1);
   const int32_t* su_adj = pu_adj + a.n_pu;
-  // lane items (i, x) over a [count][W] grid: start (lane / W, lane % W),
-  // step 32 = (di, dx)
-  const int i0 = lane / W, x0 = lane % W, di = 32 / W, dx = 32 % W;
+  // thread items (i, x) over a [count][W] grid: start (r / W, r % W), step
+  // TEAM = (di, dx)
+  const int i0 = r / W, x0 = r % W, di = TEAM / W, dx = TEAM % W;
   int64_t lo = *lo_io, hi = *hi_io;
   int level = *level_io;
   {
     const int nP0 = (int)(hi - lo);
-    for (int j = lane; j < nP0; j += 32) top_p[j] = -1;
-    __syncwarp();
+    for (int j = r; j < nP0; j += TEAM) top_p[j] = -1;
+    team_sync<TEAM>();
     for (int i = i0, x = x0; i < nP0;) {
       const size_t src = (size_t)(lo + i) * W + x;
       const uint64_t m = a.maxm[src];
@@ -276,12 +384,12 @@ __device__ void expand_warp(const EnumArgs& a, int64_t* lo_io, int64_t* hi_io, i
         ++i;
       }
     }
-    __syncwarp();
+    team_sync<TEAM>();
   }
   while (true) {
     const int nP = (int)(hi - lo);
-    if (lane == 0) *s_nc = 0;
-    __syncwarp();
+    if (r == 0) *s_nc = 0;
+    team_sync<TEAM>();
     // phase A: canonical candidates
     for (int i = i0, x = x0; i < nP;) {
       uint64_t cand = par[(size_t)i * R + 2 * W + x];
@@ -318,8 +426,9 @@ __device__ void expand_warp(const EnumArgs& a, int64_t* lo_io, int64_t* hi_io, i
         ++i;
       }
     }
-    for (int j = lane; j < cap_small; j += 32) top_c[j] = -1;
-    __syncwarp();
+    for (int j = r; j < cap; j += TEAM) top_c[j] = -1;
+    if (TEAM != 32) __threadfence_block();  // spills visible to the CTA
+    team_sync<TEAM>();
     const int nC = *s_nc;
     // phase B: child rows
     for (int k = i0, x = x0; k < nC;) {
@@ -353,7 +462,7 @@ __device__ void expand_warp(const EnumArgs& a, int64_t* lo_io, int64_t* hi_io, i
       a.bits[slot * W + x] = jb;
       a.maxm[slot * W + x] = m;
       a.addm[slot * W + x] = ad;
-      if (k < cap_small) {
+      if (k < cap) {
         chi[(size_t)k * R + x] = jb;
         chi[(size_t)k * R + W + x] = m;
         chi[(size_t)k * R + 2 * W + x] = ad;
@@ -367,16 +476,20 @@ __device__ void expand_warp(const EnumArgs& a, int64_t* lo_io, int64_t* hi_io, i
         ++k;
       }
     }
-    __syncwarp();
+    team_sync<TEAM>();
     const int64_t new_hi = hi + nC;
-    if (lane == 0) *s_next = (unsigned long long)new_hi;
-    __syncwarp();
-    if (nC == 0 || nC > cap_small || new_hi > a.budget || new_hi > a.cap) break;
-    // advance without leaving the warp (the CTA step's bookkeeping)
+    if (r == 0) *s_next = (unsigned long long)new_hi;
+    team_sync<TEAM>();
+    // stay while the next level fits this team: warp mode for tiny levels,
+    // CTA mode for the rest up to the shared-memory cap
+    const bool tiny = (int64_t)nC * W <= a.warp_items && nC <= small_cap(W);
+    const bool fits = TEAM == 32 ? tiny : (nC <= cap && !tiny);
+    if (nC == 0 || !fits || new_hi > a.budget || new_hi > a.cap) break;
+    // advance without leaving the team (the CTA step's bookkeeping)
     lo = hi;
     hi = new_hi;
     ++level;
-    if (lane == 0) a.level_off[level + 1] = hi;
+    if (r == 0) a.level_off[level + 1] = hi;
     uint64_t* t = par;
     par = chi;
     chi = t;
@@ -447,9 +560,10 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs
     }
     __syncthreads();
     if (!a.hash_mode) {
-      if (a.csr_in_smem && hi - lo <= small_cap(W)) {
+      const int64_t nP = hi - lo;
+      if (a.csr_in_smem && nP <= small_cap(W) && nP * W <= a.warp_items) {
         if (tid < 32) {
-          expand_warp(a, &lo, &hi, &level, &s_next, s_dyn, &s_nc);
+          expand_resident<32>(a, &lo, &hi, &level, &s_next, s_dyn, &s_nc);
           if (tid == 0) {
             s_lo = lo;
             s_hi = hi;
@@ -460,8 +574,12 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs
         lo = s_lo;
         hi = s_hi;
         level = s_level;
+      } else if (a.csr_in_smem && nP <= cta_cap(W)) {
+        // every thread runs the same control flow on shared counters, so
+        // (lo, hi, level) stay identical across the CTA
+        expand_resident<kEnumThreads>(a, &lo, &hi, &level, &s_next, s_dyn, &s_nc);
       } else {
-        expand_thread(a, adj, lo, hi, level, &s_next);
+        expand_cta(a, adj, lo, hi, level, &s_next);
       }
     } else {
       // phase 1: every parent writes every child into the candidate buffer
@@ -603,6 +721,8 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
   a.n_pu = L.n_pu;
   a.n_su = L.n_su;
   a.spill_par = L.spill_par;
+  a.warp_items = 48;  // measured: C2 / C4 best at 32-64
+  if (const char* e = std::getenv("DSG_ENUM_WARP_ITEMS")) a.warp_items = std::atoi(e);
   a.spill_v = L.spill_v;
   size_t smem = enum_warp_bytes(a.W);
   const size_t csr = enum_csr_bytes(a.n, a.n_pu, a.n_su);
