@@ -209,7 +209,7 @@ def run_reference_arm(args, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "rational(int64 num/den)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "rational(int64 num/den)",
         "data": "synthetic", "config": {"workload": w.name, "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
