@@ -190,9 +190,25 @@ class PodGraph:
         rt = np.dtype([("num", np.int64), ("den", np.int64)])
 
         def rats(attr):
+            # plain lists first, one bulk fill (a per-element structured
+            # assignment costs ~1 us each)
+            nums, dens = [], []
+            for nd in nodes:
+                x = getattr(nd, attr)
+                if type(x) is Fraction:
+                    nums.append(x.numerator)
+                    dens.append(x.denominator)
+                elif type(x) is int:
+                    nums.append(x)
+                    dens.append(1)
+                else:
+                    q, d = to_dsg_rat(x)
+                    nums.append(q)
+                    dens.append(d)
             a = np.zeros(max(n, 1), dtype=rt)
-            for i, nd in enumerate(nodes):
-                a[i] = to_dsg_rat(getattr(nd, attr))
+            if n:
+                a["num"][:n] = nums
+                a["den"][:n] = dens
             return a
 
         self.cpu = rats("cpu_time")

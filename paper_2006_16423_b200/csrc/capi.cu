@@ -942,6 +942,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     B.grouped = grouped ? 1 : 0;
     PP.grouped = B.grouped;
     B.group_slack = group_slack;
+    B.lag = 1 << 30;
+    if (const char* e = std::getenv("DSG_SCHED_LAG")) B.lag = std::max(1, std::atoi(e));
     B.n_levels = lat.n_levels;
     B.pair_off = up64("pp.pair_off", pair_off);
     B.n_pairs = pair_off[lat.n_levels];

@@ -204,6 +204,7 @@ struct ItemBuild {
   int n_levels;
   int grouped;               // old mode-0 chunks: one item per 4 units
   int group_slack;           //   ... when their last source level < s - slack
+  int lag;                   // list bucket = max(dep, s - lag)
   const int64_t* pair_off;   // [n_levels + 1] prefix of chunks over levels
   int64_t n_pairs;
   unsigned long long* cnt;   // [2 * n_levels + 1] scratch

@@ -47,6 +47,11 @@ using namespace scan;
 constexpr int kWarps = kTileTargets / 32;  // warps per CTA (4)
 constexpr int kGroup = 32;                 // targets per mode-0 item
 constexpr int kGroupMaxAW = 16;            // grouped items (a column set per warp) up to this
+// The exact-word/exact-cell variants (the C2 hot loop) are held to 64
+// registers so 8 CTAs fit per SM (measured: 7.4 ms vs 8.0 ms at 80
+// registers on C2; the few spills sit off the source loop).  The other
+// variants keep their natural allocation (bounding them spills the hot loop).
+constexpr int kMinBlocksExact = 8;
 constexpr uint64_t kWatchdogNs = 20000000000ull;
 
 template <typename V>
@@ -172,8 +177,7 @@ __device__ bool arrive_finalize_unit(const LevelLaunch& a, const PersistPlan& p,
 }
 
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
-__global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const LevelLaunch a,
-                                                                         const PersistPlan p) {
+__device__ __forceinline__ void persistent_body(const LevelLaunch& a, const PersistPlan& p) {
   constexpr V INF = VTraits<V>::INF;
   constexpr bool kGeneric = LP1 == 0;
   constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
@@ -414,6 +418,19 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
   if (lane == 0 && nested_total) atomicAdd(a.pair_counter, (unsigned long long)nested_total);
 }
 
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
+__global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const LevelLaunch a,
+                                                                         const PersistPlan p) {
+  persistent_body<V, LP1, KP1MAX, TRAIN, WT, CX>(a, p);
+}
+
+// exact variants: register budget for kMinBlocksExact resident CTAs per SM
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
+__global__ void __launch_bounds__(kTileTargets, kMinBlocksExact)
+    persistent_levels_kernel_x(const LevelLaunch a, const PersistPlan p) {
+  persistent_body<V, LP1, KP1MAX, TRAIN, WT, CX>(a, p);
+}
+
 }  // namespace
 
 // Grouped items (experimental, env DSG_GROUPING=1): measured slower than
@@ -437,7 +454,9 @@ size_t persist_smem(const LevelLaunch& L, bool generic, size_t vsz, bool grouped
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT = 0, bool CX = false>
 void run_variant(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
   const size_t smem = persist_smem(L, LP1 == 0, sizeof(V), grouping_enabled(L));
-  auto kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN, WT, CX>;
+  void (*kern)(const LevelLaunch, const PersistPlan);
+  if constexpr (CX) kern = persistent_levels_kernel_x<V, LP1, KP1MAX, TRAIN, WT, CX>;
+  else kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN, WT, CX>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -504,7 +523,7 @@ void dispatch(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, Persi
 
 // ---- item list on the device
 struct PairInfo {
-  int s, dep;
+  int s, dep, bucket;
   bool grouped;    // one item per 4 units (old mode-0 chunk)
   int64_t c, units_r, n_items;
 };
@@ -531,6 +550,10 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
   const int64_t units = mode == 0 ? (T + kGroup - 1) / kGroup : T;
   r.units_r = b.world > 1 ? (units > b.rank ? (units - b.rank + b.world - 1) / b.world : 0) : units;
   r.grouped = b.grouped && mode == 0 && r.dep < lo - b.group_slack;
+  // scheduling bucket: a chunk for a far-future level waits in the list until
+  // `lag` levels before its target, so each bucket holds a bounded amount of
+  // near-term work and the critical items are not queued behind the future
+  r.bucket = max(r.dep, lo - b.lag);
   r.n_items = r.grouped ? (r.units_r + kWarps - 1) / kWarps : r.units_r;
   return r;
 }
@@ -539,7 +562,8 @@ __global__ void item_count_kernel(const PersistPlan p, const ItemBuild b) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= b.n_pairs) return;
   const PairInfo r = pair_info(p, b, q);
-  if (r.n_items) atomicAdd(b.cnt + 2 * r.dep + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.n_items);
+  if (r.n_items)
+    atomicAdd(b.cnt + 2 * r.bucket + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.n_items);
 }
 
 // exclusive scan of cnt[0, n) in place, one CTA
@@ -579,7 +603,7 @@ __global__ void item_fill_kernel(const PersistPlan p, const ItemBuild b) {
   const PairInfo r = pair_info(p, b, q);
   if (!r.n_items) return;
   const unsigned long long pos =
-      atomicAdd(b.cnt + 2 * r.dep + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.n_items);
+      atomicAdd(b.cnt + 2 * r.bucket + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.n_items);
   for (int64_t k = 0; k < r.n_items; ++k) {
     if (r.grouped) {
       // own-unit indices [4k, 4k+4): warp w takes 4k + w

@@ -60,3 +60,20 @@ print(" level   T  items chunks mode   start_us    done_us  gap_us  max_scan_us"
 for i in range(0, min(lim, len(rows)), step):
     s, T, it, ch, md, st, dn, ms = rows[i]
     print(f"{int(s):6d} {int(T):4d} {int(it):6d} {int(ch):6d} {int(md):4d} {st:10.1f} {dn:10.1f} {lat[i]:7.2f} {ms:10.2f}")
+
+# critical path per level: previous level done -> critical items (dep = s-1)
+# claimed / scanning / done -> this level done
+print("\ncritical path (us): level T prev_done crit_claim crit_scan0 crit_end done | n_crit")
+done_at = {}
+for s in range(1, n_levels):
+    sel = np.nonzero(items[:, 0] == s)[0]
+    if len(sel) and last[sel].any():
+        done_at[s] = rel[sel][last[sel], 3].max()
+for s in range(2, min(n_levels, lim + 1)):
+    sel = np.nonzero((items[:, 0] == s) & (items[:, 3] == s - 1))[0]
+    if not len(sel) or s not in done_at or (s - 1) not in done_at:
+        continue
+    r = rel[sel]
+    print(f"{s:5d} {level_off[s + 1] - level_off[s]:4d} {done_at[s - 1]:9.1f} {r[:, 0].min() - done_at[s - 1]:7.1f} "
+          f"{r[:, 1].min() - done_at[s - 1]:7.1f} {r[:, 3].max() - done_at[s - 1]:7.1f} "
+          f"{done_at[s] - done_at[s - 1]:7.1f} | {len(sel)}")
