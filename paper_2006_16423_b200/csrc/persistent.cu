@@ -52,6 +52,11 @@ constexpr int kGroupMaxAW = 16;            // grouped items (a column set per wa
 // registers on C2; the few spills sit off the source loop).  The other
 // variants keep their natural allocation (bounding them spills the hot loop).
 constexpr int kMinBlocksExact = 8;
+#ifndef DSG_MIN_BLOCKS_BIG
+#define DSG_MIN_BLOCKS_BIG 6
+#endif
+// more register cells (e.g. C3's 3x7): a softer cap
+constexpr int kMinBlocksExactBig = DSG_MIN_BLOCKS_BIG;
 constexpr uint64_t kWatchdogNs = 20000000000ull;
 
 template <typename V>
@@ -426,7 +431,8 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
 
 // exact variants: register budget for kMinBlocksExact resident CTAs per SM
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
-__global__ void __launch_bounds__(kTileTargets, kMinBlocksExact)
+__global__ void __launch_bounds__(kTileTargets,
+                                  LP1 * KP1MAX <= 9 ? kMinBlocksExact : kMinBlocksExactBig)
     persistent_levels_kernel_x(const LevelLaunch a, const PersistPlan p) {
   persistent_body<V, LP1, KP1MAX, TRAIN, WT, CX>(a, p);
 }
@@ -491,11 +497,15 @@ void dispatch_cells(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st,
   // small bitsets: target words in registers (32-bit values, the common case)
   if constexpr (sizeof(V) == 4) {
     if (lp1 == 1 && kp1 == 9) {
-      // exact words and cells: no predicates in the hot loop
+      // exact words and cells: no predicates in the hot loop (C2: K=8, L=0)
       if (L.AW == 2) return run_variant<V, 1, 9, TRAIN, 2, true>(L, P, st, info);
       if (L.AW == 4) return run_variant<V, 1, 9, TRAIN, 4, true>(L, P, st, info);
       if (L.AW == 6) return run_variant<V, 1, 9, TRAIN, 6, true>(L, P, st, info);
       if (L.AW == 8) return run_variant<V, 1, 9, TRAIN, 8, true>(L, P, st, info);
+    }
+    if (lp1 == 3 && kp1 == 7) {  // C3: K=6, L=2
+      if (L.AW == 2) return run_variant<V, 3, 7, TRAIN, 2, true>(L, P, st, info);
+      if (L.AW == 4) return run_variant<V, 3, 7, TRAIN, 4, true>(L, P, st, info);
     }
     if (L.W <= 8) {
       if (lp1 == 1 && kp1 <= 9) return run_variant<V, 1, 9, TRAIN, 8>(L, P, st, info);
