@@ -795,7 +795,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   pl.chunk_len.assign(lat.n_levels, 1);
   pl.mode.assign(lat.n_levels, 0);
   pl.item_base.assign(lat.n_levels + 1, 0);
-  std::vector<int64_t> tile_base(lat.n_levels, 0), part_base(lat.n_levels, 0);
+  std::vector<int64_t> tile_base(lat.n_levels, 0);
   std::vector<int64_t> chunk_lo, chunk_base(lat.n_levels, 0);
   size_t part_elems = 1;
   pl.total_tiles = 0;
@@ -864,17 +864,9 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   }
   pl.item_base[lat.n_levels] = pl.total_items;
   if (pl.persistent) {
-    // the dataflow kernel keeps every level's partials live at once; mode 0
-    // with 32-bit values merges through atomics instead
+    // the dataflow kernel merges every chunk into the target's keys with a
+    // value atomicMin (both item shapes): no partials
     part_elems = 1;
-    for (int s = 1; s < lat.n_levels; ++s) {
-      part_base[s] = (int64_t)part_elems;
-      const int64_t T = lat.level_off[s + 1] - lat.level_off[s];
-      // mode 0 merges chunks with atomicMin (no partials); mode 1 keeps one
-      // partial per (target, chunk, cell)
-      const int64_t rows = pl.mode[s] == 0 ? 0 : T;
-      part_elems += (size_t)(pl.n_chunks[s] * C * rows);
-    }
   }
   LL.part_val = ctx.get(pfx + "dp.part_val", part_elems * vsz);
   LL.part_arg = nullptr;
@@ -907,7 +899,6 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.chunk_lo = up64("pp.chunk_lo", chunk_lo);
   PP.chunk_base = up64("pp.chunk_base", chunk_base);
   PP.tile_base = up64("pp.tile_base", tile_base);
-  PP.part_base = up64("pp.part_base", part_base);
   PP.chunk_len0 = (int)chunk_len0;
   PP.chunk_len1 = (int)chunk_len1;
   PP.poll_ns_max = poll_ns_max;
@@ -947,7 +938,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     B.n_levels = lat.n_levels;
     B.pair_off = up64("pp.pair_off", pair_off);
     B.n_pairs = pair_off[lat.n_levels];
-    B.cnt = ctx.get_t<unsigned long long>(pfx + "pp.item_cnt", 2 * (size_t)lat.n_levels + 1);
+    B.cnt = ctx.get_t<unsigned long long>(pfx + "pp.item_cnt", 3 * (size_t)lat.n_levels + 1);
     B.items = ctx.get_t<int4>(pfx + "pp.items", (size_t)pl.total_items + 1);
     B.rank = pl.rank;
     B.world = pl.world;

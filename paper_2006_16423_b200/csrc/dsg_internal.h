@@ -165,7 +165,6 @@ struct PersistPlan {
   // complete in order), then target level s.  CTAs claim them in this order
   // from one atomic counter, so a CTA never sits on an unready item while
   // ready ones are queued behind it.
-  const int64_t* part_base;  // [n_levels] offset of each level's partials
   const int4* items;         // [total_items]
   int grouped;               // grouped items present (4 target column sets)
   unsigned long long* next;  // claim counter, zeroed per solve

@@ -120,6 +120,37 @@ __device__ bool wait_level(const PersistPlan& p, int j) {
   return s_ok != 0;
 }
 
+// Wait until this GPU's counter *c reaches need (the finisher of a mode-1
+// target waits for the target's other chunks).  Returns false on stop/err.
+__device__ bool wait_count(const PersistPlan& p, const unsigned* c, unsigned need) {
+  __shared__ int s_ok2;
+  if (threadIdx.x == 0) {
+    s_ok2 = 1;
+    if (ld_relaxed(c) < need) {
+      unsigned ns = 32, polls = 0;
+      const uint64_t t0 = globaltimer();
+      while (ld_relaxed(c) < need) {
+        __nanosleep(ns);
+        ns = ns < p.poll_ns_max ? ns * 2 : p.poll_ns_max;
+        if ((++polls & 63) != 0) continue;
+        if (ld_relaxed((const unsigned*)p.stop) != 0) {
+          s_ok2 = 0;
+          break;
+        }
+        if (globaltimer() - t0 > kWatchdogNs) {
+          atomicExch(p.err, 1);
+          atomicExch(p.stop, 1);
+          s_ok2 = 0;
+          break;
+        }
+      }
+    }
+    __threadfence();  // acquire the other chunks' key merges
+  }
+  __syncthreads();
+  return s_ok2 != 0;
+}
+
 // Level s gained n finished targets: release their rows, bump the level
 // counter on every rank (system scope when peers read it over NVLink).
 __device__ __forceinline__ void release_done(const PersistPlan& p, int s, unsigned n) {
@@ -224,7 +255,6 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
     const int64_t T = t_hi - t_lo;
     const int64_t chunks = p.n_chunks[s];
     const int mode = p.mode[s];
-    const size_t pb = (size_t)p.part_base[s];
     int64_t s0, s1;
     if (mode == 0) {
       mode0_chunk(p, s, chunk, s0, s1);
@@ -232,13 +262,10 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       s0 = p.chunk_lo[p.chunk_base[s] + chunk];
       s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
     }
-    // sources [s0, s1) must be final
     const uint64_t tr0 = p.trace ? globaltimer() : 0;
-    if (!wait_level(p, item.w)) break;
-    const uint64_t tr1 = p.trace ? globaltimer() : 0;
+    uint64_t tr1 = 0;
     if (blockIdx.x == 0 && tid == 0 && p.deadline_ns && globaltimer() > (uint64_t)p.deadline_ns)
       atomicExch(p.stop, 1);
-
     V best[CMAX];
     bool any_last = false;  // trace: some unit of this item finalized
     if (mode == 0) {
@@ -277,13 +304,16 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
             if (c < C) best[c] = __ldcg(key + c);
         }
       }
+      // sources [s0, s1) must be final; the target data and the key seeds
+      // above do not depend on them, so their latency hides behind the wait
+      if (!wait_level(p, item.w)) break;
+      tr1 = p.trace ? globaltimer() : 0;
       if (grouped) {
         __syncwarp();
         if (wact)
           nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
               a, x, s0, s1, 1, tcol + lane, icol + lane, best, colv);
       } else {
-        __syncthreads();
         nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
             a, x, s0 + warp, s1, kWarps, tcol + lane, icol + lane, best, colv);
         // merge the 4 warps into warp 0 through the merge buffer
@@ -330,17 +360,37 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       if (any_last) s_any_last = 1;
     } else {
       // ------------------------------------ lanes own sources
+      // Every mode-1 chunk has <= 128 sources (capi.cu), one per thread.
+      // The block costs (K2+K3) are static, so they run before the
+      // dependency wait; after it only the row loads and the min-max update
+      // remain.  The newest chunk (c = chunks-1, the one that gates the
+      // level) is the target's finisher: it waits for the other chunks'
+      // key merges, folds its own minima in and finalizes — no atomic merge
+      // or arrival round trip on the critical path.  The item list puts it
+      // after the target's other chunks, so its wait cannot deadlock.
       init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
       const int64_t t = t_lo + unit;
+      const bool fin = chunk == chunks - 1;
       for (int w = tid; w < a.AW; w += kTileTargets) {
         s_tgt[w] = __ldg(a.abits + (size_t)t * a.AW + w);
         if (TRAIN && w < W) s_int[w] = __ldg(a.intbits + (size_t)t * W + w);
       }
-      __syncthreads();
       const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
-      nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, 1, false, TS, WT, CX, 1>(
-          a, x, s0 + tid, s1, kTileTargets, s_tgt, s_int, best, colv);
-      // lanes -> warp (shuffle min) -> CTA (shared memory) -> one partial
+      V* key = keys + (size_t)t * C;
+      __syncthreads();
+      const int64_t my = s0 + tid;
+      PrePair<V> q{};
+      if (my < s1) q = pre_pair<V, TRAIN, 1>(a, x, my, s_tgt, s_int);
+      if (!wait_level(p, item.w)) break;  // (ends with __syncthreads)
+      if (fin && chunks > 1 &&
+          !wait_count(p, p.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1)))
+        break;
+      tr1 = p.trace ? globaltimer() : 0;
+      V kv = INF;  // the other chunks' merged minimum of cell tid (finisher)
+      if (fin && tid < C) kv = __ldcg(key + tid);
+      if (my < s1) post_pair<V, LP1, KP1MAX, TS, CX>(a, q, my, best, colv);
+      nested_total += q.nested ? 1u : 0u;
+      // lanes -> warp (shuffle min) -> CTA (shared memory)
       if (!kGeneric) {
 #pragma unroll
         for (int c = 0; c < CMAX; ++c) {
@@ -356,53 +406,42 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
         }
       }
       __syncthreads();
-      V* pv = (V*)a.part_val + pb;
+      // threads over cells: merge into the keys (value atomicMin), or, for
+      // the finisher, fold in the merged keys
       for (int c = tid; c < C; c += kTileTargets) {
         V v = m_val[c * TS];
+#pragma unroll
         for (int w = 1; w < kWarps; ++w) v = min(v, m_val[c * TS + w]);
-        pv[((size_t)unit * chunks + chunk) * C + c] = v;
-      }
-      // arrival: the last chunk of this target finalizes it
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();  // cumulative release of this CTA's partials
-        s_last = atomicAdd(p.tile_count + p.tile_base[s] + unit, 1u) == chunks - 1;
-        if (s_last) __threadfence();  // acquire the other chunks' partials
+        if (fin) m_val[c * TS] = min(v, c == tid ? kv : __ldcg(key + c));
+        else if (v != INF) atomic_min_v(key + c, v);
       }
       __syncthreads();
-      if (s_last) {
-        // one target: warps over cells, lanes over chunks, shuffle min
-        const V* pvr = (const V*)a.part_val + pb;
-        for (int c = warp; c < C; c += kWarps) {
-          V v = INF;
-          for (int64_t ch = lane; ch < chunks; ch += 32)
-            v = min(v, __ldcg(pvr + ((size_t)unit * chunks + ch) * C + c));
-          v = warp_min(v);
-          if (lane == 0) m_val[c * TS] = v;
-        }
-        __syncthreads();
+      if (!fin) {
         if (tid == 0) {
-          if (!kGeneric) {
+          __threadfence();  // cumulative release of this CTA's merges
+          atomicAdd(p.tile_count + p.tile_base[s] + unit, 1u);
+        }
+      } else if (tid == 0) {
+        if (!kGeneric) {
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c)
+            if (c < C) best[c] = m_val[c * TS];
+          monotone_regs<V, LP1, CMAX>(best, C);
+          for (int r = 0; r < p.world; ++r) {
+            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
 #pragma unroll
             for (int c = 0; c < CMAX; ++c)
-              if (c < C) best[c] = m_val[c * TS];
-            monotone_regs<V, LP1, CMAX>(best, C);
-            for (int r = 0; r < p.world; ++r) {
-              V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
-#pragma unroll
-              for (int c = 0; c < CMAX; ++c)
-                if (c < C) dpt[c] = best[c];
-            }
-          } else {
-            monotone_strided(m_val, TS, a.K, a.L);
-            for (int r = 0; r < p.world; ++r) {
-              V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
-              for (int c = 0; c < C; ++c) dpt[c] = m_val[c * TS];
-            }
+              if (c < C) dpt[c] = best[c];
           }
-          release_done(p, s, 1u);
+        } else {
+          monotone_strided(m_val, TS, a.K, a.L);
+          for (int r = 0; r < p.world; ++r) {
+            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+            for (int c = 0; c < C; ++c) dpt[c] = m_val[c * TS];
+          }
         }
-        if (tid == 0) s_any_last = 1;
+        release_done(p, s, 1u);
+        s_any_last = 1;
       }
     }
     __syncthreads();
@@ -568,12 +607,20 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
   return r;
 }
 
+// order inside a dependency bucket: critical items (target level = dep + 1)
+// first, a mode-1 target's finisher (its last chunk) after them — after all
+// the target's other chunks, which it waits for —, then the rest
+__device__ __forceinline__ int item_class(const PersistPlan& p, const PairInfo& r) {
+  if (r.s != r.dep + 1) return 2;
+  return (p.mode[r.s] == 1 && r.c == p.n_chunks[r.s] - 1) ? 1 : 0;
+}
+
 __global__ void item_count_kernel(const PersistPlan p, const ItemBuild b) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= b.n_pairs) return;
   const PairInfo r = pair_info(p, b, q);
   if (r.n_items)
-    atomicAdd(b.cnt + 2 * r.bucket + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.n_items);
+    atomicAdd(b.cnt + 3 * r.bucket + item_class(p, r), (unsigned long long)r.n_items);
 }
 
 // exclusive scan of cnt[0, n) in place, one CTA
@@ -613,7 +660,7 @@ __global__ void item_fill_kernel(const PersistPlan p, const ItemBuild b) {
   const PairInfo r = pair_info(p, b, q);
   if (!r.n_items) return;
   const unsigned long long pos =
-      atomicAdd(b.cnt + 2 * r.bucket + (r.s == r.dep + 1 ? 0 : 1), (unsigned long long)r.n_items);
+      atomicAdd(b.cnt + 3 * r.bucket + item_class(p, r), (unsigned long long)r.n_items);
   for (int64_t k = 0; k < r.n_items; ++k) {
     if (r.grouped) {
       // own-unit indices [4k, 4k+4): warp w takes 4k + w
@@ -628,7 +675,7 @@ __global__ void item_fill_kernel(const PersistPlan p, const ItemBuild b) {
 }  // namespace
 
 void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t st) {
-  const int n = 2 * B.n_levels;
+  const int n = 3 * B.n_levels;
   cudaMemsetAsync(B.cnt, 0, sizeof(unsigned long long) * (n + 1), st);
   const int threads = 256;
   const unsigned blocks = (unsigned)((B.n_pairs + threads - 1) / threads);

@@ -272,6 +272,63 @@ __device__ __forceinline__ V replicated(const LevelLaunch& a, V acc, V mem_blk, 
   return a.repl_combine == 0 ? (V)(divided + sync) : vmax(divided, sync);
 }
 
+// K4 for one nested, ungated pair: cell = min(cell, max(dp[I'][k-1][l],
+// acc)) and min(cell, max(dp[I'][k][l-1], cpu)).  row: the source row's
+// cells 0..CMAX-2 in registers (register cells); sdp: the row in memory
+// (generic cells, replication).
+template <typename V, int LP1, int KP1MAX, int CS, bool CX>
+__device__ __forceinline__ void k4_update(const LevelLaunch& a, const V* sdp, const V* row, V acc,
+                                          V cpu, V mem_blk, V* best, V* colv) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr bool kGeneric = LP1 == 0;
+  constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
+  const int C = CX ? CMAX : a.C;
+  if (kGeneric && a.repl && acc != INF) {
+    const int lp1 = a.L + 1;
+    for (int rr = 1; rr <= a.K; ++rr) {
+      const V load = rr == 1 ? acc : replicated<V>(a, acc, mem_blk, rr);
+      for (int k = rr; k <= a.K; ++k)
+        for (int l = 0; l <= a.L; ++l) {
+          const int c = k * lp1 + l;
+          colv[c * CS] = min(colv[c * CS], vmax(sdp[c - rr * lp1], load));
+        }
+    }
+    acc = INF;  // accelerator candidates done; the CPU ones below
+  }
+  if (!kGeneric) {
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) {
+      const int k = c / (LP1 ? LP1 : 1);
+      const int l = c % (LP1 ? LP1 : 1);
+      if (c < C) {
+        V b = best[c];
+        if (k >= 1) b = min(b, vmax(row[c - LP1], acc));
+        if (l >= 1) b = min(b, vmax(row[c - 1], cpu));
+        best[c] = b;
+      }
+    }
+  } else {
+    // generic cells: batches of 8 so the source-row loads are all in
+    // flight before the shared-memory read-modify-writes
+    const int lp1 = a.L + 1;
+    constexpr int B = 8;
+    for (int c0 = 0; c0 < C; c0 += B) {
+      V va[B], vc[B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        const int c = c0 + i;
+        va[i] = (c < C && c >= lp1) ? sdp[c - lp1] : INF;
+        vc[i] = (c < C && (c % lp1) != 0) ? sdp[c - 1] : INF;
+      }
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        const int c = c0 + i;
+        if (c < C) colv[c * CS] = min(colv[c * CS], min(vmax(va[i], acc), vmax(vc[i], cpu)));
+      }
+    }
+  }
+}
+
 // Scan sources s0, s0+step, ... < s1 for target x: the fused K2+K3+K4 loop.
 // The K4 update is value-only — cell = min(cell, max(dp[I'][k-1][l], acc))
 // and min(cell, max(dp[I'][k][l-1], cpu)), two IMNMX per candidate; the
@@ -359,53 +416,60 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
       pair_cost<V, TRAIN, TS>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk);
     }
     if (gated) continue;
-    // K4: min-max update
-    if (kGeneric && a.repl && acc != INF) {
-      const int lp1 = a.L + 1;
-      for (int rr = 1; rr <= a.K; ++rr) {
-        const V load = rr == 1 ? acc : replicated<V>(a, acc, mem_blk, rr);
-        for (int k = rr; k <= a.K; ++k)
-          for (int l = 0; l <= a.L; ++l) {
-            const int c = k * lp1 + l;
-            colv[c * CS] = min(colv[c * CS], vmax(sdp[c - rr * lp1], load));
-          }
-      }
-      acc = INF;  // accelerator candidates done; the CPU ones below
-    }
-    if (!kGeneric) {
-#pragma unroll
-      for (int c = 0; c < CMAX; ++c) {
-        const int k = c / (LP1 ? LP1 : 1);
-        const int l = c % (LP1 ? LP1 : 1);
-        if (c < C) {
-          V b = best[c];
-          if (k >= 1) b = min(b, vmax(row[c - LP1], acc));
-          if (l >= 1) b = min(b, vmax(row[c - 1], cpu));
-          best[c] = b;
-        }
-      }
-    } else {
-      // generic cells: batches of 8 so the source-row loads are all in
-      // flight before the shared-memory read-modify-writes
-      const int lp1 = a.L + 1;
-      constexpr int B = 8;
-      for (int c0 = 0; c0 < C; c0 += B) {
-        V va[B], vc[B];
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-          const int c = c0 + i;
-          va[i] = (c < C && c >= lp1) ? sdp[c - lp1] : INF;
-          vc[i] = (c < C && (c % lp1) != 0) ? sdp[c - 1] : INF;
-        }
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-          const int c = c0 + i;
-          if (c < C) colv[c * CS] = min(colv[c * CS], min(vmax(va[i], acc), vmax(vc[i], cpu)));
-        }
-      }
-    }
+    k4_update<V, LP1, KP1MAX, CS, CX>(a, sdp, row, acc, cpu, mem_blk, best, colv);
   }
   return nested_cnt;
+}
+
+// Split K2+K3 / K4 for items whose sources may not be final yet (mode 1,
+// one source per thread): everything but the source's dp row is static, so
+// the subset test and the block cost run BEFORE the dependency wait and only
+// the row loads + the min-max update remain after it.  No pruning (it needs
+// the row).
+template <typename V>
+struct PrePair {
+  bool ok;  // nested and not gated
+  bool nested;
+  V acc, cpu, mem_blk;
+};
+
+template <typename V, bool TRAIN, int TS>
+__device__ __forceinline__ PrePair<V> pre_pair(const LevelLaunch& a, const Target<V>& x, int64_t s,
+                                               const uint64_t* tA, const uint64_t* tInt) {
+  PrePair<V> q;
+  q.ok = false;
+  q.nested = false;
+  q.acc = q.cpu = q.mem_blk = (V)0;
+  const ulonglong2* __restrict__ sA2 =
+      reinterpret_cast<const ulonglong2*>(a.abits + (size_t)s * a.AW);
+  uint64_t stray = 0;
+  for (int w = 0; w < a.W; w += 2) {
+    const ulonglong2 v = __ldg(sA2 + (w >> 1));
+    stray |= v.x & ~tA[w * TS];
+    if (w + 1 < a.W) stray |= v.y & ~tA[(w + 1) * TS];
+  }
+  if (!x.active || stray != 0ull) return q;
+  q.nested = true;
+  bool gated;
+  pair_cost<V, TRAIN, TS>(a, x, s, tA, tInt, gated, q.acc, q.cpu, q.mem_blk);
+  q.ok = !gated;
+  return q;
+}
+
+template <typename V, int LP1, int KP1MAX, int CS, bool CX>
+__device__ __forceinline__ void post_pair(const LevelLaunch& a, const PrePair<V>& q, int64_t s,
+                                          V* best, V* colv) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr int CMAX = LP1 == 0 ? 1 : LP1 * KP1MAX;
+  if (!q.ok) return;
+  const int C = CX ? CMAX : a.C;
+  const V* sdp = (const V*)a.dp + (size_t)s * C;
+  V row[CMAX > 1 ? CMAX - 1 : 1];
+  if constexpr (LP1 != 0) {
+#pragma unroll
+    for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? sdp[c] : INF;
+  }
+  k4_update<V, LP1, KP1MAX, CS, CX>(a, sdp, row, q.acc, q.cpu, q.mem_blk, best, colv);
 }
 
 template <typename V, int LP1, int KP1MAX, int CS>
