@@ -552,6 +552,7 @@ struct Lattice {
   int n_levels = 0;
   std::vector<int64_t> level_off;  // host copy, n_levels + 1
   uint64_t* sbits = nullptr;       // sorted, device
+  uint64_t* smax = nullptr;        // maximal elements of each ideal, same order
 };
 
 Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, int64_t budget,
@@ -618,7 +619,8 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
     lat.level_off.resize(lat.n_levels + 1);
     D2H(lat.level_off.data(), lvl_d, sizeof(int64_t) * (lat.n_levels + 1));
     lat.sbits = ctx.get_t<uint64_t>(pfx + "lat.sbits", (size_t)lat.I * W);
-    launch_lex_rank(W, lat.I, L.bits, L.level_of, lvl_d, lat.sbits, ctx.stream);
+    lat.smax = ctx.get_t<uint64_t>(pfx + "lat.smax", (size_t)lat.I * W);
+    launch_lex_rank(W, lat.I, L.bits, L.maxm, L.level_of, lvl_d, lat.sbits, lat.smax, ctx.stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx.stream));
     return lat;
@@ -691,6 +693,20 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   const int64_t I = lat.I;
   pl.I = I;
 
+  // level of every ordinal (dependency waits, covers, traceback)
+  pl.level_off_d = ctx.get_t<int64_t>(pfx + "pp.level_off", lat.level_off.size() + 1);
+  CK(cudaMemcpyAsync(pl.level_off_d, lat.level_off.data(), sizeof(int64_t) * lat.level_off.size(),
+                     cudaMemcpyHostToDevice, st));
+  ctx.h2d_bytes += (int64_t)(sizeof(int64_t) * lat.level_off.size());
+  pl.level_of_d = ctx.get_t<int32_t>(pfx + "pp.level_of", (size_t)I);
+  launch_level_of(pl.level_off_d, lat.n_levels, I, pl.level_of_d, st);
+  // lower covers (the newest-level sources of every target, no subset scan)
+  int64_t* cov_off = ctx.get_t<int64_t>(pfx + "lat.cov_off", (size_t)I + 1);
+  launch_cover_count(W, I, lat.smax, cov_off, st);
+  launch_scan_counts(cov_off, I, 1, st);
+  int64_t n_cov = 0;
+  D2H(&n_cov, cov_off + I, sizeof(int64_t));
+
   // ---- descriptors
   const auto t2 = Clock::now();
   DescribeLaunch& D = pl.D;
@@ -731,6 +747,12 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   D.litems = ctx.get_t<MaskItem>(pfx + "d.litems", totals[kCntLItems]);
   launch_describe(D, true, st);
   CK(cudaGetLastError());
+  if (n_cov > INT32_MAX) throw Fail{DSG_UNSUPPORTED, "cover lists exceed 2^31 entries"};
+  int32_t* cov = ctx.get_t<int32_t>(pfx + "lat.cov", (size_t)n_cov + 1);
+  int* cov_err = ctx.get_t<int>(pfx + "lat.cov_err", 1);
+  CK(cudaMemsetAsync(cov_err, 0, sizeof(int), st));
+  launch_cover_fill(W, I, lat.sbits, lat.smax, pl.level_of_d, pl.level_off_d, cov_off, cov, cov_err,
+                    st);
   pl.t_desc_ms = ms_since(t2);
 
   // ---- DP tables and launch parameters
@@ -779,6 +801,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   LL.bw_from = dg.g.bw_from;
   LL.bw_to = dg.g.bw_to;
   LL.n_nodes = P.n;
+  LL.cov_off = cov_off;
+  LL.cov = cov;
   LL.dp = ctx.get(pfx + "dp.values", (size_t)I * C * vsz);
   LL.bp = nullptr;  // values only; the traceback re-derives the argmins
   LL.pair_counter = ctx.get_t<unsigned long long>(pfx + "dp.pairs", 1);
@@ -832,22 +856,23 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       min_chunk = 4;
     }
     int64_t chunks = std::max<int64_t>(1, (target_items + units - 1) / units);
+    // The newest level's sources are handled by ONE cover chunk (the last
+    // chunk): each target's lower covers (enumerate.cu) are exactly its
+    // nested sources in level s-1, so that critical chunk evaluates a handful
+    // of pairs instead of scanning the whole level.
     if (pl.persistent && pl.mode[s] == 0) {
       const int64_t R = lat.level_off[s - 1];
-      chunks = (R + chunk_len0 - 1) / chunk_len0 + (S - R + chunk_len1 - 1) / chunk_len1;
+      chunks = (R + chunk_len0 - 1) / chunk_len0 + 1;
       chunk_base[s] = -1;
       pl.chunk_len[s] = chunk_len0;
     } else if (pl.persistent) {
       const int64_t R = s >= 2 ? lat.level_off[s - 1] : 0;
-      const int64_t rlen = kTileTargets;
-      const int64_t rc = (S - R + rlen - 1) / rlen;
       int64_t oc = (R + kTileTargets - 1) / kTileTargets;
       const int64_t olen = oc ? (R + oc - 1) / oc : 1;
       chunk_base[s] = (int64_t)chunk_lo.size();
       for (int64_t c = 0; c < oc; ++c) chunk_lo.push_back(std::min(R, c * olen));
-      for (int64_t c = 0; c < rc; ++c) chunk_lo.push_back(R + c * rlen);
-      chunk_lo.push_back(S);
-      chunks = oc + rc;
+      chunk_lo.push_back(R);
+      chunks = oc + 1;
       pl.chunk_len[s] = 0;
     } else {
       chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / min_chunk));
@@ -870,16 +895,6 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   }
   LL.part_val = ctx.get(pfx + "dp.part_val", part_elems * vsz);
   LL.part_arg = nullptr;
-  // level of every ordinal (dependency waits, traceback)
-  {
-    pl.level_off_d = ctx.get_t<int64_t>(pfx + "pp.level_off", lat.level_off.size() + 1);
-    CK(cudaMemcpyAsync(pl.level_off_d, lat.level_off.data(), sizeof(int64_t) * lat.level_off.size(),
-                       cudaMemcpyHostToDevice, st));
-    pl.level_of_d = ctx.get_t<int32_t>(pfx + "pp.level_of", (size_t)I);
-    launch_level_of(pl.level_off_d, lat.n_levels, I, pl.level_of_d, st);
-    CK(cudaStreamSynchronize(st));  // the host vector is a temporary
-    ctx.h2d_bytes += (int64_t)(sizeof(int64_t) * lat.level_off.size());
-  }
   if (!pl.persistent) return;
 
   // ---- persistent plan (device copies)
@@ -935,6 +950,12 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     B.group_slack = group_slack;
     B.lag = 1 << 30;
     if (const char* e = std::getenv("DSG_SCHED_LAG")) B.lag = std::max(1, std::atoi(e));
+    // dedicated cover-item CTAs (needs >= 2 CTAs: one of each role)
+    int crit_ctas = 0;
+    if (const char* e = std::getenv("DSG_CRIT_CTAS")) crit_ctas = std::max(0, std::atoi(e));
+    if (crit_ctas >= pl.pinfo.blocks) crit_ctas = pl.pinfo.blocks / 2;
+    B.split = crit_ctas > 0 ? 1 : 0;
+    PP.crit_ctas = crit_ctas;
     B.n_levels = lat.n_levels;
     B.pair_off = up64("pp.pair_off", pair_off);
     B.n_pairs = pair_off[lat.n_levels];
@@ -944,6 +965,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     B.world = pl.world;
     PP.items = B.items;
     PP.total_items = pl.total_items;
+    PP.crit_end = B.cnt + 2 * (size_t)lat.n_levels - 1;  // end of the last cover key
     pl.items_d = B.items;
     pl.item_build = B;  // launched after the mode table is on the device
   }
@@ -954,7 +976,10 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     PP.mode = mode_d;
     launch_build_items(PP, pl.item_build, st);
     CK(cudaGetLastError());
+    int cov_bad = 0;
+    D2H(&cov_bad, cov_err, sizeof(int));
     CK(cudaStreamSynchronize(st));  // host vectors are temporaries
+    if (cov_bad) throw Fail{DSG_CUDA_ERROR, "lower-cover lookup failed"};
   }
   PP.tile_count = ctx.get_t<unsigned>(pfx + "pp.tile_count", (size_t)pl.total_tiles + 1);
   pl.ctl_words = (size_t)lat.n_levels + 64;
@@ -962,6 +987,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.stop = reinterpret_cast<int*>(pl.ctl);
   PP.err = reinterpret_cast<int*>(pl.ctl + 1);
   PP.next = reinterpret_cast<unsigned long long*>(pl.ctl + 2);  // ctl[2..3], zeroed per solve
+  PP.crit_next = reinterpret_cast<unsigned long long*>(pl.ctl + 4);  // ctl[4..5]
   PP.done = pl.ctl + 32;
   PP.keys = ctx.get_t<unsigned long long>(pfx + "pp.keys", (size_t)I * C);  // value atomics
   // peer tables: this GPU only, until a sharded session attaches its peers

@@ -49,8 +49,14 @@ struct EnumLaunch {
 };
 
 void launch_enumerate(const EnumLaunch& L, cudaStream_t st);
-void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const int32_t* level_of,
-                     const int64_t* level_off, uint64_t* out_bits, cudaStream_t st);
+void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
+                     const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,
+                     uint64_t* out_maxm, cudaStream_t st);
+// lower covers of every ideal (ordinals one level down), CSR over ordinals
+void launch_cover_count(int W, int64_t I, const uint64_t* smax, int64_t* cnt, cudaStream_t st);
+void launch_cover_fill(int W, int64_t I, const uint64_t* sbits, const uint64_t* smax,
+                       const int32_t* level_of, const int64_t* level_off, const int64_t* cov_off,
+                       int32_t* cov, int* err, cudaStream_t st);
 
 // ------------------------------------------------------- descriptors
 // Per-ideal table sizes (pass 1) -> exclusive offsets (scan) -> fill (pass 2).
@@ -132,6 +138,9 @@ struct LevelLaunch {
   const uint64_t* bw_from;
   const uint64_t* bw_to;
   int n_nodes;
+  // lower covers of every ideal: ordinals one level down, CSR over ordinals
+  const int64_t* cov_off;     // [I + 1]
+  const int32_t* cov;
   // dp
   void* dp;                   // V[I][C]
   int32_t* bp;                // [I][C]
@@ -168,6 +177,9 @@ struct PersistPlan {
   const int4* items;         // [total_items]
   int grouped;               // grouped items present (4 target column sets)
   unsigned long long* next;  // claim counter, zeroed per solve
+  unsigned long long* crit_next;  // claim counter of the cover-item queue
+  int crit_ctas;                  // CTAs that run only cover items (0: one queue)
+  const unsigned long long* crit_end;  // -> number of cover items (after the build)
   const int32_t* level_of;   // [I] level of each ordinal
   int64_t total_items;
   unsigned* tile_count;      // [total counters], zeroed
@@ -204,6 +216,7 @@ struct ItemBuild {
   int grouped;               // old mode-0 chunks: one item per 4 units
   int group_slack;           //   ... when their last source level < s - slack
   int lag;                   // list bucket = max(dep, s - lag)
+  int split;                 // cover items in their own queue at the front
   const int64_t* pair_off;   // [n_levels + 1] prefix of chunks over levels
   int64_t n_pairs;
   unsigned long long* cnt;   // [2 * n_levels + 1] scratch

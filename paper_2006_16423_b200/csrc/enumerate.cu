@@ -676,9 +676,11 @@ __device__ __forceinline__ bool lex_less(const uint64_t* a, const uint64_t* b, i
 }
 
 __global__ void lex_rank_scatter_kernel(int W, int64_t total, const uint64_t* __restrict__ bits,
+                                        const uint64_t* __restrict__ maxm,
                                         const int32_t* __restrict__ level_of,
                                         const int64_t* __restrict__ level_off,
-                                        uint64_t* __restrict__ out_bits) {
+                                        uint64_t* __restrict__ out_bits,
+                                        uint64_t* __restrict__ out_maxm) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   int s = level_of[i];
@@ -687,7 +689,62 @@ __global__ void lex_rank_scatter_kernel(int W, int64_t total, const uint64_t* __
   int64_t rank = 0;
   for (int64_t j = lo; j < hi; ++j) rank += lex_less(bits + (size_t)j * W, bi, W) ? 1 : 0;
   uint64_t* o = out_bits + (size_t)(lo + rank) * W;
-  for (int w = 0; w < W; ++w) o[w] = bi[w];
+  uint64_t* om = out_maxm + (size_t)(lo + rank) * W;
+  const uint64_t* mi = maxm + (size_t)i * W;
+  for (int w = 0; w < W; ++w) {
+    o[w] = bi[w];
+    om[w] = mi[w];
+  }
+}
+
+// Lower covers: the sub-ideals I' ⊂ I one level down are
+// exactly I \ {v} for the maximal elements v of I (in the universe order),
+// so the DP's newest-level pairs need no subset scan.  Their ordinals are
+// found by binary search in level s-1, which is sorted by lex_less.
+__global__ void cover_count_kernel(int W, int64_t I, const uint64_t* __restrict__ smax,
+                                   int64_t* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > I) return;
+  int64_t c = 0;
+  if (i < I)
+    for (int w = 0; w < W; ++w) c += __popcll(smax[(size_t)i * W + w]);
+  cnt[i] = i < I ? c : 0;
+}
+
+__global__ void cover_fill_kernel(int W, int64_t I, const uint64_t* __restrict__ sbits,
+                                  const uint64_t* __restrict__ smax,
+                                  const int32_t* __restrict__ level_of,
+                                  const int64_t* __restrict__ level_off,
+                                  const int64_t* __restrict__ cov_off, int32_t* __restrict__ cov,
+                                  int* __restrict__ err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= I) return;
+  const int s = level_of[i];
+  if (s == 0) return;
+  const int64_t lo0 = level_off[s - 1], hi0 = level_off[s];
+  const uint64_t* bi = sbits + (size_t)i * W;
+  int64_t out = cov_off[i];
+  uint64_t key[kMaxWords];
+  for (int w = 0; w < W; ++w) key[w] = bi[w];
+  for (int w = 0; w < W; ++w) {
+    uint64_t m = smax[(size_t)i * W + w];
+    while (m) {
+      const uint64_t bit = m & (~m + 1);
+      m ^= bit;
+      key[w] &= ~bit;  // I \ {v}
+      int64_t lo = lo0, hi = hi0;  // first j with !(bits_j < key)
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (lex_less(sbits + (size_t)mid * W, key, W)) lo = mid + 1;
+        else hi = mid;
+      }
+      bool eq = lo < hi0;
+      for (int x = 0; eq && x < W; ++x) eq = sbits[(size_t)lo * W + x] == key[x];
+      if (!eq) atomicExch(err, 1);  // cannot happen for a lattice from K1
+      cov[out++] = eq ? (int32_t)lo : 0;
+      key[w] |= bit;
+    }
+  }
 }
 
 }  // namespace
@@ -735,12 +792,29 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
   count_launch();
 }
 
-void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const int32_t* level_of,
-                     const int64_t* level_off, uint64_t* out_bits, cudaStream_t st) {
+void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
+                     const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,
+                     uint64_t* out_maxm, cudaStream_t st) {
   int threads = 256;
   int64_t blocks = (total + threads - 1) / threads;
-  lex_rank_scatter_kernel<<<(unsigned)blocks, threads, 0, st>>>(W, total, bits, level_of, level_off,
-                                                                 out_bits);
+  lex_rank_scatter_kernel<<<(unsigned)blocks, threads, 0, st>>>(W, total, bits, maxm, level_of,
+                                                                 level_off, out_bits, out_maxm);
+  count_launch();
+}
+
+void launch_cover_count(int W, int64_t I, const uint64_t* smax, int64_t* cnt, cudaStream_t st) {
+  const int threads = 256;
+  cover_count_kernel<<<(unsigned)((I + 1 + threads - 1) / threads), threads, 0, st>>>(W, I, smax,
+                                                                                       cnt);
+  count_launch();
+}
+
+void launch_cover_fill(int W, int64_t I, const uint64_t* sbits, const uint64_t* smax,
+                       const int32_t* level_of, const int64_t* level_off, const int64_t* cov_off,
+                       int32_t* cov, int* err, cudaStream_t st) {
+  const int threads = 128;
+  cover_fill_kernel<<<(unsigned)((I + threads - 1) / threads), threads, 0, st>>>(
+      W, I, sbits, smax, level_of, level_off, cov_off, cov, err);
   count_launch();
 }
 

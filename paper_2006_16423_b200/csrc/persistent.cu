@@ -71,18 +71,60 @@ __device__ __forceinline__ void atomic_min_v(int64_t* p, int64_t v) {
   atomicMin(reinterpret_cast<long long*>(p), (long long)v);
 }
 
-// Implicit mode-0 chunk boundaries (see PersistPlan::chunk_len0).
+// Implicit mode-0 chunk boundaries (see PersistPlan::chunk_len0): old
+// sources [c*len0, ...) below R = level_off[s-1]; the last chunk is the cover
+// chunk (each target's lower covers, all in level s-1): s0 = s1 = -1.
 __device__ __forceinline__ void mode0_chunk(const PersistPlan& p, int s, int64_t c, int64_t& s0,
                                             int64_t& s1) {
-  const int64_t R = p.level_off[s - 1], S = p.level_off[s];
+  const int64_t R = p.level_off[s - 1];
   const int64_t n_old = (R + p.chunk_len0 - 1) / p.chunk_len0;
   if (c < n_old) {
     s0 = c * p.chunk_len0;
     s1 = min(s0 + p.chunk_len0, R);
   } else {
-    s0 = R + (c - n_old) * p.chunk_len1;
-    s1 = min(s0 + p.chunk_len1, S);
+    s0 = s1 = -1;
   }
+}
+
+// Mode 0 cover chunk: lane = target, warp w takes covers w, w+4, ... of it.
+// Per-lane trip counts differ, so no warp collectives in here.
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool CX>
+__device__ __forceinline__ unsigned scan_covers(const LevelLaunch& a, const Target<V>& x, int first,
+                                                int step, const uint64_t* tA, const uint64_t* tInt,
+                                                V* best, V* colv) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr bool kGeneric = LP1 == 0;
+  constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
+  constexpr V NEG = (V)(-INF - 1);
+  if (!x.active) return 0;
+  const int C = CX ? CMAX : a.C;
+  const int64_t c0 = __ldg(a.cov_off + x.t), c1 = __ldg(a.cov_off + x.t + 1);
+  unsigned n = 0;
+  for (int64_t j = c0 + first; j < c1; j += step) {
+    const int64_t src = __ldg(a.cov + j);
+    ++n;
+    bool gated;
+    V acc, cpu, mem_blk;
+    const V* sdp = (const V*)a.dp + (size_t)src * C;
+    V row[CMAX > 1 ? CMAX - 1 : 1];
+    if constexpr (!kGeneric) {
+#pragma unroll
+      for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? sdp[c] : INF;
+      auto need = [&](V proc) {
+        V thr = NEG;
+#pragma unroll
+        for (int c = LP1; c < CMAX; ++c)
+          if (c < C) thr = vmax(thr, row[c - LP1] < best[c] ? best[c] : NEG);
+        return proc < thr;
+      };
+      pair_cost<V, TRAIN, TS>(a, x, src, tA, tInt, gated, acc, cpu, mem_blk, need);
+    } else {
+      pair_cost<V, TRAIN, TS>(a, x, src, tA, tInt, gated, acc, cpu, mem_blk);
+    }
+    if (gated) continue;
+    k4_update<V, LP1, KP1MAX, TS, CX>(a, sdp, row, acc, cpu, mem_blk, best, colv);
+  }
+  return n;
 }
 
 // Wait until level j is complete (then so are all levels below it: every
@@ -234,20 +276,30 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
   V* colv = g_val + (size_t)warp * C * TS + lane;
   V* keys = reinterpret_cast<V*>(p.keys);
   unsigned nested_total = 0;
+  // Roles: with crit_ctas > 0 the list starts with the cover items (they gate
+  // the levels) and the first crit_ctas CTAs claim only those, so a level's
+  // critical work never queues behind ready background work; the other CTAs
+  // claim the rest.  Every item still waits only for items listed before it
+  // in its own queue or for cover items, which the critical CTAs run in level
+  // order, so neither queue can deadlock.
+  const bool crit_role = (int)blockIdx.x < p.crit_ctas;
+  const int64_t n_crit = p.crit_ctas > 0 ? (int64_t)*p.crit_end : 0;
+  unsigned long long* ctr = crit_role ? p.crit_next : p.next;
+  const int64_t q_lo = crit_role ? 0 : n_crit, q_hi = crit_role ? n_crit : p.total_items;
   __shared__ long long s_gi;
   if (tid == 0) {
-    s_gi = (long long)atomicAdd(p.next, 1ull);
+    s_gi = q_lo + (long long)atomicAdd(ctr, 1ull);
     s_any_last = 0;
   }
   __syncthreads();
 
   while (true) {
     const int64_t gi = s_gi;
-    if (gi >= p.total_items) break;
+    if (gi >= q_hi) break;
     const int4 item = __ldg(p.items + gi);
     // claim the next item now; its latency hides behind this one
     unsigned long long next_gi = 0;
-    if (tid == 0) next_gi = atomicAdd(p.next, 1ull);
+    if (tid == 0) next_gi = q_lo + atomicAdd(ctr, 1ull);
     const int s = item.x;
     const int64_t unit = item.y;
     const int64_t chunk = item.z & ((1 << 30) - 1);
@@ -258,9 +310,11 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
     int64_t s0, s1;
     if (mode == 0) {
       mode0_chunk(p, s, chunk, s0, s1);
-    } else {
+    } else if (chunk < chunks - 1) {
       s0 = p.chunk_lo[p.chunk_base[s] + chunk];
       s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
+    } else {
+      s0 = s1 = -1;  // the cover chunk
     }
     const uint64_t tr0 = p.trace ? globaltimer() : 0;
     uint64_t tr1 = 0;
@@ -314,8 +368,13 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
           nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
               a, x, s0, s1, 1, tcol + lane, icol + lane, best, colv);
       } else {
-        nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
-            a, x, s0 + warp, s1, kWarps, tcol + lane, icol + lane, best, colv);
+        if (s0 < 0)
+          nested_total += scan_covers<V, LP1, KP1MAX, TRAIN, TS, CX>(a, x, warp, kWarps,
+                                                                     tcol + lane, icol + lane,
+                                                                     best, colv);
+        else
+          nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
+              a, x, s0 + warp, s1, kWarps, tcol + lane, icol + lane, best, colv);
         // merge the 4 warps into warp 0 through the merge buffer
         for (int src = 1; src < kWarps; ++src) {
           __syncthreads();
@@ -378,9 +437,16 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
       V* key = keys + (size_t)t * C;
       __syncthreads();
-      const int64_t my = s0 + tid;
+      // this thread's source: s0 + tid (old chunk) or the target's cover tid
+      int64_t my = s0 + tid;
+      bool has = my < s1;
+      if (fin) {
+        const int64_t c0 = __ldg(a.cov_off + t), c1 = __ldg(a.cov_off + t + 1);
+        has = c0 + tid < c1;
+        my = has ? (int64_t)__ldg(a.cov + c0 + tid) : 0;
+      }
       PrePair<V> q{};
-      if (my < s1) q = pre_pair<V, TRAIN, 1>(a, x, my, s_tgt, s_int);
+      if (has) q = pre_pair<V, TRAIN, 1>(a, x, my, s_tgt, s_int);
       if (!wait_level(p, item.w)) break;  // (ends with __syncthreads)
       if (fin && chunks > 1 &&
           !wait_count(p, p.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1)))
@@ -388,8 +454,18 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       tr1 = p.trace ? globaltimer() : 0;
       V kv = INF;  // the other chunks' merged minimum of cell tid (finisher)
       if (fin && tid < C) kv = __ldcg(key + tid);
-      if (my < s1) post_pair<V, LP1, KP1MAX, TS, CX>(a, q, my, best, colv);
+      if (has) post_pair<V, LP1, KP1MAX, TS, CX>(a, q, my, best, colv);
       nested_total += q.nested ? 1u : 0u;
+      if (fin) {
+        // targets with more than 128 lower covers (DAG width > 128)
+        const int64_t c0 = __ldg(a.cov_off + t), c1 = __ldg(a.cov_off + t + 1);
+        for (int64_t j = c0 + tid + kTileTargets; j < c1; j += kTileTargets) {
+          const int64_t src = __ldg(a.cov + j);
+          const PrePair<V> q2 = pre_pair<V, TRAIN, 1>(a, x, src, s_tgt, s_int);
+          post_pair<V, LP1, KP1MAX, TS, CX>(a, q2, src, best, colv);
+          nested_total += 1u;
+        }
+      }
       // lanes -> warp (shuffle min) -> CTA (shared memory)
       if (!kGeneric) {
 #pragma unroll
@@ -593,9 +669,9 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
   if (mode == 0) {
     mode0_chunk(p, lo, r.c, s0, s1);
   } else {
-    s1 = p.chunk_lo[p.chunk_base[lo] + r.c + 1];
+    s1 = r.c < p.n_chunks[lo] - 1 ? p.chunk_lo[p.chunk_base[lo] + r.c + 1] : -1;
   }
-  r.dep = p.level_of[s1 - 1];
+  r.dep = s1 < 0 ? lo - 1 : p.level_of[s1 - 1];  // the cover chunk waits for level s-1
   const int64_t units = mode == 0 ? (T + kGroup - 1) / kGroup : T;
   r.units_r = b.world > 1 ? (units > b.rank ? (units - b.rank + b.world - 1) / b.world : 0) : units;
   r.grouped = b.grouped && mode == 0 && r.dep < lo - b.group_slack;
@@ -607,12 +683,18 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
   return r;
 }
 
-// order inside a dependency bucket: critical items (target level = dep + 1)
-// first, a mode-1 target's finisher (its last chunk) after them — after all
-// the target's other chunks, which it waits for —, then the rest
-__device__ __forceinline__ int item_class(const PersistPlan& p, const PairInfo& r) {
-  if (r.s != r.dep + 1) return 2;
-  return (p.mode[r.s] == 1 && r.c == p.n_chunks[r.s] - 1) ? 1 : 0;
+// Sort key of an item.  One queue (b.split == 0): by dependency bucket, and
+// inside a bucket the critical items (target level = dep + 1, i.e. the cover
+// chunks) first — a mode-1 target's finisher after them, after all the
+// target's other chunks, which it waits for —, then the rest.  Two queues
+// (b.split != 0): the cover items first (keys [0, 2n)), by level, then the
+// background items by bucket (keys [2n, 3n)).
+__device__ __forceinline__ int item_key(const PersistPlan& p, const ItemBuild& b,
+                                        const PairInfo& r) {
+  const bool crit = r.s == r.dep + 1;
+  const int cls = !crit ? 2 : (p.mode[r.s] == 1 && r.c == p.n_chunks[r.s] - 1) ? 1 : 0;
+  if (!b.split) return 3 * r.bucket + cls;
+  return crit ? 2 * r.bucket + cls : 2 * b.n_levels + r.bucket;
 }
 
 __global__ void item_count_kernel(const PersistPlan p, const ItemBuild b) {
@@ -620,7 +702,7 @@ __global__ void item_count_kernel(const PersistPlan p, const ItemBuild b) {
   if (q >= b.n_pairs) return;
   const PairInfo r = pair_info(p, b, q);
   if (r.n_items)
-    atomicAdd(b.cnt + 3 * r.bucket + item_class(p, r), (unsigned long long)r.n_items);
+    atomicAdd(b.cnt + item_key(p, b, r), (unsigned long long)r.n_items);
 }
 
 // exclusive scan of cnt[0, n) in place, one CTA
@@ -660,7 +742,7 @@ __global__ void item_fill_kernel(const PersistPlan p, const ItemBuild b) {
   const PairInfo r = pair_info(p, b, q);
   if (!r.n_items) return;
   const unsigned long long pos =
-      atomicAdd(b.cnt + 3 * r.bucket + item_class(p, r), (unsigned long long)r.n_items);
+      atomicAdd(b.cnt + item_key(p, b, r), (unsigned long long)r.n_items);
   for (int64_t k = 0; k < r.n_items; ++k) {
     if (r.grouped) {
       // own-unit indices [4k, 4k+4): warp w takes 4k + w

@@ -356,14 +356,29 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
   constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
   constexpr V NEG = (V)(-INF - 1);
   const int W = (CX && WT > 0) ? WT : a.W;  // exact: W rounded up, pad word 0
+  const int AWp = (CX && WT > 0) ? WT : a.AW;  // row pitch (a compile-time constant when exact)
   const int C = CX ? CMAX : a.C;
   const V* dp = (const V*)a.dp;
   unsigned nested_cnt = 0;
+  // L == 0 (accelerator cells only): a pair can change a cell only through
+  // max(dp[I'][k-1], acc) < best[k], and acc >= proc, so it is a candidate
+  // only if the block is supported, fits in memory and proc < max_k best[k].
+  // Everything else — most nested pairs of a memory-bound DP — skips the row
+  // loads, the pruning test and the min-max update (the minima are unchanged,
+  // so results stay bit-identical).  maxbest only shrinks; it is refreshed
+  // after every update.
+  constexpr bool kAccOnly = LP1 == 1;
+  V maxbest = NEG;
+  if constexpr (kAccOnly) {
+#pragma unroll
+    for (int c = 1; c < CMAX; ++c)
+      if (c < C) maxbest = vmax(maxbest, best[c]);
+  }
   for (int64_t s = s0; s < s1; s += step) {
     if (PF > 0 && s + PF * step < s1) {
       // pull a later source's rows into L1 while this one is evaluated
       const int64_t sn = s + PF * step;
-      prefetch_l1(a.abits + (size_t)sn * a.AW);
+      prefetch_l1(a.abits + (size_t)sn * AWp);
       prefetch_l1(a.srec + sn);
       prefetch_l1((const V*)a.dp + (size_t)sn * C);
     }
@@ -371,7 +386,7 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     // 16-byte source words (rows padded to even length, pad word 0); the
     // target's pad column is never read past W
     const ulonglong2* __restrict__ sA2 =
-        reinterpret_cast<const ulonglong2*>(a.abits + (size_t)s * a.AW);
+        reinterpret_cast<const ulonglong2*>(a.abits + (size_t)s * AWp);
     uint64_t stray = 0;
     if constexpr (WT > 0) {
 #pragma unroll
@@ -392,8 +407,24 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     }
     const bool nested = x.active && stray == 0ull;
     if (UNIFORM && !__any_sync(0xffffffffu, nested)) continue;
+    bool cand = true;
+    if constexpr (kAccOnly) {
+      // the first 32 bytes of the source record: cpu, acc, mem, unsup
+      // (every lane evaluates it, so the vote below is warp-uniform)
+      const int4* q = reinterpret_cast<const int4*>(a.srec + s);
+      const int4 r0 = __ldg(q), r1 = __ldg(q + 1);
+      const V racc = (V)(int64_t)(((uint64_t)(uint32_t)r0.w << 32) | (uint32_t)r0.z);
+      const V rmem = (V)(int64_t)(((uint64_t)(uint32_t)r1.y << 32) | (uint32_t)r1.x);
+      cand = nested && a.K > 0 && (x.un - r1.z) == 0 && (V)(x.acc - racc) < maxbest;
+      if (a.memcheck) cand = cand && !((V)(x.mem - rmem) > (V)a.mlim);
+      if (UNIFORM && !__any_sync(0xffffffffu, cand)) {
+        nested_cnt += nested ? 1u : 0u;
+        continue;
+      }
+    }
     if (!nested) continue;
     ++nested_cnt;
+    if (!cand) continue;
     bool gated;
     V acc, cpu, mem_blk;
     const V* sdp = dp + (size_t)s * C;
@@ -417,6 +448,12 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     }
     if (gated) continue;
     k4_update<V, LP1, KP1MAX, CS, CX>(a, sdp, row, acc, cpu, mem_blk, best, colv);
+    if constexpr (kAccOnly) {
+      maxbest = NEG;
+#pragma unroll
+      for (int c = 1; c < CMAX; ++c)
+        if (c < C) maxbest = vmax(maxbest, best[c]);
+    }
   }
   return nested_cnt;
 }
