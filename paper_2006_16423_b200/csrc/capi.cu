@@ -803,14 +803,19 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   LL.n_nodes = P.n;
   LL.cov_off = cov_off;
   LL.cov = cov;
-  LL.dp = ctx.get(pfx + "dp.values", (size_t)I * C * vsz);
+  LL.dp = ctx.get(pfx + "dp.values", (size_t)I * C * vsz + 64);  // + staging slack
   LL.bp = nullptr;  // values only; the traceback re-derives the argmins
   LL.pair_counter = ctx.get_t<unsigned long long>(pfx + "dp.pairs", 1);
 
   // ---- chunk plan
   pl.pinfo = PersistInfo{};
   if (pl.persistent) {
-    query_persistent(LL, &pl.pinfo);
+    PersistPlan q{};  // what sizes the CTA's shared memory (see the chunk plan)
+    q.chunk_len0 = 64;
+    if (const char* e = std::getenv("DSG_CHUNK_LEN")) q.chunk_len0 = std::max(4, std::atoi(e));
+    q.stage = 1;
+    if (const char* e = std::getenv("DSG_STAGE")) q.stage = std::atoi(e) != 0;
+    query_persistent(LL, q, &pl.pinfo);
     if (opt->reserved > 0) pl.pinfo.blocks = std::min(pl.pinfo.blocks, opt->reserved);
   }
   const int64_t target_items =
@@ -830,12 +835,13 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   // (see the item list below).  Per-level path: 128-target tiles x uniform
   // chunks of >= 16 sources.
   const int64_t kSmallLevel = 16;
-  // mode 0: every chunk short and implicit (chunk c = sources [c*len,
-  // (c+1)*len), len 48: measured best on C2/C3) — with readiness-ordered
-  // claims the scan stays balanced and no long item sits on the critical
-  // path; mode 1: older sources in long cost-balanced chunks, the newest
-  // level in 128s (explicit boundaries)
-  int64_t chunk_len0 = 48, chunk_len1 = 16;
+  // mode 0: old sources (levels <= s-2) in short implicit chunks (chunk c =
+  // sources [c*len, (c+1)*len), len 64: measured best on C2/C3 once the
+  // newest level moved to the cover chunk; 48 / 96 are 3-5 % slower) — with
+  // readiness-ordered claims the scan stays balanced and no long item sits
+  // on the critical path; mode 1: old sources in cost-balanced chunks of
+  // <= 128 (explicit boundaries).  Both: one cover chunk for level s-1.
+  int64_t chunk_len0 = 64, chunk_len1 = 16;
   unsigned poll_ns_max = 256;  // measured: 256 ns beats 1 us on C2/C3
   if (const char* e = std::getenv("DSG_CHUNK_LEN")) chunk_len0 = std::max(4, std::atoi(e));
   if (const char* e = std::getenv("DSG_CHUNK_LEN1")) chunk_len1 = std::max(4, std::atoi(e));
@@ -915,6 +921,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.chunk_base = up64("pp.chunk_base", chunk_base);
   PP.tile_base = up64("pp.tile_base", tile_base);
   PP.chunk_len0 = (int)chunk_len0;
+  PP.stage = 1;
+  if (const char* e = std::getenv("DSG_STAGE")) PP.stage = std::atoi(e) != 0;
   PP.chunk_len1 = (int)chunk_len1;
   PP.poll_ns_max = poll_ns_max;
   // work items in readiness order, built on the device (launch_build_items):

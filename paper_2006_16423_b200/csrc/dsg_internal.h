@@ -165,6 +165,7 @@ struct PersistPlan {
   // because those items gate level s.  Mode-1 levels list their
   // boundaries: [chunk_lo[b+c], chunk_lo[b+c+1]), b = chunk_base[s].
   int chunk_len0, chunk_len1;
+  int stage;                 // stage old mode-0 chunks in shared memory
   unsigned poll_ns_max;      // dependency-wait backoff cap
   const int64_t* chunk_lo;
   const int64_t* chunk_base;
@@ -227,7 +228,7 @@ void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t s
 // mode-0 chunks over old levels become one item per 4 units (a warp each)
 bool grouping_enabled(const LevelLaunch& L);
 
-void query_persistent(const LevelLaunch& L, PersistInfo* info);
+void query_persistent(const LevelLaunch& L, const PersistPlan& P, PersistInfo* info);
 void launch_persistent(const LevelLaunch& L, const PersistPlan& P, cudaStream_t st,
                        PersistInfo* info);
 void launch_read_globaltimer(uint64_t* out, cudaStream_t st);

@@ -254,6 +254,43 @@ __device__ bool arrive_finalize_unit(const LevelLaunch& a, const PersistPlan& p,
   return true;
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+// Stage a mode-0 old chunk's sources [s0, s1) — bitset rows, records and
+// (16-byte aligned superset of the) dp rows, all contiguous in HBM — into
+// shared memory with 16-byte async copies from all 128 threads: the chunk's
+// loads are in flight at once instead of one dependent round trip per
+// source iteration.  Ends with the CTA barrier.
+template <typename V>
+__device__ __forceinline__ SrcView<V> stage_sources(const LevelLaunch& a, int64_t s0, int64_t s1,
+                                                    int C, unsigned char* st) {
+  const int tid = threadIdx.x;
+  const int64_t n = s1 - s0;
+  const size_t nb = (size_t)n * a.AW * 8, nr = (size_t)n * sizeof(SrcRec);
+  const char* gb = reinterpret_cast<const char*>(a.abits + (size_t)s0 * a.AW);
+  const char* gr = reinterpret_cast<const char*>(a.srec + s0);
+  const size_t d0 = (size_t)s0 * C * sizeof(V), d1 = (size_t)s1 * C * sizeof(V);
+  const size_t da = d0 & ~(size_t)15, de = (d1 + 15) & ~(size_t)15;
+  const char* gd = reinterpret_cast<const char*>(a.dp) + da;
+  unsigned char* sb = st;
+  unsigned char* sr = sb + nb;
+  unsigned char* sd = sr + nr;
+  for (size_t i = (size_t)tid * 16; i < nb; i += kTileTargets * 16) cp_async16(sb + i, gb + i);
+  for (size_t i = (size_t)tid * 16; i < nr; i += kTileTargets * 16) cp_async16(sr + i, gr + i);
+  for (size_t i = (size_t)tid * 16; i < de - da; i += kTileTargets * 16) cp_async16(sd + i, gd + i);
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  SrcView<V> v;
+  v.bits = reinterpret_cast<const uint64_t*>(sb);
+  v.rec = reinterpret_cast<const SrcRec*>(sr);
+  v.dp = reinterpret_cast<const V*>(sd + (d0 - da));
+  v.base = s0;
+  return v;
+}
+
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
 __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const PersistPlan& p) {
   constexpr V INF = VTraits<V>::INF;
@@ -274,6 +311,10 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
   V* m_val = reinterpret_cast<V*>(s_int + (TRAIN ? (size_t)G * W * TS : 0));
   V* g_val = m_val + (size_t)C * TS;
   V* colv = g_val + (size_t)warp * C * TS + lane;
+  // staging area for one old chunk's sources (16-byte aligned)
+  unsigned char* st_area = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(g_val + (kGeneric ? (size_t)kWarps * C * TS : 0)) + 15) &
+      ~(uintptr_t)15);
   V* keys = reinterpret_cast<V*>(p.keys);
   unsigned nested_total = 0;
   // Roles: with crit_ctas > 0 the list starts with the cover items (they gate
@@ -364,14 +405,24 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       tr1 = p.trace ? globaltimer() : 0;
       if (grouped) {
         __syncwarp();
-        if (wact)
+        if (p.stage) {
+          const SrcView<V> sv = stage_sources<V>(a, s0, s1, C, st_area);  // (CTA barrier)
+          if (wact)
+            nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX, 0, true>(
+                a, x, s0, s1, 1, tcol + lane, icol + lane, best, colv, sv);
+        } else if (wact) {
           nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
               a, x, s0, s1, 1, tcol + lane, icol + lane, best, colv);
+        }
       } else {
         if (s0 < 0)
           nested_total += scan_covers<V, LP1, KP1MAX, TRAIN, TS, CX>(a, x, warp, kWarps,
                                                                      tcol + lane, icol + lane,
                                                                      best, colv);
+        else if (p.stage)
+          nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX, 0, true>(
+              a, x, s0 + warp, s1, kWarps, tcol + lane, icol + lane, best, colv,
+              stage_sources<V>(a, s0, s1, C, st_area));
         else
           nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
               a, x, s0 + warp, s1, kWarps, tcol + lane, icol + lane, best, colv);
@@ -564,17 +615,23 @@ bool grouping_enabled(const LevelLaunch& L) {
 
 namespace {
 
-size_t persist_smem(const LevelLaunch& L, bool generic, size_t vsz, bool grouped) {
+size_t persist_smem(const LevelLaunch& L, const PersistPlan* P, bool generic, size_t vsz,
+                    bool grouped) {
   const size_t G = grouped ? kWarps : 1;
   size_t s = G * kGroup * sizeof(uint64_t) * (L.AW + (L.training ? L.W : 0));  // targets
   s += (size_t)L.C * kGroup * vsz;                                           // merge buffer
   if (generic) s += (size_t)kWarps * L.C * kGroup * vsz;
+  if (P && P->stage) {
+    // one old chunk: bitset rows, records, dp rows (+ alignment slack)
+    const size_t n = (size_t)P->chunk_len0;
+    s += 16 + n * L.AW * 8 + n * sizeof(SrcRec) + n * L.C * vsz + 32;
+  }
   return s;
 }
 
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT = 0, bool CX = false>
 void run_variant(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
-  const size_t smem = persist_smem(L, LP1 == 0, sizeof(V), grouping_enabled(L));
+  const size_t smem = persist_smem(L, P, LP1 == 0, sizeof(V), grouping_enabled(L));
   void (*kern)(const LevelLaunch, const PersistPlan);
   if constexpr (CX) kern = persistent_levels_kernel_x<V, LP1, KP1MAX, TRAIN, WT, CX>;
   else kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN, WT, CX>;
@@ -770,10 +827,9 @@ void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t s
   count_launch();
 }
 
-void query_persistent(const LevelLaunch& L, PersistInfo* info) {
+void query_persistent(const LevelLaunch& L, const PersistPlan& P, PersistInfo* info) {
   info->query_only = 1;
-  PersistPlan dummy{};
-  dispatch(L, &dummy, nullptr, info);
+  dispatch(L, &P, nullptr, info);
   info->query_only = 0;
 }
 

@@ -67,6 +67,36 @@ __device__ __forceinline__ SrcRec load_rec(const SrcRec* p) {
   return r;
 }
 
+// The same record from shared memory (staged chunks, plain loads).
+__device__ __forceinline__ SrcRec load_rec_s(const SrcRec* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  const int4 a = q[0], b = q[1], c = q[2], d = q[3];
+  SrcRec r;
+  r.cpu = (int64_t)(((uint64_t)(uint32_t)a.y << 32) | (uint32_t)a.x);
+  r.acc = (int64_t)(((uint64_t)(uint32_t)a.w << 32) | (uint32_t)a.z);
+  r.mem = (int64_t)(((uint64_t)(uint32_t)b.y << 32) | (uint32_t)b.x);
+  r.unsup = b.z;
+  r.n_chunks = b.w;
+  r.chunk0 = c.x;
+  r.n_f = c.y;
+  r.n_n = c.z;
+  r.off_f = c.w;
+  r.off_n = d.x;
+  r.pad = d.y;
+  r.infmask = ((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z;
+  return r;
+}
+
+// A chunk's source rows staged in shared memory (mode-0 old chunks): bitset
+// rows (pitch AW), records and dp rows of ordinals [base, base + n).
+template <typename V>
+struct SrcView {
+  const uint64_t* bits;
+  const SrcRec* rec;
+  const V* dp;
+  int64_t base;
+};
+
 // General backward-contiguity gate (is_contiguous over reachability_within
 // of the backward part, graph.cpp:349-363), used when the fast up-set test
 // does not apply.  tA: the target column (stride TS).
@@ -240,12 +270,13 @@ struct AlwaysNeeded {
 // non-negative, graph.cpp:457-467), so when it cannot the frontier walk is
 // skipped (by the whole warp when no lane needs it) and acc = INF — the
 // cell minima are unchanged.
-template <typename V, bool TRAIN, int TS, class Need = AlwaysNeeded>
+template <typename V, bool TRAIN, int TS, class Need = AlwaysNeeded, bool STAGED = false>
 __device__ __forceinline__ bool pair_cost(const LevelLaunch& a, const Target<V>& x, int64_t s,
                                           const uint64_t* tA, const uint64_t* tInt, bool& gated,
-                                          V& acc, V& cpu, V& mem_blk, Need need = Need()) {
+                                          V& acc, V& cpu, V& mem_blk, Need need = Need(),
+                                          const SrcRec* rs = nullptr) {
   constexpr V INF = VTraits<V>::INF;
-  const SrcRec r = load_rec(a.srec + s);
+  const SrcRec r = STAGED ? load_rec_s(rs) : load_rec(a.srec + s);
   gated = false;
   if (TRAIN && a.has_bw) {
     const uint64_t* sA = a.abits + (size_t)s * a.AW;
@@ -346,11 +377,11 @@ __device__ __forceinline__ void k4_update(const LevelLaunch& a, const V* sdp, co
 // when each thread walks its own sources (lanes own sources), not when the
 // warp shares them.
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int CS, int WT = 0,
-          bool CX = false, int PF = 0>
+          bool CX = false, int PF = 0, bool STAGED = false>
 __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Target<V>& x,
                                                  int64_t s0, int64_t s1, int step,
                                                  const uint64_t* tA, const uint64_t* tInt, V* best,
-                                                 V* colv) {
+                                                 V* colv, SrcView<V> sv = SrcView<V>{}) {
   constexpr V INF = VTraits<V>::INF;
   constexpr bool kGeneric = LP1 == 0;
   constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
@@ -385,14 +416,14 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     // K2: I' ⊆ I
     // 16-byte source words (rows padded to even length, pad word 0); the
     // target's pad column is never read past W
-    const ulonglong2* __restrict__ sA2 =
-        reinterpret_cast<const ulonglong2*>(a.abits + (size_t)s * AWp);
+    const ulonglong2* __restrict__ sA2 = reinterpret_cast<const ulonglong2*>(
+        STAGED ? sv.bits + (size_t)(s - sv.base) * AWp : a.abits + (size_t)s * AWp);
     uint64_t stray = 0;
     if constexpr (WT > 0) {
 #pragma unroll
       for (int j = 0; j < WT / 2; ++j) {
         if (2 * j < W) {
-          const ulonglong2 v = __ldg(sA2 + j);
+          const ulonglong2 v = STAGED ? sA2[j] : __ldg(sA2 + j);
           stray |= v.x & ~tA[2 * j * TS];
           if (2 * j + 1 < W) stray |= v.y & ~tA[(2 * j + 1) * TS];
         }
@@ -400,7 +431,7 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     } else {
 #pragma unroll 4
       for (int w = 0; w < W; w += 2) {
-        const ulonglong2 v = __ldg(sA2 + (w >> 1));
+        const ulonglong2 v = STAGED ? sA2[w >> 1] : __ldg(sA2 + (w >> 1));
         stray |= v.x & ~tA[w * TS];
         if (w + 1 < W) stray |= v.y & ~tA[(w + 1) * TS];
       }
@@ -411,8 +442,8 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     if constexpr (kAccOnly) {
       // the first 32 bytes of the source record: cpu, acc, mem, unsup
       // (every lane evaluates it, so the vote below is warp-uniform)
-      const int4* q = reinterpret_cast<const int4*>(a.srec + s);
-      const int4 r0 = __ldg(q), r1 = __ldg(q + 1);
+      const int4* q = reinterpret_cast<const int4*>(STAGED ? sv.rec + (s - sv.base) : a.srec + s);
+      const int4 r0 = STAGED ? q[0] : __ldg(q), r1 = STAGED ? q[1] : __ldg(q + 1);
       const V racc = (V)(int64_t)(((uint64_t)(uint32_t)r0.w << 32) | (uint32_t)r0.z);
       const V rmem = (V)(int64_t)(((uint64_t)(uint32_t)r1.y << 32) | (uint32_t)r1.x);
       cand = nested && a.K > 0 && (x.un - r1.z) == 0 && (V)(x.acc - racc) < maxbest;
@@ -427,7 +458,7 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     if (!cand) continue;
     bool gated;
     V acc, cpu, mem_blk;
-    const V* sdp = dp + (size_t)s * C;
+    const V* sdp = STAGED ? sv.dp + (size_t)(s - sv.base) * C : dp + (size_t)s * C;
     // the source row cells the update reads (indices <= C-2), loaded once
     V row[CMAX > 1 ? CMAX - 1 : 1];
     if constexpr (!kGeneric) {
@@ -442,9 +473,11 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
           if (c < C) thr = vmax(thr, row[c - LP1] < best[c] ? best[c] : NEG);
         return proc < thr;
       };
-      pair_cost<V, TRAIN, TS>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk, need);
+      pair_cost<V, TRAIN, TS, decltype(need), STAGED>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk,
+                                                      need, sv.rec + (s - sv.base));
     } else {
-      pair_cost<V, TRAIN, TS>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk);
+      pair_cost<V, TRAIN, TS, AlwaysNeeded, STAGED>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk,
+                                                    AlwaysNeeded(), sv.rec + (s - sv.base));
     }
     if (gated) continue;
     k4_update<V, LP1, KP1MAX, CS, CX>(a, sdp, row, acc, cpu, mem_blk, best, colv);
