@@ -811,8 +811,9 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   pl.pinfo = PersistInfo{};
   if (pl.persistent) {
     PersistPlan q{};  // what sizes the CTA's shared memory (see the chunk plan)
-    q.chunk_len0 = 64;
+    q.chunk_len0 = q.chunk_len1 = 64;
     if (const char* e = std::getenv("DSG_CHUNK_LEN")) q.chunk_len0 = std::max(4, std::atoi(e));
+    if (const char* e = std::getenv("DSG_CHUNK_LEN1")) q.chunk_len1 = std::max(4, std::atoi(e));
     q.stage = 1;
     if (const char* e = std::getenv("DSG_STAGE")) q.stage = std::atoi(e) != 0;
     query_persistent(LL, q, &pl.pinfo);
@@ -841,7 +842,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   // readiness-ordered claims the scan stays balanced and no long item sits
   // on the critical path; mode 1: old sources in cost-balanced chunks of
   // <= 128 (explicit boundaries).  Both: one cover chunk for level s-1.
-  int64_t chunk_len0 = 64, chunk_len1 = 16;
+  int64_t chunk_len0 = 64, chunk_len1 = 64;
   unsigned poll_ns_max = 256;  // measured: 256 ns beats 1 us on C2/C3
   if (const char* e = std::getenv("DSG_CHUNK_LEN")) chunk_len0 = std::max(4, std::atoi(e));
   if (const char* e = std::getenv("DSG_CHUNK_LEN1")) chunk_len1 = std::max(4, std::atoi(e));
@@ -867,8 +868,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     // nested sources in level s-1, so that critical chunk evaluates a handful
     // of pairs instead of scanning the whole level.
     if (pl.persistent && pl.mode[s] == 0) {
-      const int64_t R = lat.level_off[s - 1];
-      chunks = (R + chunk_len0 - 1) / chunk_len0 + 1;
+      const int64_t R = lat.level_off[s - 1], R2 = s >= 2 ? lat.level_off[s - 2] : 0;
+      chunks = (R2 + chunk_len0 - 1) / chunk_len0 + (R - R2 + chunk_len1 - 1) / chunk_len1 + 1;
       chunk_base[s] = -1;
       pl.chunk_len[s] = chunk_len0;
     } else if (pl.persistent) {
@@ -967,7 +968,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     B.n_levels = lat.n_levels;
     B.pair_off = up64("pp.pair_off", pair_off);
     B.n_pairs = pair_off[lat.n_levels];
-    B.cnt = ctx.get_t<unsigned long long>(pfx + "pp.item_cnt", 3 * (size_t)lat.n_levels + 1);
+    B.cnt = ctx.get_t<unsigned long long>(pfx + "pp.item_cnt", 4 * (size_t)lat.n_levels + 1);
     B.items = ctx.get_t<int4>(pfx + "pp.items", (size_t)pl.total_items + 1);
     B.rank = pl.rank;
     B.world = pl.world;

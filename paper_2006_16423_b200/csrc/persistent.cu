@@ -74,13 +74,21 @@ __device__ __forceinline__ void atomic_min_v(int64_t* p, int64_t v) {
 // Implicit mode-0 chunk boundaries (see PersistPlan::chunk_len0): old
 // sources [c*len0, ...) below R = level_off[s-1]; the last chunk is the cover
 // chunk (each target's lower covers, all in level s-1): s0 = s1 = -1.
+// Level s-2's sources (the semi-critical chunks: they wait for level s-2,
+// which completes just before level s-1 does) use the shorter length
+// chunk_len1.
 __device__ __forceinline__ void mode0_chunk(const PersistPlan& p, int s, int64_t c, int64_t& s0,
                                             int64_t& s1) {
   const int64_t R = p.level_off[s - 1];
-  const int64_t n_old = (R + p.chunk_len0 - 1) / p.chunk_len0;
+  const int64_t R2 = s >= 2 ? p.level_off[s - 2] : 0;
+  const int64_t n_old = (R2 + p.chunk_len0 - 1) / p.chunk_len0;
+  const int64_t n_mid = (R - R2 + p.chunk_len1 - 1) / p.chunk_len1;
   if (c < n_old) {
     s0 = c * p.chunk_len0;
-    s1 = min(s0 + p.chunk_len0, R);
+    s1 = min(s0 + p.chunk_len0, R2);
+  } else if (c < n_old + n_mid) {
+    s0 = R2 + (c - n_old) * p.chunk_len1;
+    s1 = min(s0 + p.chunk_len1, R);
   } else {
     s0 = s1 = -1;
   }
@@ -623,7 +631,7 @@ size_t persist_smem(const LevelLaunch& L, const PersistPlan* P, bool generic, si
   if (generic) s += (size_t)kWarps * L.C * kGroup * vsz;
   if (P && P->stage) {
     // one old chunk: bitset rows, records, dp rows (+ alignment slack)
-    const size_t n = (size_t)P->chunk_len0;
+    const size_t n = (size_t)max(P->chunk_len0, P->chunk_len1);
     s += 16 + n * L.AW * 8 + n * sizeof(SrcRec) + n * L.C * vsz + 32;
   }
   return s;
@@ -746,12 +754,16 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
 // target's other chunks, which it waits for —, then the rest.  Two queues
 // (b.split != 0): the cover items first (keys [0, 2n)), by level, then the
 // background items by bucket (keys [2n, 3n)).
+// Background items of a bucket are ordered near-first: the chunks of level
+// dep + 2 (they gate the level after the one being finished) before the
+// chunks of later levels.
 __device__ __forceinline__ int item_key(const PersistPlan& p, const ItemBuild& b,
                                         const PairInfo& r) {
   const bool crit = r.s == r.dep + 1;
-  const int cls = !crit ? 2 : (p.mode[r.s] == 1 && r.c == p.n_chunks[r.s] - 1) ? 1 : 0;
-  if (!b.split) return 3 * r.bucket + cls;
-  return crit ? 2 * r.bucket + cls : 2 * b.n_levels + r.bucket;
+  const int cls = crit ? ((p.mode[r.s] == 1 && r.c == p.n_chunks[r.s] - 1) ? 1 : 0)
+                       : (r.s == r.dep + 2 ? 2 : 3);
+  if (!b.split) return 4 * r.bucket + cls;
+  return crit ? 2 * r.bucket + cls : 2 * b.n_levels + 2 * r.bucket + (cls - 2);
 }
 
 __global__ void item_count_kernel(const PersistPlan p, const ItemBuild b) {
@@ -814,7 +826,7 @@ __global__ void item_fill_kernel(const PersistPlan p, const ItemBuild b) {
 }  // namespace
 
 void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t st) {
-  const int n = 3 * B.n_levels;
+  const int n = 4 * B.n_levels;
   cudaMemsetAsync(B.cnt, 0, sizeof(unsigned long long) * (n + 1), st);
   const int threads = 256;
   const unsigned blocks = (unsigned)((B.n_pairs + threads - 1) / threads);
