@@ -117,7 +117,7 @@ __device__ __forceinline__ unsigned scan_covers(const LevelLaunch& a, const Targ
     V row[CMAX > 1 ? CMAX - 1 : 1];
     if constexpr (!kGeneric) {
 #pragma unroll
-      for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? sdp[c] : INF;
+      for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? ld_row<false>(sdp + c) : INF;
       auto need = [&](V proc) {
         V thr = NEG;
 #pragma unroll
@@ -135,9 +135,19 @@ __device__ __forceinline__ unsigned scan_covers(const LevelLaunch& a, const Targ
   return n;
 }
 
+// Release-add without an L1 invalidation (atom.release: MEMBAR.ALL + ATOM;
+// __threadfence() + atomicAdd would add CCTL.IVALL, which discards the L1
+// of every CTA on the SM).  ATOM, not RED: a counter others spin on should
+// reach L2 at once.
+__device__ __forceinline__ unsigned atom_release_add(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // Wait until level j is complete (then so are all levels below it: every
 // unit of level j consumes all of level j-1).  Returns false on stop/err.
-__device__ bool wait_level(const PersistPlan& p, int j) {
+__device__ bool wait_level(const PersistPlan& p, int j, bool acquire = false) {
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
     s_ok = 1;
@@ -163,8 +173,17 @@ __device__ bool wait_level(const PersistPlan& p, int j) {
         }
       }
     }
-    if (p.world == 1) __threadfence();  // acquire the finished rows
-    else __threadfence_system();        // ... including peers' NVLink stores
+    // world == 1: no acquire fence — every later read of data produced in
+    // this kernel (dp rows, keys) goes to L2 (ld.global.cg / cp.async.cg)
+    // and is control-dependent on the counter value just observed, and the
+    // producers released (MEMBAR) before bumping it.  An acquire would
+    // invalidate the whole L1 of the SM (CCTL.IVALL) on every item.
+    // Mode-1 items (one source row per thread: the rows share L1 lines, so
+    // L1-cached loads are much cheaper than per-cell L2 loads) acquire
+    // instead, which invalidates the L1.
+    if (p.world > 1) __threadfence_system();  // peers' NVLink stores
+    else if (acquire) __threadfence();
+    asm volatile("" ::: "memory");
   }
   __syncthreads();
   return s_ok != 0;
@@ -195,7 +214,7 @@ __device__ bool wait_count(const PersistPlan& p, const unsigned* c, unsigned nee
         }
       }
     }
-    __threadfence();  // acquire the other chunks' key merges
+    asm volatile("" ::: "memory");  // keys are read at L2 (see wait_level)
   }
   __syncthreads();
   return s_ok2 != 0;
@@ -205,8 +224,7 @@ __device__ bool wait_count(const PersistPlan& p, const unsigned* c, unsigned nee
 // counter on every rank (system scope when peers read it over NVLink).
 __device__ __forceinline__ void release_done(const PersistPlan& p, int s, unsigned n) {
   if (p.world == 1) {
-    __threadfence();  // release the rows
-    atomicAdd(p.peer_done[0] + s, n);
+    atom_release_add(p.peer_done[0] + s, n);  // release the rows
   } else {
     __threadfence_system();  // rows reached every peer before its counter moves
     for (int r = 0; r < p.world; ++r) atomicAdd_system(p.peer_done[r] + s, n);
@@ -227,9 +245,8 @@ __device__ bool arrive_finalize_unit(const LevelLaunch& a, const PersistPlan& p,
   unsigned last = 0;
   __syncwarp();
   if (lane == 0) {
-    __threadfence();  // cumulative release of this warp's merges
-    last = atomicAdd(p.tile_count + p.tile_base[s] + unit, 1u) == chunks - 1;
-    if (last) __threadfence();  // acquire the other chunks' merges
+    // release this warp's merges; the last arriver reads the others' at L2
+    last = atom_release_add(p.tile_count + p.tile_base[s] + unit, 1u) == chunks - 1;
   }
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return false;
@@ -506,7 +523,7 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       }
       PrePair<V> q{};
       if (has) q = pre_pair<V, TRAIN, 1>(a, x, my, s_tgt, s_int);
-      if (!wait_level(p, item.w)) break;  // (ends with __syncthreads)
+      if (!wait_level(p, item.w, true)) break;  // acquire (ends with __syncthreads)
       if (fin && chunks > 1 &&
           !wait_count(p, p.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1)))
         break;

@@ -35,6 +35,16 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
+// A source dp row cell: rows finished by other CTAs inside the persistent
+// kernel are read at L2 (ld.global.cg: never a stale L1 line, so the
+// dependency wait needs no L1 invalidation); staged rows come from shared
+// memory.
+template <bool SMEM, typename V>
+__device__ __forceinline__ V ld_row(const V* p) {
+  if constexpr (SMEM) return *p;
+  else return __ldcg(p);
+}
+
 template <typename V>
 __device__ __forceinline__ V vmax(V a, V b) {
   return a > b ? a : b;
@@ -307,7 +317,7 @@ __device__ __forceinline__ V replicated(const LevelLaunch& a, V acc, V mem_blk, 
 // acc)) and min(cell, max(dp[I'][k][l-1], cpu)).  row: the source row's
 // cells 0..CMAX-2 in registers (register cells); sdp: the row in memory
 // (generic cells, replication).
-template <typename V, int LP1, int KP1MAX, int CS, bool CX>
+template <typename V, int LP1, int KP1MAX, int CS, bool CX, bool SMEM = false>
 __device__ __forceinline__ void k4_update(const LevelLaunch& a, const V* sdp, const V* row, V acc,
                                           V cpu, V mem_blk, V* best, V* colv) {
   constexpr V INF = VTraits<V>::INF;
@@ -321,7 +331,7 @@ __device__ __forceinline__ void k4_update(const LevelLaunch& a, const V* sdp, co
       for (int k = rr; k <= a.K; ++k)
         for (int l = 0; l <= a.L; ++l) {
           const int c = k * lp1 + l;
-          colv[c * CS] = min(colv[c * CS], vmax(sdp[c - rr * lp1], load));
+          colv[c * CS] = min(colv[c * CS], vmax(ld_row<SMEM>(sdp + c - rr * lp1), load));
         }
     }
     acc = INF;  // accelerator candidates done; the CPU ones below
@@ -348,8 +358,8 @@ __device__ __forceinline__ void k4_update(const LevelLaunch& a, const V* sdp, co
 #pragma unroll
       for (int i = 0; i < B; ++i) {
         const int c = c0 + i;
-        va[i] = (c < C && c >= lp1) ? sdp[c - lp1] : INF;
-        vc[i] = (c < C && (c % lp1) != 0) ? sdp[c - 1] : INF;
+        va[i] = (c < C && c >= lp1) ? ld_row<SMEM>(sdp + c - lp1) : INF;
+        vc[i] = (c < C && (c % lp1) != 0) ? ld_row<SMEM>(sdp + c - 1) : INF;
       }
 #pragma unroll
       for (int i = 0; i < B; ++i) {
@@ -463,7 +473,7 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
     V row[CMAX > 1 ? CMAX - 1 : 1];
     if constexpr (!kGeneric) {
 #pragma unroll
-      for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? sdp[c] : INF;
+      for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? ld_row<STAGED>(sdp + c) : INF;
       // prune: the accelerator cost matters only if max(dp[I'][k-1][l], proc)
       // beats the running minimum of some cell, i.e. proc < thr
       auto need = [&](V proc) {
@@ -480,7 +490,7 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
                                                     AlwaysNeeded(), sv.rec + (s - sv.base));
     }
     if (gated) continue;
-    k4_update<V, LP1, KP1MAX, CS, CX>(a, sdp, row, acc, cpu, mem_blk, best, colv);
+    k4_update<V, LP1, KP1MAX, CS, CX, STAGED>(a, sdp, row, acc, cpu, mem_blk, best, colv);
     if constexpr (kAccOnly) {
       maxbest = NEG;
 #pragma unroll
@@ -539,7 +549,8 @@ __device__ __forceinline__ void post_pair(const LevelLaunch& a, const PrePair<V>
 #pragma unroll
     for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? sdp[c] : INF;
   }
-  k4_update<V, LP1, KP1MAX, CS, CX>(a, sdp, row, q.acc, q.cpu, q.mem_blk, best, colv);
+  // plain (L1) loads: the caller's dependency wait acquired (L1 invalidated)
+  k4_update<V, LP1, KP1MAX, CS, CX, true>(a, sdp, row, q.acc, q.cpu, q.mem_blk, best, colv);
 }
 
 template <typename V, int LP1, int KP1MAX, int CS>
