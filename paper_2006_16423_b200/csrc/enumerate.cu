@@ -366,8 +366,12 @@ __device__ void expand_resident(const EnumArgs& a, int64_t* lo_io, int64_t* hi_i
   const int i0 = r / W, x0 = r % W, di = TEAM / W, dx = TEAM % W;
   int64_t lo = *lo_io, hi = *hi_io;
   int level = *level_io;
+  // child counters, double-buffered by level parity: the next level's is
+  // reset during this level's phase B, so a level costs two team barriers
+  int par_nc = 0;
   {
     const int nP0 = (int)(hi - lo);
+    if (r == 0) s_nc[0] = s_nc[1] = 0;
     for (int j = r; j < nP0; j += TEAM) top_p[j] = -1;
     team_sync<TEAM>();
     for (int i = i0, x = x0; i < nP0;) {
@@ -388,8 +392,7 @@ __device__ void expand_resident(const EnumArgs& a, int64_t* lo_io, int64_t* hi_i
   }
   while (true) {
     const int nP = (int)(hi - lo);
-    if (r == 0) *s_nc = 0;
-    team_sync<TEAM>();
+    int* nc = s_nc + par_nc;
     // phase A: canonical candidates
     for (int i = i0, x = x0; i < nP;) {
       uint64_t cand = par[(size_t)i * R + 2 * W + x];
@@ -408,7 +411,7 @@ __device__ void expand_resident(const EnumArgs& a, int64_t* lo_io, int64_t* hi_i
             canon = is_pred;
           }
           if (!canon) continue;
-          const int k = atomicAdd(s_nc, 1);
+          const int k = atomicAdd(nc, 1);
           const int64_t slot = hi + k;
           if (k < kAccCap) {
             acc_i[k] = i;
@@ -429,7 +432,8 @@ __device__ void expand_resident(const EnumArgs& a, int64_t* lo_io, int64_t* hi_i
     for (int j = r; j < cap; j += TEAM) top_c[j] = -1;
     if (TEAM != 32) __threadfence_block();  // spills visible to the CTA
     team_sync<TEAM>();
-    const int nC = *s_nc;
+    const int nC = *nc;
+    if (r == 0) s_nc[par_nc ^ 1] = 0;  // read by everyone before the last barrier
     // phase B: child rows
     for (int k = i0, x = x0; k < nC;) {
       const int64_t slot = hi + k;
@@ -476,10 +480,10 @@ __device__ void expand_resident(const EnumArgs& a, int64_t* lo_io, int64_t* hi_i
         ++k;
       }
     }
-    team_sync<TEAM>();
+    team_sync<TEAM>();  // child rows, top_c, the reset counter
     const int64_t new_hi = hi + nC;
-    if (r == 0) *s_next = (unsigned long long)new_hi;
-    team_sync<TEAM>();
+    if (r == 0) *s_next = (unsigned long long)new_hi;  // read by the caller after its barrier
+    par_nc ^= 1;
     // stay while the next level fits this team: warp mode for tiny levels,
     // CTA mode for the rest up to the shared-memory cap
     const bool tiny = (int64_t)nC * W <= a.warp_items && nC <= small_cap(W);
@@ -508,7 +512,7 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs
   __shared__ unsigned long long s_next;
   __shared__ unsigned long long s_cand;
   __shared__ int s_stop;
-  __shared__ int s_nc;
+  __shared__ int s_nc[2];
   __shared__ int64_t s_lo, s_hi;
   __shared__ int s_level;
   const int tid = threadIdx.x;
@@ -563,7 +567,7 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs
       const int64_t nP = hi - lo;
       if (a.csr_in_smem && nP <= small_cap(W) && nP * W <= a.warp_items) {
         if (tid < 32) {
-          expand_resident<32>(a, &lo, &hi, &level, &s_next, s_dyn, &s_nc);
+          expand_resident<32>(a, &lo, &hi, &level, &s_next, s_dyn, s_nc);
           if (tid == 0) {
             s_lo = lo;
             s_hi = hi;
@@ -577,7 +581,7 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs
       } else if (a.csr_in_smem && nP <= cta_cap(W)) {
         // every thread runs the same control flow on shared counters, so
         // (lo, hi, level) stay identical across the CTA
-        expand_resident<kEnumThreads>(a, &lo, &hi, &level, &s_next, s_dyn, &s_nc);
+        expand_resident<kEnumThreads>(a, &lo, &hi, &level, &s_next, s_dyn, s_nc);
       } else {
         expand_cta(a, adj, lo, hi, level, &s_next);
       }
