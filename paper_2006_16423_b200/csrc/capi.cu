@@ -843,6 +843,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   // on the critical path; mode 1: old sources in cost-balanced chunks of
   // <= 128 (explicit boundaries).  Both: one cover chunk for level s-1.
   int64_t chunk_len0 = 64, chunk_len1 = 64;
+  int grade = 1;
+  if (const char* e = std::getenv("DSG_GRADE")) grade = std::max(1, std::atoi(e));
   unsigned poll_ns_max = 256;  // measured: 256 ns beats 1 us on C2/C3
   if (const char* e = std::getenv("DSG_CHUNK_LEN")) chunk_len0 = std::max(4, std::atoi(e));
   if (const char* e = std::getenv("DSG_CHUNK_LEN1")) chunk_len1 = std::max(4, std::atoi(e));
@@ -868,8 +870,14 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     // nested sources in level s-1, so that critical chunk evaluates a handful
     // of pairs instead of scanning the whole level.
     if (pl.persistent && pl.mode[s] == 0) {
-      const int64_t R = lat.level_off[s - 1], R2 = s >= 2 ? lat.level_off[s - 2] : 0;
-      chunks = (R2 + chunk_len0 - 1) / chunk_len0 + (R - R2 + chunk_len1 - 1) / chunk_len1 + 1;
+      // as mode0_chunk (persistent.cu): old levels, graded recent levels, cover
+      const int G = std::min(grade, s - 1);
+      const int64_t Rg = lat.level_off[s - 1 - G];
+      chunks = (Rg + chunk_len0 - 1) / chunk_len0 + 1;
+      for (int d = G; d >= 1; --d) {
+        const int64_t len = std::min(chunk_len0, chunk_len1 << (d - 1));
+        chunks += (lat.level_off[s - d] - lat.level_off[s - 1 - d] + len - 1) / len;
+      }
       chunk_base[s] = -1;
       pl.chunk_len[s] = chunk_len0;
     } else if (pl.persistent) {
@@ -925,6 +933,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.stage = 1;
   if (const char* e = std::getenv("DSG_STAGE")) PP.stage = std::atoi(e) != 0;
   PP.chunk_len1 = (int)chunk_len1;
+  PP.grade = grade;
   PP.poll_ns_max = poll_ns_max;
   // work items in readiness order, built on the device (launch_build_items):
   // buckets by dep = level of the chunk's last source, critical items first;

@@ -165,6 +165,7 @@ struct PersistPlan {
   // because those items gate level s.  Mode-1 levels list their
   // boundaries: [chunk_lo[b+c], chunk_lo[b+c+1]), b = chunk_base[s].
   int chunk_len0, chunk_len1;
+  int grade;                 // recent levels chunked by slack (see mode0_chunk)
   int stage;                 // stage old mode-0 chunks in shared memory
   unsigned poll_ns_max;      // dependency-wait backoff cap
   const int64_t* chunk_lo;

@@ -71,27 +71,36 @@ __device__ __forceinline__ void atomic_min_v(int64_t* p, int64_t v) {
   atomicMin(reinterpret_cast<long long*>(p), (long long)v);
 }
 
-// Implicit mode-0 chunk boundaries (see PersistPlan::chunk_len0): old
-// sources [c*len0, ...) below R = level_off[s-1]; the last chunk is the cover
-// chunk (each target's lower covers, all in level s-1): s0 = s1 = -1.
-// Level s-2's sources (the semi-critical chunks: they wait for level s-2,
-// which completes just before level s-1 does) use the shorter length
-// chunk_len1.
+// Implicit mode-0 chunk boundaries.  An item's latency under full load
+// grows with its length, and an item whose last source is in level s-1-d
+// has d levels of slack before it gates level s.  So the recent levels are
+// chunked short, graded by that slack: level s-1-d (d = 1..grade) in chunks
+// of min(len0, len1 << (d-1)); everything older (levels <= s-2-grade) in
+// chunks of len0; the last chunk is the cover chunk (each target's lower
+// covers, all in level s-1): s0 = s1 = -1.
 __device__ __forceinline__ void mode0_chunk(const PersistPlan& p, int s, int64_t c, int64_t& s0,
                                             int64_t& s1) {
-  const int64_t R = p.level_off[s - 1];
-  const int64_t R2 = s >= 2 ? p.level_off[s - 2] : 0;
-  const int64_t n_old = (R2 + p.chunk_len0 - 1) / p.chunk_len0;
-  const int64_t n_mid = (R - R2 + p.chunk_len1 - 1) / p.chunk_len1;
+  const int G = min(p.grade, s - 1);
+  const int64_t Rg = p.level_off[s - 1 - G];
+  const int64_t n_old = (Rg + p.chunk_len0 - 1) / p.chunk_len0;
   if (c < n_old) {
     s0 = c * p.chunk_len0;
-    s1 = min(s0 + p.chunk_len0, R2);
-  } else if (c < n_old + n_mid) {
-    s0 = R2 + (c - n_old) * p.chunk_len1;
-    s1 = min(s0 + p.chunk_len1, R);
-  } else {
-    s0 = s1 = -1;
+    s1 = min(s0 + p.chunk_len0, Rg);
+    return;
   }
+  c -= n_old;
+  for (int d = G; d >= 1; --d) {
+    const int64_t lo = p.level_off[s - 1 - d], hi = p.level_off[s - d];
+    const int64_t len = min((int64_t)p.chunk_len0, (int64_t)p.chunk_len1 << (d - 1));
+    const int64_t n = (hi - lo + len - 1) / len;
+    if (c < n) {
+      s0 = lo + c * len;
+      s1 = min(s0 + len, hi);
+      return;
+    }
+    c -= n;
+  }
+  s0 = s1 = -1;
 }
 
 // Mode 0 cover chunk: lane = target, warp w takes covers w, w+4, ... of it.
