@@ -679,19 +679,57 @@ __device__ __forceinline__ bool lex_less(const uint64_t* a, const uint64_t* b, i
   return false;
 }
 
-__global__ void lex_rank_scatter_kernel(int W, int64_t total, const uint64_t* __restrict__ bits,
-                                        const uint64_t* __restrict__ maxm,
-                                        const int32_t* __restrict__ level_of,
-                                        const int64_t* __restrict__ level_off,
-                                        uint64_t* __restrict__ out_bits,
-                                        uint64_t* __restrict__ out_maxm) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  int s = level_of[i];
-  int64_t lo = level_off[s], hi = level_off[s + 1];
-  const uint64_t* bi = bits + (size_t)i * W;
-  int64_t rank = 0;
-  for (int64_t j = lo; j < hi; ++j) rank += lex_less(bits + (size_t)j * W, bi, W) ? 1 : 0;
+constexpr int kRankRows = 64;   // ideals ranked per CTA
+constexpr int kRankParts = 4;   // threads per ideal (each takes every 4th row)
+
+__global__ void __launch_bounds__(kRankRows* kRankParts)
+    lex_rank_scatter_kernel(int W, int64_t total, const uint64_t* __restrict__ bits,
+                            const uint64_t* __restrict__ maxm, const int32_t* __restrict__ level_of,
+                            const int64_t* __restrict__ level_off, uint64_t* __restrict__ out_bits,
+                            uint64_t* __restrict__ out_maxm) {
+  extern __shared__ uint64_t s_tile[];  // [tile rows][W], bit-reversed
+  __shared__ int s_part[kRankParts][kRankRows];
+  const int row = threadIdx.x % kRankRows, part = threadIdx.x / kRankRows;
+  const int64_t i0 = (int64_t)blockIdx.x * kRankRows;
+  const int64_t i = i0 + row;
+  const bool act = i < total;
+  const int64_t il = min(i, total - 1);
+  const int s = level_of[il];
+  const int64_t lo = level_off[s], hi = level_off[s + 1];
+  const uint64_t* bi = bits + (size_t)il * W;
+  int rank = 0;
+  if (W <= 8) {
+    // bit-reversed words: lex_less(a, b) <=> rev(a) > rev(b) as a big-endian
+    // multi-word integer (the smallest differing index becomes the most
+    // significant differing bit), so a comparison is a plain word compare.
+    // The CTA tiles the union of its rows' levels through shared memory.
+    uint64_t key[8];
+    for (int w = 0; w < W; ++w) key[w] = __brevll(bi[w]);
+    const int64_t il_last = min(i0 + kRankRows, total) - 1;
+    const int64_t ulo = level_off[level_of[i0]], uhi = level_off[level_of[il_last] + 1];
+    const int tile = kRankRows * kRankParts;
+    for (int64_t t0 = ulo; t0 < uhi; t0 += tile) {
+      const int n = (int)min((int64_t)tile, uhi - t0);
+      __syncthreads();
+      for (int k = threadIdx.x; k < n * W; k += blockDim.x)
+        s_tile[k] = __brevll(bits[(size_t)t0 * W + k]);
+      __syncthreads();
+      const int j0 = (int)max((int64_t)0, lo - t0), j1 = (int)min((int64_t)n, hi - t0);
+      for (int j = j0 + part; j < j1; j += kRankParts) {
+        const uint64_t* bj = s_tile + (size_t)j * W;
+        int w = 0;
+        while (w < W - 1 && bj[w] == key[w]) ++w;
+        rank += bj[w] > key[w] ? 1 : 0;
+      }
+    }
+  } else {
+    for (int64_t j = lo + part; j < hi; j += kRankParts)
+      rank += lex_less(bits + (size_t)j * W, bi, W) ? 1 : 0;
+  }
+  s_part[part][row] = rank;
+  __syncthreads();
+  if (part != 0 || !act) return;
+  for (int q = 1; q < kRankParts; ++q) rank += s_part[q][row];
   uint64_t* o = out_bits + (size_t)(lo + rank) * W;
   uint64_t* om = out_maxm + (size_t)(lo + rank) * W;
   const uint64_t* mi = maxm + (size_t)i * W;
@@ -799,10 +837,10 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
 void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
                      const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,
                      uint64_t* out_maxm, cudaStream_t st) {
-  int threads = 256;
-  int64_t blocks = (total + threads - 1) / threads;
-  lex_rank_scatter_kernel<<<(unsigned)blocks, threads, 0, st>>>(W, total, bits, maxm, level_of,
-                                                                 level_off, out_bits, out_maxm);
+  const int64_t blocks = (total + kRankRows - 1) / kRankRows;
+  const size_t smem = W <= 8 ? (size_t)kRankRows * kRankParts * W * sizeof(uint64_t) : 0;
+  lex_rank_scatter_kernel<<<(unsigned)blocks, kRankRows * kRankParts, smem, st>>>(
+      W, total, bits, maxm, level_of, level_off, out_bits, out_maxm);
   count_launch();
 }
 

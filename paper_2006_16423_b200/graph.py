@@ -241,22 +241,36 @@ class AccParts:
     unsupported: bool = False
 
 
+def _fsum(vals: Iterable[Num]) -> Num:
+    """Exact sum of rationals (INF absorbing): numerators summed per
+    denominator with Python ints, one Fraction per distinct denominator —
+    the same value as a Rat accumulation in any order, without a gcd per
+    addition."""
+    acc: Dict[int, int] = {}
+    for x in vals:
+        if isinstance(x, float):
+            if x == INF:
+                return INF
+            x = Fraction(x)
+        d = x.denominator
+        acc[d] = acc.get(d, 0) + x.numerator
+    total = Fraction(0)
+    for d, n in acc.items():
+        total += Fraction(n, d)
+    return total
+
+
 def acc_cost_parts(g: Graph, s: Iterable[int]) -> AccParts:
     """graph.cpp:397-428: comm_in charges each outside producer once."""
     s = set(s)
     p = AccParts()
-    for v in sorted(s):
-        n = g.node(v)
-        if not n.acc_supported():
-            p.unsupported = True
-        else:
-            p.proc += n.acc_time
-        p.mem += n.mem_size
-        if any(w not in s for w in g.out(v)):
-            p.comm_out += n.comm_time
+    nodes = [g.node(v) for v in s]
+    p.unsupported = any(not n.acc_supported() for n in nodes)
+    p.proc = _fsum(n.acc_time for n in nodes if n.acc_supported())
+    p.mem = _fsum(n.mem_size for n in nodes)
+    p.comm_out = _fsum(g.node(v).comm_time for v in s if any(w not in s for w in g.out(v)))
     producers = {u for v in s for u in g.in_(v) if u not in s}
-    for u in sorted(producers):
-        p.comm_in += g.node(u).comm_time
+    p.comm_in = _fsum(g.node(u).comm_time for u in producers)
     return p
 
 
@@ -278,10 +292,7 @@ def acc_cost(g: Graph, s: Iterable[int], config: DeviceConfig) -> Num:
 
 
 def cpu_cost(g: Graph, s: Iterable[int]) -> Num:
-    total: Num = Fraction(0)
-    for v in s:
-        total += g.node(v).cpu_time
-    return total
+    return _fsum(g.node(v).cpu_time for v in s)
 
 
 def _replicated(load: Num, mem: Num, r: int, config: DeviceConfig) -> Num:
@@ -311,7 +322,7 @@ def make_canonical_split(g: Graph, config: DeviceConfig, blocks: List[SplitBlock
             split.assignment[g.id_of(v)] = pl
         load = cpu_cost(g, b.members) if b.cpu else acc_cost(g, b.members, config)
         if not b.cpu and b.repl > 1:
-            mem = sum((g.node(v).mem_size for v in b.members), Fraction(0))
+            mem = _fsum(g.node(v).mem_size for v in b.members)
             load = _replicated(load, mem, b.repl, config)
             split.replication[pl.label()] = b.repl
             for r in range(b.repl):
