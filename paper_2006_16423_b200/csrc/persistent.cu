@@ -532,13 +532,17 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       }
       PrePair<V> q{};
       if (has) q = pre_pair<V, TRAIN, 1>(a, x, my, s_tgt, s_int);
-      if (!wait_level(p, item.w, true)) break;  // acquire (ends with __syncthreads)
+      // the finisher first waits for its target's other chunks (they depend
+      // on older levels and are usually done long before level s-1), and
+      // loads their merged minima (cell tid) before the level wait, so
+      // neither round trip sits on the level-to-level chain
       if (fin && chunks > 1 &&
           !wait_count(p, p.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1)))
         break;
-      tr1 = p.trace ? globaltimer() : 0;
-      V kv = INF;  // the other chunks' merged minimum of cell tid (finisher)
+      V kv = INF;
       if (fin && tid < C) kv = __ldcg(key + tid);
+      if (!wait_level(p, item.w, true)) break;  // acquire (ends with __syncthreads)
+      tr1 = p.trace ? globaltimer() : 0;
       if (has) post_pair<V, LP1, KP1MAX, TS, CX>(a, q, my, best, colv);
       nested_total += q.nested ? 1u : 0u;
       if (fin) {
