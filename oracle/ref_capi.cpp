@@ -119,8 +119,13 @@ int guarded(char* msg, int64_t* budget_limit, F&& f) {
 
 }  // namespace
 
-extern "C" int dsgref_dp_solve(int32_t mode, const dsg_graph* graph, const dsg_config* config,
-                               const dsg_options* options, dsg_result* result) {
+namespace {
+
+// mode DSG_MODE_* or kModeDpl (solve_dpl with `seed`, dp_solver.cpp:462-477)
+constexpr int32_t kModeDpl = 100;
+
+int solve_into(int32_t mode, uint64_t seed, const dsg_graph* graph, const dsg_config* config,
+               const dsg_options* options, dsg_result* result) {
   std::memset(result, 0, sizeof *result);
   result->best_k = result->best_l = -1;
   result->n_pairs = -1;
@@ -134,7 +139,8 @@ extern "C" int dsgref_dp_solve(int32_t mode, const dsg_graph* graph, const dsg_c
       opt.deadline = std::chrono::steady_clock::now() +
                      std::chrono::nanoseconds(static_cast<long long>(options->deadline_seconds * 1e9));
     }
-    Split s = mode == DSG_MODE_TRAINING     ? solve_maxload_training(g, cfg, opt)
+    Split s = mode == kModeDpl              ? solve_dpl(g, cfg, seed, opt)
+              : mode == DSG_MODE_TRAINING   ? solve_maxload_training(g, cfg, opt)
               : mode == DSG_MODE_REPLICATED ? solve_maxload_replicated(g, cfg, opt)
                                             : solve_maxload_inference(g, cfg, opt);
     result->objective = from_rat(s.objective_value);
@@ -166,6 +172,27 @@ extern "C" int dsgref_dp_solve(int32_t mode, const dsg_graph* graph, const dsg_c
   result->t_total_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return st;
+}
+
+}  // namespace
+
+extern "C" int dsgref_dp_solve(int32_t mode, const dsg_graph* graph, const dsg_config* config,
+                               const dsg_options* options, dsg_result* result) {
+  return solve_into(mode, 0, graph, config, options, result);
+}
+
+// solve_dpl (dp_solver.cpp:462-477) and seeded_topo_order (407-438): the
+// checkers for the DPL row of SURVEY 8(f).
+extern "C" int dsgref_dpl_solve(const dsg_graph* graph, const dsg_config* config, uint64_t seed,
+                                const dsg_options* options, dsg_result* result) {
+  return solve_into(kModeDpl, seed, graph, config, options, result);
+}
+
+extern "C" int dsgref_topo_order(const dsg_graph* graph, uint64_t seed, int32_t* out) {
+  Graph g = to_graph(graph);
+  std::vector<int> order = seeded_topo_order(g, seed);
+  for (size_t i = 0; i < order.size(); ++i) out[i] = order[i];
+  return static_cast<int>(order.size());
 }
 
 extern "C" void dsgref_result_free(dsg_result* r) {

@@ -4,6 +4,8 @@ behind the reference's solver API.
 
 Reference API → this package:
   solve_maxload_inference / _training   (dp_solver.hpp:21-29)  → solver.*
+  solve_maxload_replicated, seeded_topo_order, linearize, solve_dpl
+                                        (dp_solver.hpp:36-52)  → solver.*
   enumerate_ideals / _within            (graph.hpp:253-258)     → solver.*
   Graph, Node, Edge, DeviceConfig, Split (graph.hpp)             → graph.*
   InfeasibleError, DeadlineExceeded, …  (errors.hpp)            → errors.*
@@ -15,7 +17,8 @@ from .graph import (INF, AccParts, DeviceConfig, Edge, Graph, Interleaving, Node
                     combine_interleaving, cpu_cost, is_contiguous, is_ideal, make_canonical_split,
                     make_node, recompute_maxload, verify_split)
 from .solver import (IdealIndex, SolveOptions, enumerate_ideals, enumerate_ideals_within,
-                     kernel_launch_count, load_library, solve_maxload_inference,
+                     kernel_launch_count, linearize, load_library, seeded_topo_order,
+                     solve_dpl, solve_maxload_inference,
                      solve_maxload_replicated, solve_maxload_training)
 
 __all__ = [
@@ -25,6 +28,6 @@ __all__ = [
     "acc_cost_parts", "combine_interleaving", "cpu_cost", "is_contiguous", "is_ideal",
     "make_canonical_split", "make_node", "recompute_maxload", "verify_split", "IdealIndex",
     "SolveOptions", "enumerate_ideals", "enumerate_ideals_within", "kernel_launch_count",
-    "load_library", "solve_maxload_inference", "solve_maxload_replicated",
+    "linearize", "load_library", "seeded_topo_order", "solve_dpl", "solve_maxload_inference", "solve_maxload_replicated",
     "solve_maxload_training",
 ]

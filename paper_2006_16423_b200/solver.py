@@ -275,6 +275,72 @@ def solve_maxload_replicated(g: Graph, config: DeviceConfig, opt: Optional[Solve
     return _solve(_abi.DSG_MODE_REPLICATED, g, config, opt)
 
 
+def seeded_topo_order(g: Graph, seed: int) -> List[int]:
+    """dp_solver.hpp:39-41 (dp_solver.cpp:407-438): DFS topological order,
+    roots and every out_all list shuffled by one SplitMix64 stream keyed on
+    `seed`, reversed post-order.  Host-side ordering, not on the hot path."""
+    from .workloads import MASK64, SplitMix64
+    rng = SplitMix64((seed * 0x9E3779B97F4A7C15 + 0x2545F4914F6CDD1D) & MASK64)
+    n = g.size()
+    roots = list(range(n))
+    rng.shuffle(roots)
+    succ = []
+    for v in range(n):
+        lst = list(g.out_all(v))
+        rng.shuffle(lst)
+        succ.append(lst)
+    seen = [False] * n
+    post: List[int] = []
+    for r in roots:
+        if seen[r]:
+            continue
+        seen[r] = True
+        stack = [[r, 0]]
+        while stack:
+            top = stack[-1]
+            if top[1] < len(succ[top[0]]):
+                w = succ[top[0]][top[1]]
+                top[1] += 1
+                if not seen[w]:
+                    seen[w] = True
+                    stack.append([w, 0])
+            else:
+                post.append(top[0])
+                stack.pop()
+    post.reverse()
+    return post
+
+
+def _chain_along(g: Graph, order: List[int]) -> Graph:
+    """Artificial precedence edges between consecutive nodes of `order`
+    (dp_solver.cpp:443-454); existing real/artificial pairs are not repeated."""
+    from .graph import Edge
+    have = {(e.src, e.dst) for e in g.edges()} | {(e.src, e.dst) for e in g.artificial_edges()}
+    art = list(g.artificial_edges())
+    for a, b in zip(order, order[1:]):
+        pair = (g.id_of(a), g.id_of(b))
+        if pair not in have:
+            have.add(pair)
+            art.append(Edge(*pair))
+    return Graph(g.nodes(), g.edges(), art)
+
+
+def linearize(g: Graph, seed: int) -> Graph:
+    """dp_solver.hpp:43-46: the |V|+1-prefix chain along seeded_topo_order."""
+    return _chain_along(g, seeded_topo_order(g, seed))
+
+
+def solve_dpl(g: Graph, config: DeviceConfig, seed: int, opt: Optional[SolveOptions] = None):
+    """dp_solver.hpp:48-52 (dp_solver.cpp:462-477): linearize (forward part
+    only for training graphs), then the exact device DP on the chained graph."""
+    training = g.has_backward_nodes()
+    order = seeded_topo_order(g, seed)
+    if training:
+        order = [v for v in order if not g.node(v).is_backward]
+    chained = _chain_along(g, order)
+    return (solve_maxload_training if training else solve_maxload_inference)(chained, config, opt)
+
+
 @dataclass
 class IdealIndex:
     """graph.hpp:243-249: ideals in size-major, lexicographic order."""

@@ -69,3 +69,40 @@ def objective_or_inf(kind: str, mode: int, g: Graph, cfg: DeviceConfig):
         return dp(kind, mode, g, cfg).objective
     except InfeasibleError:
         return INF
+
+
+def ref_topo_order(g: Graph, seed: int):
+    """seeded_topo_order of the unmodified reference (dp_solver.cpp:407-438)."""
+    lib = _load("ref")
+    if lib is None:
+        raise FileNotFoundError("oracle/_ref not built")
+    fn = lib.dsgref_topo_order
+    fn.argtypes = [C.POINTER(_abi.dsg_graph), C.c_uint64, C.POINTER(C.c_int32)]
+    fn.restype = C.c_int
+    pg = _abi.pod_graph(g)
+    out = (C.c_int32 * max(1, g.size()))()
+    n = fn(C.byref(pg.struct), seed, out)
+    return [int(out[i]) for i in range(n)]
+
+
+def ref_dpl(g: Graph, cfg: DeviceConfig, seed: int):
+    """solve_dpl of the unmodified reference (dp_solver.cpp:462-477)."""
+    from paper_2006_16423_b200.errors import raise_for_status
+    from paper_2006_16423_b200.solver import _raw_from
+    lib = _load("ref")
+    if lib is None:
+        raise FileNotFoundError("oracle/_ref not built")
+    fn = lib.dsgref_dpl_solve
+    fn.argtypes = [C.POINTER(_abi.dsg_graph), C.POINTER(_abi.dsg_config), C.c_uint64,
+                   C.POINTER(_abi.dsg_options), C.POINTER(_abi.dsg_result)]
+    fn.restype = C.c_int
+    pg = _abi.pod_graph(g)
+    pc = _abi.pod_config(cfg)
+    po = _abi.pod_options(_abi.DSG_DEFAULT_IDEAL_BUDGET, 0.0, -1, 1, 0, 0)
+    res = _abi.dsg_result()
+    fn(C.byref(pg.struct), C.byref(pc), seed, C.byref(po), C.byref(res))
+    try:
+        raise_for_status(res.status, res.message, res.budget_limit)
+        return _raw_from(res, cfg)
+    finally:
+        lib.dsgref_result_free(C.byref(res))
