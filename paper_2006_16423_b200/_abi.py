@@ -190,26 +190,18 @@ class PodGraph:
         rt = np.dtype([("num", np.int64), ("den", np.int64)])
 
         def rats(attr):
-            # plain lists first, one bulk fill (a per-element structured
-            # assignment costs ~1 us each)
-            nums, dens = [], []
-            for nd in nodes:
-                x = getattr(nd, attr)
-                if type(x) is Fraction:
-                    nums.append(x.numerator)
-                    dens.append(x.denominator)
-                elif type(x) is int:
-                    nums.append(x)
-                    dens.append(1)
-                else:
-                    q, d = to_dsg_rat(x)
-                    nums.append(q)
-                    dens.append(d)
-            a = np.zeros(max(n, 1), dtype=rt)
-            if n:
-                a["num"][:n] = nums
-                a["den"][:n] = dens
-            return a
+            # one pass per column over Fraction's slots into an (n, 2) int64
+            # buffer viewed as dsg_rat (properties and per-element structured
+            # assignment dominate otherwise)
+            a = np.zeros((max(n, 1), 2), dtype=np.int64)
+            try:
+                a[:n, 0] = [getattr(nd, attr)._numerator for nd in nodes]
+                a[:n, 1] = [getattr(nd, attr)._denominator for nd in nodes]
+            except AttributeError:  # int / float / INF weights
+                pairs = [to_dsg_rat(getattr(nd, attr)) for nd in nodes]
+                a[:n, 0] = [q for q, _ in pairs]
+                a[:n, 1] = [d for _, d in pairs]
+            return a.view(rt).reshape(-1)
 
         self.cpu = rats("cpu_time")
         self.acc = rats("acc_time")
