@@ -35,7 +35,11 @@ namespace {
 
 namespace cg = cooperative_groups;
 
-constexpr int kEnumThreads = 1024;
+// measured on C2 / C4 / C5 (tools/build_variant.py): 1024 beats 512 and 256
+#ifndef DSG_ENUM_THREADS
+#define DSG_ENUM_THREADS 1024
+#endif
+constexpr int kEnumThreads = DSG_ENUM_THREADS;
 
 __device__ __forceinline__ uint64_t above_mask(int v, int w) {
   // bits with index > v inside word w

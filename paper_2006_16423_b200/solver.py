@@ -18,7 +18,9 @@ from .errors import DeviceError, raise_for_status
 from .graph import DeviceConfig, Graph, SplitBlock, make_canonical_split
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdsg_b200.so")
+# DSG_B200_LIB: an alternative build of the same library (kernel variants
+# under test); the default is the in-tree build.
+LIB_PATH = os.environ.get("DSG_B200_LIB") or os.path.join(_HERE, "libdsg_b200.so")
 _lib: Optional[C.CDLL] = None
 
 
