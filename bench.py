@@ -275,7 +275,6 @@ def run_ours(args, world, rank, local):
             raw = sess.run()
             h2d.append(up["h2d_bytes"])
         else:
-            from paper_2006_16423_b200 import _abi
             _abi.pod_graph(w.graph)  # the flatten run_dp would do, timed on its own
             t_flat = time.perf_counter()
             raw = solver.run_dp(lib, "dsg", mode, w.graph, w.config, solver.SolveOptions(device=local))
