@@ -248,6 +248,7 @@ struct TraceState {
   int32_t n_blocks;
   int32_t best_k, best_l;
   int64_t best_value;
+  uint32_t arrivals;  // search CTAs done this step; the last one decides
 };
 
 struct TraceBuffers {

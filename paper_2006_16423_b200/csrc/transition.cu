@@ -127,6 +127,7 @@ __global__ void traceback_init_kernel(int64_t I, int K, int L, const V* dp, Trac
   const V best = row[K * lp1 + L];
   st->best_value = (int64_t)best;
   st->n_blocks = 0;
+  st->arrivals = 0;
   if (best == INF) {
     st->status = 2;  // infeasible
     return;
@@ -152,14 +153,22 @@ __global__ void traceback_init_kernel(int64_t I, int K, int L, const V* dp, Trac
   st->status = (I - 1 == 0 && bk == 0 && bl == 0) ? 1 : 0;
 }
 
+template <typename V>
+__device__ void traceback_decide(int K, int L, int W, int AW, const V* dp, const uint64_t* abits,
+                                 V dv, int32_t dg, TraceState* st, int64_t* ords,
+                                 int64_t* prevs, int32_t* kinds, uint64_t* block_bits);
+
 // The direct (pre-monotone) minimum of cell (ord, k, l) and its smallest
 // argmin, one partial per CTA; sources are spread over the whole grid.
 template <typename V, bool TRAIN>
 __global__ void __launch_bounds__(256) traceback_search_kernel(const LevelLaunch a,
-                                                               const TraceState* st,
+                                                               TraceState* st,
                                                                const int32_t* level_of,
                                                                const int64_t* level_off,
-                                                               V* part_v, int32_t* part_g) {
+                                                               V* part_v, int32_t* part_g,
+                                                               int64_t* ords, int64_t* prevs,
+                                                               int32_t* kinds,
+                                                               uint64_t* block_bits) {
   constexpr V INF = VTraits<V>::INF;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ V red_v[256];
@@ -214,24 +223,49 @@ __global__ void __launch_bounds__(256) traceback_search_kernel(const LevelLaunch
     }
     __syncthreads();
   }
+  // the last CTA to arrive reduces the partials and takes the step
+  // (threadFenceReduction pattern: no separate decide launch per step)
+  __shared__ bool s_last;
   if (threadIdx.x == 0) {
     part_v[blockIdx.x] = red_v[0];
     part_g[blockIdx.x] = red_g[0];
+    __threadfence();
+    s_last = atomicAdd(&st->arrivals, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  bv = INF;
+  bg = INT_MAX;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+    vmin_arg(bv, bg, __ldcg(part_v + i), __ldcg(part_g + i));
+  red_v[threadIdx.x] = bv;
+  red_g[threadIdx.x] = bg;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      V v = red_v[threadIdx.x];
+      int32_t g = red_g[threadIdx.x];
+      vmin_arg(v, g, red_v[threadIdx.x + off], red_g[threadIdx.x + off]);
+      red_v[threadIdx.x] = v;
+      red_g[threadIdx.x] = g;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st->arrivals = 0;
+    traceback_decide<V>(a.K, a.L, a.W, a.AW, dp, a.abits, red_v[0], red_g[0], st, ords, prevs,
+                        kinds, block_bits);
   }
 }
 
-// Replay monotone_pass's strict tests for cell (ord, k, l) and step.
+// Replay monotone_pass's strict tests for cell (ord, k, l) given its direct
+// minimum (dv, argmin dg), and step.  Run by one thread of the last search CTA.
 template <typename V>
-__global__ void traceback_decide_kernel(int K, int L, int W, int AW, const V* dp,
-                                        const uint64_t* abits,
-                                        const V* part_v, const int32_t* part_g, int n_parts,
-                                        TraceState* st, int64_t* ords, int64_t* prevs,
-                                        int32_t* kinds, uint64_t* block_bits) {
+__device__ void traceback_decide(int K, int L, int W, int AW, const V* dp, const uint64_t* abits,
+                                 V dv, int32_t dg, TraceState* st, int64_t* ords,
+                                 int64_t* prevs, int32_t* kinds, uint64_t* block_bits) {
   constexpr V INF = VTraits<V>::INF;
-  if (st->status != 0 || threadIdx.x != 0) return;
-  V dv = INF;
-  int32_t dg = INT_MAX;
-  for (int i = 0; i < n_parts; ++i) vmin_arg(dv, dg, part_v[i], part_g[i]);
   const int lp1 = L + 1, C = (K + 1) * lp1;
   const int64_t ord = st->ord;
   int k = st->k, l = st->l;
@@ -313,14 +347,12 @@ void traceback_t(const LevelLaunch& L, const int32_t* level_of, const int64_t* l
   for (int step = 0; step <= L.K + L.L; ++step) {
     if (L.training)
       traceback_search_kernel<V, true><<<grid, 256, smem, st>>>(
-          L, b.state, level_of, level_off, (V*)b.part_v, b.part_g);
+          L, b.state, level_of, level_off, (V*)b.part_v, b.part_g, b.ords, b.prevs, b.kinds,
+          b.block_bits);
     else
       traceback_search_kernel<V, false><<<grid, 256, smem, st>>>(
-          L, b.state, level_of, level_off, (V*)b.part_v, b.part_g);
-    traceback_decide_kernel<V><<<1, 32, 0, st>>>(L.K, L.L, L.W, L.AW, (const V*)L.dp, L.abits,
-                                                 (const V*)b.part_v, b.part_g, grid, b.state,
-                                                 b.ords, b.prevs, b.kinds, b.block_bits);
-    count_launch();
+          L, b.state, level_of, level_off, (V*)b.part_v, b.part_g, b.ords, b.prevs, b.kinds,
+          b.block_bits);
     count_launch();
   }
   (void)sm_count;
