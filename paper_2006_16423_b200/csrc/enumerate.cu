@@ -317,19 +317,6 @@ __device__ void expand_thread(const EnumArgs& a, const Adj& g, int64_t lo, int64
   }
 }
 
-// Highest set bit of s strictly below bit t and strictly above bit v, or -1.
-__device__ __forceinline__ int prev_bit(const uint64_t* s, int t, int v) {
-  for (int w = (t - 1) >> 6; w >= 0 && w >= (v >> 6); --w) {
-    uint64_t x = s[w];
-    if (w == (t >> 6)) x &= (t & 63) ? (~0ull >> (64 - (t & 63))) : 0ull;
-    if (x) {
-      const int u = (w << 6) | (63 - __clzll((long long)x));
-      return u > v ? u : -1;
-    }
-  }
-  return -1;
-}
-
 // Resident levels, run by a team — warp 0 alone (TEAM = 32, tiny levels,
 // no CTA barrier) or the whole CTA (TEAM = kEnumThreads) — level after level
 // while the frontier stays in shared memory, without an L2 round trip on the
@@ -407,12 +394,18 @@ __device__ void expand_resident(const EnumArgs& a, int64_t* lo_io, int64_t* hi_i
           const int b = __ffsll((long long)cand) - 1;
           cand &= cand - 1;
           const int v = (x << 6) | b;
-          const int p0 = pu_off[v], p1 = pu_off[v + 1];
+          // canonical <=> every maximal element of J above v is a
+          // predecessor of v: (max(J) ∩ above(v)) \ pred(v) = ∅, word by
+          // word up to the top maximal element's word
           bool canon = true;
-          for (int t = top; t > v && canon; t = prev_bit(M, t, v)) {
-            bool is_pred = false;
-            for (int e = p0; e < p1; ++e) is_pred |= pu_adj[e] == t;
-            canon = is_pred;
+          if (top > v) {
+            const uint64_t* pv = a.pred_u + (size_t)v * W;
+            for (int w = v >> 6; w <= (top >> 6); ++w) {
+              if (M[w] & above_mask(v, w) & ~__ldg(pv + w)) {
+                canon = false;
+                break;
+              }
+            }
           }
           if (!canon) continue;
           const int k = atomicAdd(nc, 1);
