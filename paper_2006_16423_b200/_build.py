@@ -18,8 +18,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdsg_b200.so")
-SOURCES = ["capi.cu", "enumerate.cu", "describe.cu", "transition.cu", "persistent.cu"]
-HEADERS = ["dsg_device.cuh", "dsg_internal.h", "scan.cuh"]
+SOURCES = ["capi.cu", "enumerate.cu", "describe.cu", "transition.cu", "persistent.cu",
+           # the dataflow kernel's variants, one translation unit each (parallel nvcc)
+           "persistent_x_i32_inf.cu", "persistent_x_i32_train.cu",
+           "persistent_g_i32_inf.cu", "persistent_g_i32_train.cu",
+           "persistent_g_i64_inf.cu", "persistent_g_i64_train.cu"]
+HEADERS = ["dsg_device.cuh", "dsg_internal.h", "scan.cuh", "persistent_impl.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -53,14 +57,17 @@ def build_lib(force: bool = False, verbose: bool = False, extra=()) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    hdrs = [d for d in deps if not d.endswith(".cu")]
     for s in SOURCES:
         obj = os.path.join(objdir, s.replace(".cu", ".o"))
+        objs.append(obj)
+        if not force and not extra and not _stale(obj, [os.path.join(CSRC, s), *hdrs]):
+            continue  # object newer than its source and every header
         cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
                "-c", os.path.join(CSRC, s), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
-        objs.append(obj)
     failed = []
     for s, p in procs:
         out, _ = p.communicate()

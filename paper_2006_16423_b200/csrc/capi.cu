@@ -205,6 +205,7 @@ struct Prepared {
   int interleave = 0;
   bool has_bw = false;
   bool inf_cpu_mem = false;  // deferred std::domain_error("subtracting infinity")
+  bool neg_comm = false;     // some finite comm_time < 0 (acc >= proc fails under Sum)
   bool repl = false;         // solve_maxload_replicated
   int repl_combine = 0;
   int64_t repl_bn = 1, repl_bd = 1;
@@ -386,6 +387,7 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     P.mem[v] = (int64_t)s;
     P.unsup[v] = qa[v].inf;
     P.comminf[v] = qm[v].inf;
+    if (!qm[v].inf && qm[v].num < 0) P.neg_comm = true;
   }
   if (P.repl) {
     // sync terms reach (K-1)/K * Σ|mem| * b_den / |b_num| on top of the loads
@@ -668,6 +670,12 @@ struct Pipeline {
   unsigned* ctl = nullptr;  // [0] stop, [1] err, [32 + s] level s done
   size_t ctl_words = 0;
   int rank = 0, world = 1;
+  // virtual shards (dsg_options::shard_count > 1): all `world` ranks run in
+  // this process's one cooperative launch, each with its own tables
+  bool virt = false;
+  std::vector<VRank> vranks;  // host copy; [0] aliases the tables above
+  VRank* vranks_d = nullptr;
+  int* tables_bad = nullptr;  // replica comparison after the solve
   std::vector<void*> peer_dp;
   std::vector<int32_t*> peer_bp;
   int64_t* level_off_d = nullptr;
@@ -685,6 +693,17 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   const int W = P.W, K = P.K, Lc = P.L, C = P.C;
   const int vb = P.value_bits;
   const size_t vsz = vb == 32 ? 4 : 8;
+  if (opt->shard_count > 1) {
+    // virtual shards: the multi-GPU wavefront's ranks emulated in one launch
+    if (opt->shard_count > DSG_MAX_SHARDS) throw Fail{DSG_INVALID, "shard_count above DSG_MAX_SHARDS"};
+    if (pl.world > 1 && !pl.virt)
+      throw Fail{DSG_UNSUPPORTED, "virtual shards inside a multi-GPU sharded session"};
+    if (flags & DSG_FLAG_LEVEL_LAUNCH)
+      throw Fail{DSG_UNSUPPORTED, "virtual shards need the persistent level kernel"};
+    pl.virt = true;
+    pl.world = opt->shard_count;
+    pl.rank = 0;
+  }
   const auto t1 = Clock::now();
   pl.lat = enumerate_device(ctx, P, dg, opt->ideal_budget, (flags & DSG_FLAG_HASH_ENUM) != 0, pfx);
   const Lattice& lat = pl.lat;
@@ -775,6 +794,9 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   LL.repl_bn = P.repl_bn;
   LL.repl_bd = P.repl_bd;
   LL.repl_sign = P.repl_sign;
+  // the exact pruning assumes acc(B) >= proc(B), which negative comm weights
+  // break under Interleaving::Sum (graph.cpp:457-467): no pruning then
+  LL.no_prune = (P.neg_comm && P.interleave == DSG_INTERLEAVE_SUM) ? 1 : 0;
   if ((i128)I * (K + 2) >= ((i128)1 << 31))
     throw Fail{DSG_UNSUPPORTED, "ideal count x (accelerators + 2) exceeds the 31-bit argmin"};
   LL.abits = D.abits;
@@ -817,7 +839,16 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     q.stage = 1;
     if (const char* e = std::getenv("DSG_STAGE")) q.stage = std::atoi(e) != 0;
     query_persistent(LL, q, &pl.pinfo);
-    if (opt->reserved > 0) pl.pinfo.blocks = std::min(pl.pinfo.blocks, opt->reserved);
+    if (pl.pinfo.blocks <= 0) {
+      // the CTA's shared memory does not fit (very large (K+1)(L+1) with
+      // 64-bit values): the per-level driver needs none of it
+      if (pl.virt) throw Fail{DSG_UNSUPPORTED, "virtual shards: persistent kernel does not fit"};
+      pl.persistent = false;
+    } else if (opt->reserved > 0) {
+      pl.pinfo.blocks = std::min(pl.pinfo.blocks, opt->reserved);
+    }
+    // every virtual rank needs at least one CTA
+    if (pl.virt) pl.pinfo.blocks = std::max(pl.pinfo.blocks, pl.world);
   }
   const int64_t target_items =
       pl.persistent ? std::max(1, pl.pinfo.blocks) : (int64_t)ctx.sm_count * 8;
@@ -937,41 +968,35 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.poll_ns_max = poll_ns_max;
   // work items in readiness order, built on the device (launch_build_items):
   // buckets by dep = level of the chunk's last source, critical items first;
-  // a sharded solve lists only this rank's units
+  // a sharded solve lists only this rank's units (virtual shards: one list
+  // per rank)
+  std::vector<int64_t> rank_items(pl.virt ? pl.world : 1, 0);
   {
     std::vector<int64_t> pair_off(lat.n_levels + 1, 0);
-    const bool grouped = grouping_enabled(LL);
-    int group_slack = 8;
-    if (const char* e = std::getenv("DSG_GROUP_SLACK")) group_slack = std::max(1, std::atoi(e));
-    pl.total_items = 0;
-    for (int l = 1; l < lat.n_levels; ++l) {
-      pair_off[l + 1] = pair_off[l] + pl.n_chunks[l];
-      const int64_t T = lat.level_off[l + 1] - lat.level_off[l];
-      const int64_t units = pl.mode[l] == 0 ? (T + 31) / 32 : T;
-      const int64_t units_r =
-          pl.world > 1 ? (units > pl.rank ? (units - pl.rank + pl.world - 1) / pl.world : 0) : units;
-      // old mode-0 chunks (their last source below level l-1) are grouped
-      // (grouped: last source level < l - slack; chunk c < n_old ends at
-      // min((c+1)*len, R) - 1, R = level_off[l-1])
-      int64_t n_grp = 0;
-      if (grouped && pl.mode[l] == 0 && l - group_slack >= 1) {
-        const int64_t R = lat.level_off[l - 1];
-        const int64_t n_old = (R + chunk_len0 - 1) / chunk_len0;
-        n_grp = group_slack == 1 ? n_old
-                                 : std::min<int64_t>(n_old, lat.level_off[l - group_slack] / chunk_len0);
+    for (int l = 1; l < lat.n_levels; ++l) pair_off[l + 1] = pair_off[l] + pl.n_chunks[l];
+    auto items_of_rank = [&](int rank) {
+      int64_t total = 0;
+      for (int l = 1; l < lat.n_levels; ++l) {
+        const int64_t T = lat.level_off[l + 1] - lat.level_off[l];
+        const int64_t units = pl.mode[l] == 0 ? (T + 31) / 32 : T;
+        const int64_t units_r =
+            pl.world > 1 ? (units > rank ? (units - rank + pl.world - 1) / pl.world : 0) : units;
+        total += pl.n_chunks[l] * units_r;
       }
-      pl.total_items += n_grp * ((units_r + 3) / 4) + (pl.n_chunks[l] - n_grp) * units_r;
-    }
+      return total;
+    };
+    for (size_t r = 0; r < rank_items.size(); ++r)
+      rank_items[r] = items_of_rank(pl.virt ? (int)r : pl.rank);
+    pl.total_items = rank_items[0];
     ItemBuild B{};
-    B.grouped = grouped ? 1 : 0;
-    PP.grouped = B.grouped;
-    B.group_slack = group_slack;
     B.lag = 1 << 30;
     if (const char* e = std::getenv("DSG_SCHED_LAG")) B.lag = std::max(1, std::atoi(e));
-    // dedicated cover-item CTAs (needs >= 2 CTAs: one of each role)
+    // dedicated cover-item CTAs (needs >= 2 CTAs: one of each role; one
+    // queue per rank with virtual shards)
     int crit_ctas = 0;
     if (const char* e = std::getenv("DSG_CRIT_CTAS")) crit_ctas = std::max(0, std::atoi(e));
     if (crit_ctas >= pl.pinfo.blocks) crit_ctas = pl.pinfo.blocks / 2;
+    if (pl.virt) crit_ctas = 0;
     B.split = crit_ctas > 0 ? 1 : 0;
     PP.crit_ctas = crit_ctas;
     B.n_levels = lat.n_levels;
@@ -987,18 +1012,6 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     pl.items_d = B.items;
     pl.item_build = B;  // launched after the mode table is on the device
   }
-  {
-    int32_t* mode_d = ctx.get_t<int32_t>(pfx + "pp.mode", pl.mode.size());
-    CK(cudaMemcpyAsync(mode_d, pl.mode.data(), sizeof(int32_t) * pl.mode.size(),
-                       cudaMemcpyHostToDevice, st));
-    PP.mode = mode_d;
-    launch_build_items(PP, pl.item_build, st);
-    CK(cudaGetLastError());
-    int cov_bad = 0;
-    D2H(&cov_bad, cov_err, sizeof(int));
-    CK(cudaStreamSynchronize(st));  // host vectors are temporaries
-    if (cov_bad) throw Fail{DSG_CUDA_ERROR, "lower-cover lookup failed"};
-  }
   PP.tile_count = ctx.get_t<unsigned>(pfx + "pp.tile_count", (size_t)pl.total_tiles + 1);
   pl.ctl_words = (size_t)lat.n_levels + 64;
   pl.ctl = ctx.get_t<unsigned>(pfx + "pp.ctl", pl.ctl_words);
@@ -1008,6 +1021,52 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.crit_next = reinterpret_cast<unsigned long long*>(pl.ctl + 4);  // ctl[4..5]
   PP.done = pl.ctl + 32;
   PP.keys = ctx.get_t<unsigned long long>(pfx + "pp.keys", (size_t)I * C);  // value atomics
+  PP.virt = 0;
+  PP.vrank = nullptr;
+  {
+    int32_t* mode_d = ctx.get_t<int32_t>(pfx + "pp.mode", pl.mode.size());
+    CK(cudaMemcpyAsync(mode_d, pl.mode.data(), sizeof(int32_t) * pl.mode.size(),
+                       cudaMemcpyHostToDevice, st));
+    PP.mode = mode_d;
+    launch_build_items(PP, pl.item_build, st);
+    if (pl.virt) {
+      // virtual ranks 1..world-1: everything a rank owns on its own GPU
+      pl.vranks.assign(pl.world, VRank{});
+      pl.vranks[0] = VRank{PP.items, pl.total_items, pl.ctl, PP.tile_count, PP.keys, LL.dp};
+      for (int r = 1; r < pl.world; ++r) {
+        const std::string vp = pfx + "v" + std::to_string(r) + ".";
+        ItemBuild B = pl.item_build;
+        B.rank = r;
+        B.items = ctx.get_t<int4>(vp + "items", (size_t)rank_items[r] + 1);
+        launch_build_items(PP, B, st);
+        VRank& v = pl.vranks[r];
+        v.items = B.items;
+        v.total_items = rank_items[r];
+        v.ctl = ctx.get_t<unsigned>(vp + "ctl", pl.ctl_words);
+        v.tile_count = ctx.get_t<unsigned>(vp + "tile_count", (size_t)pl.total_tiles + 1);
+        v.keys = ctx.get_t<unsigned long long>(vp + "keys", (size_t)I * C);
+        v.dp = ctx.get(vp + "dp", (size_t)I * C * vsz + 64);
+      }
+      pl.peer_dp.assign(pl.world, nullptr);
+      pl.peer_bp.assign(pl.world, nullptr);
+      pl.peer_done.assign(pl.world, nullptr);
+      for (int r = 0; r < pl.world; ++r) {
+        pl.peer_dp[r] = pl.vranks[r].dp;
+        pl.peer_done[r] = pl.vranks[r].ctl + 32;
+      }
+      pl.vranks_d = ctx.get_t<VRank>(pfx + "pp.vranks", pl.world);
+      CK(cudaMemcpyAsync(pl.vranks_d, pl.vranks.data(), sizeof(VRank) * pl.world,
+                         cudaMemcpyHostToDevice, st));
+      pl.tables_bad = ctx.get_t<int>(pfx + "pp.tables_bad", 1);
+      PP.virt = 1;
+      PP.vrank = pl.vranks_d;
+    }
+    CK(cudaGetLastError());
+    int cov_bad = 0;
+    D2H(&cov_bad, cov_err, sizeof(int));
+    CK(cudaStreamSynchronize(st));  // host vectors are temporaries
+    if (cov_bad) throw Fail{DSG_CUDA_ERROR, "lower-cover lookup failed"};
+  }
   // peer tables: this GPU only, until a sharded session attaches its peers
   if (pl.world == 1) {
     pl.peer_dp.assign(1, LL.dp);
@@ -1062,6 +1121,16 @@ void reset_tables(DeviceCtx& ctx, const Prepared& P, Pipeline& pl) {
     // level 0 (the empty ideal) is final before the launch
     launch_fill_u32(pl.PP.done, 1, 1u, st);
     launch_fill_inf(vb, pl.PP.keys, pl.I * P.C, st);
+    // virtual ranks 1..world-1: the same per-rank reset every GPU does
+    for (size_t r = 1; pl.virt && r < pl.vranks.size(); ++r) {
+      const VRank& v = pl.vranks[r];
+      launch_init_empty(vb, P.K, P.L, v.dp, st);
+      CK(cudaMemsetAsync(v.tile_count, 0, sizeof(unsigned) * (pl.total_tiles + 1), st));
+      CK(cudaMemsetAsync(v.ctl, 0, sizeof(unsigned) * pl.ctl_words, st));
+      launch_fill_u32(v.ctl + 32, 1, 1u, st);
+      launch_fill_inf(vb, v.keys, pl.I * P.C, st);
+    }
+    if (pl.virt) CK(cudaMemsetAsync(pl.tables_bad, 0, sizeof(int), st));
   }
   CK(cudaStreamSynchronize(st));
 }
@@ -1114,9 +1183,19 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
     if (PP.trace) write_trace(ctx, pl, trace_file);
     int flags_h[2] = {0, 0};
     D2H(flags_h, PP.stop, sizeof flags_h);
+    int bad = 0;
+    if (pl.virt) {
+      // every rank's replica must equal rank 0's byte for byte: each row
+      // was stored into every table by the rank that finalized it
+      const size_t bytes = (size_t)I * C * (vb == 32 ? 4 : 8);
+      for (int r = 1; r < pl.world; ++r)
+        launch_compare_tables(pl.vranks[0].dp, pl.vranks[r].dp, bytes, pl.tables_bad, st);
+      D2H(&bad, pl.tables_bad, sizeof bad);
+    }
     CK(cudaStreamSynchronize(st));
     if (flags_h[1]) throw Fail{DSG_CUDA_ERROR, "dataflow watchdog fired"};
     if (flags_h[0]) throw Fail{DSG_DEADLINE, "time limit reached"};
+    if (bad) throw Fail{DSG_LOGIC, "virtual shard dp replicas differ"};
   } else {
     CK(cudaEventRecord(ev_desc, st));
     for (int s = 1; s < lat.n_levels; ++s) {

@@ -110,6 +110,7 @@ struct LevelLaunch {
   int64_t repl_bn;     // |bandwidth numerator|
   int64_t repl_bd;     // bandwidth denominator
   int repl_sign;       // sign of the bandwidth
+  int no_prune;        // negative comm under Sum: the generic (unpruned) cells
   int64_t t_lo, t_hi;  // targets
   int64_t s_hi;        // sources [0, s_hi)
   int64_t n_chunks;
@@ -151,6 +152,18 @@ struct LevelLaunch {
 
 void launch_transition(const LevelLaunch& L, cudaStream_t st);
 
+// One virtual rank of a sharded solve emulated on one GPU (dsg_options::
+// shard_count): everything a rank of a multi-GPU solve owns on its own GPU.
+// The cooperative launch gives CTA b to rank b % world.
+struct VRank {
+  const int4* items;          // this rank's readiness-ordered item list
+  int64_t total_items;
+  unsigned* ctl;              // [0] stop [1] err [2..3] claim counter [32 + s] level s done
+  unsigned* tile_count;       // arrival counters of this rank's units
+  unsigned long long* keys;   // merge keys of this rank's targets
+  void* dp;                   // this rank's replica of the dp table (read by its CTAs)
+};
+
 // One cooperative launch for all levels (transition.cu).
 struct PersistPlan {
   int n_levels;
@@ -177,7 +190,6 @@ struct PersistPlan {
   // from one atomic counter, so a CTA never sits on an unready item while
   // ready ones are queued behind it.
   const int4* items;         // [total_items]
-  int grouped;               // grouped items present (4 target column sets)
   unsigned long long* next;  // claim counter, zeroed per solve
   unsigned long long* crit_next;  // claim counter of the cover-item queue
   int crit_ctas;                  // CTAs that run only cover items (0: one queue)
@@ -200,7 +212,12 @@ struct PersistPlan {
   int rank, world;
   void* const* peer_dp;        // [world] dp table of each rank
   int32_t* const* peer_bp;     // [world]
-  unsigned* const* peer_done;  // [world] level counters of each rank
+  unsigned* const* peer_done;  // [world] level counters of each rank (ctl + 32:
+                               // the rank's stop / err words sit at -32 / -31)
+  // virt != 0: all `world` ranks run in this one launch (virtual shards on
+  // one GPU); CTA b is rank b % world and takes its tables from vrank[rank]
+  int virt;
+  const VRank* vrank;          // [world]
 };
 
 struct PersistInfo {
@@ -215,8 +232,6 @@ struct PersistInfo {
 // = dep + 1) first inside each bucket.
 struct ItemBuild {
   int n_levels;
-  int grouped;               // old mode-0 chunks: one item per 4 units
-  int group_slack;           //   ... when their last source level < s - slack
   int lag;                   // list bucket = max(dep, s - lag)
   int split;                 // cover items in their own queue at the front
   const int64_t* pair_off;   // [n_levels + 1] prefix of chunks over levels
@@ -226,8 +241,6 @@ struct ItemBuild {
   int rank, world;
 };
 void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t st);
-// mode-0 chunks over old levels become one item per 4 units (a warp each)
-bool grouping_enabled(const LevelLaunch& L);
 
 void query_persistent(const LevelLaunch& L, const PersistPlan& P, PersistInfo* info);
 void launch_persistent(const LevelLaunch& L, const PersistPlan& P, cudaStream_t st,
@@ -236,6 +249,8 @@ void launch_read_globaltimer(uint64_t* out, cudaStream_t st);
 void launch_fill_u32(unsigned* p, int64_t n, unsigned value, cudaStream_t st);
 void launch_finalize(const LevelLaunch& L, cudaStream_t st);
 void launch_init_empty(int value_bits, int K, int L, void* dp, cudaStream_t st);
+// *bad = 1 if the two tables differ anywhere (virtual-shard replicas)
+void launch_compare_tables(const void* a, const void* b, size_t bytes, int* bad, cudaStream_t st);
 void launch_fill_inf(int value_bits, void* p, int64_t n, cudaStream_t st);
 void launch_level_of(const int64_t* level_off, int n_levels, int64_t I, int32_t* level_of,
                      cudaStream_t st);

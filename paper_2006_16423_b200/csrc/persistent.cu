@@ -1,750 +1,32 @@
-// persistent.cu — every DP level in ONE cooperative launch, as a dataflow
-// wavefront (no grid barriers).
-//
-// The reference walks targets in ordinal order (MaxloadDp::run,
-// /root/reference/proj/src/dp_solver.cpp:319-330).  dp[I] depends only on
-// dp[I'] for I' ⊊ I, all in earlier levels, so:
-//
-//   * the work is a list of items (host plan, capi.cu) sorted by readiness;
-//     CTAs claim the next item from one atomic counter;
-//   * an item scans one chunk of source ordinals for a unit of targets of
-//     level s and first waits (spin on the per-level completion counter)
-//     only until the last level its chunk covers is finished — levels
-//     complete in order, and the chunks that cover old levels start long
-//     before level s-1 is done, so levels overlap;
-//   * every item merges its per-target cell minima (value-only: the argmin
-//     is recovered for the optimal path during traceback); the item that
-//     arrives last for a unit (atomic arrival counter) applies monotone_pass
-//     (dp_solver.cpp:180-193) in registers, writes the dp rows — into every
-//     rank's table when the solve is sharded over GPUs — and bumps the
-//     level's completion counter (release).
-//
-// Two item shapes:
-//   mode 0, lanes own targets (levels with >= 16 targets): item = (group of
-//     32 targets, chunk); each lane owns one target and the 4 warps take
-//     every 4th source of the chunk, so all lanes of a warp read the same
-//     source (broadcast loads, warp-uniform frontier loop).  The warps merge
-//     in shared memory; chunks merge with a value atomicMin.
-//   mode 1, lanes own sources (levels with few targets, e.g. the long chains
-//     of C4): item = (one target, chunk); the CTA's 128 threads each take
-//     sources i, i+128, ...; a warp-shuffle min + shared memory combine them
-//     into one partial per (target, chunk, cell).
-// All CTAs are co-resident (cooperative launch) and items only wait on
-// strictly earlier levels, so the spin waits cannot deadlock; a watchdog
-// aborts (flag) instead of hanging.
+// persistent.cu — host side of the dataflow level kernel: variant dispatch
+// (the kernels live in persistent_impl.cuh, instantiated by persistent_v*.cu)
+// and the device-built, readiness-ordered work-item list.
 #include <climits>
 #include <cstdint>
 #include <cstdlib>
 
-#include "scan.cuh"
+#include "persistent_impl.cuh"
 
 namespace dsg {
 
 namespace {
 
-using namespace scan;
-
-constexpr int kWarps = kTileTargets / 32;  // warps per CTA (4)
-constexpr int kGroup = 32;                 // targets per mode-0 item
-constexpr int kGroupMaxAW = 16;            // grouped items (a column set per warp) up to this
-// The exact-word/exact-cell variants (the C2 hot loop) are held to 64
-// registers so 8 CTAs fit per SM (measured: 7.4 ms vs 8.0 ms at 80
-// registers on C2; the few spills sit off the source loop).  The other
-// variants keep their natural allocation (bounding them spills the hot loop).
-constexpr int kMinBlocksExact = 8;
-#ifndef DSG_MIN_BLOCKS_BIG
-#define DSG_MIN_BLOCKS_BIG 6
-#endif
-// more register cells (e.g. C3's 3x7): a softer cap
-constexpr int kMinBlocksExactBig = DSG_MIN_BLOCKS_BIG;
-constexpr uint64_t kWatchdogNs = 20000000000ull;
-
-template <typename V>
-__device__ __forceinline__ V warp_min(V v) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v = min(v, (V)__shfl_xor_sync(0xffffffffu, v, off));
-  return v;
-}
-
-__device__ __forceinline__ void atomic_min_v(int32_t* p, int32_t v) { atomicMin(p, v); }
-__device__ __forceinline__ void atomic_min_v(int64_t* p, int64_t v) {
-  atomicMin(reinterpret_cast<long long*>(p), (long long)v);
-}
-
-// Implicit mode-0 chunk boundaries.  An item's latency under full load
-// grows with its length, and an item whose last source is in level s-1-d
-// has d levels of slack before it gates level s.  So the recent levels are
-// chunked short, graded by that slack: level s-1-d (d = 1..grade) in chunks
-// of min(len0, len1 << (d-1)); everything older (levels <= s-2-grade) in
-// chunks of len0; the last chunk is the cover chunk (each target's lower
-// covers, all in level s-1): s0 = s1 = -1.
-__device__ __forceinline__ void mode0_chunk(const PersistPlan& p, int s, int64_t c, int64_t& s0,
-                                            int64_t& s1) {
-  const int G = min(p.grade, s - 1);
-  const int64_t Rg = p.level_off[s - 1 - G];
-  const int64_t n_old = (Rg + p.chunk_len0 - 1) / p.chunk_len0;
-  if (c < n_old) {
-    s0 = c * p.chunk_len0;
-    s1 = min(s0 + p.chunk_len0, Rg);
-    return;
-  }
-  c -= n_old;
-  for (int d = G; d >= 1; --d) {
-    const int64_t lo = p.level_off[s - 1 - d], hi = p.level_off[s - d];
-    const int64_t len = min((int64_t)p.chunk_len0, (int64_t)p.chunk_len1 << (d - 1));
-    const int64_t n = (hi - lo + len - 1) / len;
-    if (c < n) {
-      s0 = lo + c * len;
-      s1 = min(s0 + len, hi);
-      return;
-    }
-    c -= n;
-  }
-  s0 = s1 = -1;
-}
-
-// Mode 0 cover chunk: lane = target, warp w takes covers w, w+4, ... of it.
-// Per-lane trip counts differ, so no warp collectives in here.
-template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool CX>
-__device__ __forceinline__ unsigned scan_covers(const LevelLaunch& a, const Target<V>& x, int first,
-                                                int step, const uint64_t* tA, const uint64_t* tInt,
-                                                V* best, V* colv) {
-  constexpr V INF = VTraits<V>::INF;
-  constexpr bool kGeneric = LP1 == 0;
-  constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
-  constexpr V NEG = (V)(-INF - 1);
-  if (!x.active) return 0;
-  const int C = CX ? CMAX : a.C;
-  const int64_t c0 = __ldg(a.cov_off + x.t), c1 = __ldg(a.cov_off + x.t + 1);
-  unsigned n = 0;
-  for (int64_t j = c0 + first; j < c1; j += step) {
-    const int64_t src = __ldg(a.cov + j);
-    ++n;
-    bool gated;
-    V acc, cpu, mem_blk;
-    const V* sdp = (const V*)a.dp + (size_t)src * C;
-    V row[CMAX > 1 ? CMAX - 1 : 1];
-    if constexpr (!kGeneric) {
-#pragma unroll
-      for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? ld_row<false>(sdp + c) : INF;
-      auto need = [&](V proc) {
-        V thr = NEG;
-#pragma unroll
-        for (int c = LP1; c < CMAX; ++c)
-          if (c < C) thr = vmax(thr, row[c - LP1] < best[c] ? best[c] : NEG);
-        return proc < thr;
-      };
-      pair_cost<V, TRAIN, TS>(a, x, src, tA, tInt, gated, acc, cpu, mem_blk, need);
-    } else {
-      pair_cost<V, TRAIN, TS>(a, x, src, tA, tInt, gated, acc, cpu, mem_blk);
-    }
-    if (gated) continue;
-    k4_update<V, LP1, KP1MAX, TS, CX>(a, sdp, row, acc, cpu, mem_blk, best, colv);
-  }
-  return n;
-}
-
-// Release-add without an L1 invalidation (atom.release: MEMBAR.ALL + ATOM;
-// __threadfence() + atomicAdd would add CCTL.IVALL, which discards the L1
-// of every CTA on the SM).  ATOM, not RED: a counter others spin on should
-// reach L2 at once.
-__device__ __forceinline__ unsigned atom_release_add(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-
-// Wait until level j is complete (then so are all levels below it: every
-// unit of level j consumes all of level j-1).  Returns false on stop/err.
-__device__ bool wait_level(const PersistPlan& p, int j, bool acquire = false) {
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) {
-    s_ok = 1;
-    const unsigned need = (unsigned)(p.level_off[j + 1] - p.level_off[j]);
-    if (ld_relaxed_sys(p.done + j) < need) {
-      // polite polling: back off up to ~1 us so the spinning warp does not
-      // steal issue slots from the co-resident CTAs doing the real work
-      unsigned ns = 32, polls = 0;
-      const uint64_t t0 = globaltimer();
-      while (ld_relaxed_sys(p.done + j) < need) {
-        __nanosleep(ns);
-        ns = ns < p.poll_ns_max ? ns * 2 : p.poll_ns_max;
-        if ((++polls & 63) != 0) continue;
-        if (ld_relaxed((const unsigned*)p.stop) != 0) {
-          s_ok = 0;
-          break;
-        }
-        if (globaltimer() - t0 > kWatchdogNs) {
-          atomicExch(p.err, 1);
-          atomicExch(p.stop, 1);
-          s_ok = 0;
-          break;
-        }
-      }
-    }
-    // world == 1: no acquire fence — every later read of data produced in
-    // this kernel (dp rows, keys) goes to L2 (ld.global.cg / cp.async.cg)
-    // and is control-dependent on the counter value just observed, and the
-    // producers released (MEMBAR) before bumping it.  An acquire would
-    // invalidate the whole L1 of the SM (CCTL.IVALL) on every item.
-    // Mode-1 items (one source row per thread: the rows share L1 lines, so
-    // L1-cached loads are much cheaper than per-cell L2 loads) acquire
-    // instead, which invalidates the L1.
-    if (p.world > 1) __threadfence_system();  // peers' NVLink stores
-    else if (acquire) __threadfence();
-    asm volatile("" ::: "memory");
-  }
-  __syncthreads();
-  return s_ok != 0;
-}
-
-// Wait until this GPU's counter *c reaches need (the finisher of a mode-1
-// target waits for the target's other chunks).  Returns false on stop/err.
-__device__ bool wait_count(const PersistPlan& p, const unsigned* c, unsigned need) {
-  __shared__ int s_ok2;
-  if (threadIdx.x == 0) {
-    s_ok2 = 1;
-    if (ld_relaxed(c) < need) {
-      unsigned ns = 32, polls = 0;
-      const uint64_t t0 = globaltimer();
-      while (ld_relaxed(c) < need) {
-        __nanosleep(ns);
-        ns = ns < p.poll_ns_max ? ns * 2 : p.poll_ns_max;
-        if ((++polls & 63) != 0) continue;
-        if (ld_relaxed((const unsigned*)p.stop) != 0) {
-          s_ok2 = 0;
-          break;
-        }
-        if (globaltimer() - t0 > kWatchdogNs) {
-          atomicExch(p.err, 1);
-          atomicExch(p.stop, 1);
-          s_ok2 = 0;
-          break;
-        }
-      }
-    }
-    asm volatile("" ::: "memory");  // keys are read at L2 (see wait_level)
-  }
-  __syncthreads();
-  return s_ok2 != 0;
-}
-
-// Level s gained n finished targets: release their rows, bump the level
-// counter on every rank (system scope when peers read it over NVLink).
-__device__ __forceinline__ void release_done(const PersistPlan& p, int s, unsigned n) {
-  if (p.world == 1) {
-    atom_release_add(p.peer_done[0] + s, n);  // release the rows
-  } else {
-    __threadfence_system();  // rows reached every peer before its counter moves
-    for (int r = 0; r < p.world; ++r) atomicAdd_system(p.peer_done[r] + s, n);
-  }
-}
-
-// Mode 0, one warp: this chunk of `unit` has merged its minima into the
-// keys; count the arrival, and if it is the unit's last chunk apply
-// monotone_pass (dp_solver.cpp:180-193) to the merged cells, store the rows
-// into every rank's table and release them.  Returns whether it finalized.
-template <typename V, int LP1, int CMAX>
-__device__ bool arrive_finalize_unit(const LevelLaunch& a, const PersistPlan& p, int s,
-                                     int64_t unit, int64_t t_lo, int64_t T, int64_t chunks,
-                                     int lane, V* best, V* colv, const V* keys, int C) {
-  constexpr V INF = VTraits<V>::INF;
-  constexpr bool kGeneric = LP1 == 0;
-  constexpr int TS = kGroup;
-  unsigned last = 0;
-  __syncwarp();
-  if (lane == 0) {
-    // release this warp's merges; the last arriver reads the others' at L2
-    last = atom_release_add(p.tile_count + p.tile_base[s] + unit, 1u) == chunks - 1;
-  }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return false;
-  const int64_t n_act = min((int64_t)TS, T - unit * TS);
-  if (lane < n_act) {
-    const int64_t t = t_lo + unit * TS + lane;
-    const V* key = keys + (size_t)t * C;
-    if (!kGeneric) {
-#pragma unroll
-      for (int c = 0; c < CMAX; ++c)
-        if (c < C) best[c] = __ldcg(key + c);
-      monotone_regs<V, LP1, CMAX>(best, C);
-      for (int r = 0; r < p.world; ++r) {
-        V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
-#pragma unroll
-        for (int c = 0; c < CMAX; ++c)
-          if (c < C) dpt[c] = best[c];
-      }
-    } else {
-      for (int c = 0; c < C; ++c) colv[c * TS] = __ldcg(key + c);
-      monotone_strided(colv, TS, a.K, a.L);
-      for (int r = 0; r < p.world; ++r) {
-        V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
-        for (int c = 0; c < C; ++c) dpt[c] = colv[c * TS];
-      }
-    }
-  }
-  __syncwarp();
-  if (lane == 0) release_done(p, s, (unsigned)n_act);
-  return true;
-}
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-
-// Stage a mode-0 old chunk's sources [s0, s1) — bitset rows, records and
-// (16-byte aligned superset of the) dp rows, all contiguous in HBM — into
-// shared memory with 16-byte async copies from all 128 threads: the chunk's
-// loads are in flight at once instead of one dependent round trip per
-// source iteration.  Ends with the CTA barrier.
-template <typename V>
-__device__ __forceinline__ SrcView<V> stage_sources(const LevelLaunch& a, int64_t s0, int64_t s1,
-                                                    int C, unsigned char* st) {
-  const int tid = threadIdx.x;
-  const int64_t n = s1 - s0;
-  const size_t nb = (size_t)n * a.AW * 8, nr = (size_t)n * sizeof(SrcRec);
-  const char* gb = reinterpret_cast<const char*>(a.abits + (size_t)s0 * a.AW);
-  const char* gr = reinterpret_cast<const char*>(a.srec + s0);
-  const size_t d0 = (size_t)s0 * C * sizeof(V), d1 = (size_t)s1 * C * sizeof(V);
-  const size_t da = d0 & ~(size_t)15, de = (d1 + 15) & ~(size_t)15;
-  const char* gd = reinterpret_cast<const char*>(a.dp) + da;
-  unsigned char* sb = st;
-  unsigned char* sr = sb + nb;
-  unsigned char* sd = sr + nr;
-  for (size_t i = (size_t)tid * 16; i < nb; i += kTileTargets * 16) cp_async16(sb + i, gb + i);
-  for (size_t i = (size_t)tid * 16; i < nr; i += kTileTargets * 16) cp_async16(sr + i, gr + i);
-  for (size_t i = (size_t)tid * 16; i < de - da; i += kTileTargets * 16) cp_async16(sd + i, gd + i);
-  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
-  __syncthreads();
-  SrcView<V> v;
-  v.bits = reinterpret_cast<const uint64_t*>(sb);
-  v.rec = reinterpret_cast<const SrcRec*>(sr);
-  v.dp = reinterpret_cast<const V*>(sd + (d0 - da));
-  v.base = s0;
-  return v;
-}
-
-template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
-__device__ __forceinline__ void persistent_body(const LevelLaunch& a, const PersistPlan& p) {
-  constexpr V INF = VTraits<V>::INF;
-  constexpr bool kGeneric = LP1 == 0;
-  constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
-  constexpr int TS = kGroup;
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int s_last, s_any_last;
-  const int W = a.W, C = CX ? CMAX : a.C;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // shared: target columns [G][AW][32] (padded, pad word 0) + interior
-  // [G][W][32] — G = 4 when grouped items exist (one column set per warp),
-  // else 1; mode 1 uses column 0 —, merge buffer [C][32], generic cells
-  // [4 warps][C][32]
-  const int G = p.grouped ? kWarps : 1;  // == grouping_enabled(a)
-  uint64_t* s_tgt = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* s_int = s_tgt + (size_t)G * a.AW * TS;
-  V* m_val = reinterpret_cast<V*>(s_int + (TRAIN ? (size_t)G * W * TS : 0));
-  V* g_val = m_val + (size_t)C * TS;
-  V* colv = g_val + (size_t)warp * C * TS + lane;
-  // staging area for one old chunk's sources (16-byte aligned)
-  unsigned char* st_area = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(g_val + (kGeneric ? (size_t)kWarps * C * TS : 0)) + 15) &
-      ~(uintptr_t)15);
-  V* keys = reinterpret_cast<V*>(p.keys);
-  unsigned nested_total = 0;
-  // Roles: with crit_ctas > 0 the list starts with the cover items (they gate
-  // the levels) and the first crit_ctas CTAs claim only those, so a level's
-  // critical work never queues behind ready background work; the other CTAs
-  // claim the rest.  Every item still waits only for items listed before it
-  // in its own queue or for cover items, which the critical CTAs run in level
-  // order, so neither queue can deadlock.
-  const bool crit_role = (int)blockIdx.x < p.crit_ctas;
-  const int64_t n_crit = p.crit_ctas > 0 ? (int64_t)*p.crit_end : 0;
-  unsigned long long* ctr = crit_role ? p.crit_next : p.next;
-  const int64_t q_lo = crit_role ? 0 : n_crit, q_hi = crit_role ? n_crit : p.total_items;
-  __shared__ long long s_gi;
-  if (tid == 0) {
-    s_gi = q_lo + (long long)atomicAdd(ctr, 1ull);
-    s_any_last = 0;
-  }
-  __syncthreads();
-
-  while (true) {
-    const int64_t gi = s_gi;
-    if (gi >= q_hi) break;
-    const int4 item = __ldg(p.items + gi);
-    // claim the next item now; its latency hides behind this one
-    unsigned long long next_gi = 0;
-    if (tid == 0) next_gi = q_lo + atomicAdd(ctr, 1ull);
-    const int s = item.x;
-    const int64_t unit = item.y;
-    const int64_t chunk = item.z & ((1 << 30) - 1);
-    const int64_t t_lo = p.level_off[s], t_hi = p.level_off[s + 1];
-    const int64_t T = t_hi - t_lo;
-    const int64_t chunks = p.n_chunks[s];
-    const int mode = p.mode[s];
-    int64_t s0, s1;
-    if (mode == 0) {
-      mode0_chunk(p, s, chunk, s0, s1);
-    } else if (chunk < chunks - 1) {
-      s0 = p.chunk_lo[p.chunk_base[s] + chunk];
-      s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
-    } else {
-      s0 = s1 = -1;  // the cover chunk
-    }
-    const uint64_t tr0 = p.trace ? globaltimer() : 0;
-    uint64_t tr1 = 0;
-    if (blockIdx.x == 0 && tid == 0 && p.deadline_ns && globaltimer() > (uint64_t)p.deadline_ns)
-      atomicExch(p.stop, 1);
-    V best[CMAX];
-    bool any_last = false;  // trace: some unit of this item finalized
-    if (mode == 0) {
-      // ------------------------------------ lanes own targets
-      const bool grouped = ((item.z >> 30) & 1) != 0;
-      // grouped (chunks over old levels): warp w owns its own 32-target
-      // unit and scans the whole chunk — the four warps read the same
-      // sources, so three of four reads hit L1, and no cross-warp merge;
-      // split (newest-level chunks, latency-critical): the four warps share
-      // one unit and split the chunk's sources
-      int64_t unit_w = unit;
-      bool wact = true;
-      uint64_t* tcol = s_tgt;
-      uint64_t* icol = s_int;
-      if (grouped) {
-        const int64_t k = unit + warp;  // own-unit index
-        const int64_t units = (T + TS - 1) / TS;
-        const int64_t units_r =
-            p.world > 1 ? (units > p.rank ? (units - p.rank + p.world - 1) / p.world : 0) : units;
-        wact = k < units_r;
-        unit_w = p.world > 1 ? p.rank + (int64_t)p.world * k : k;
-        tcol = s_tgt + (size_t)warp * a.AW * TS;
-        icol = s_int + (size_t)warp * W * TS;
-      }
-      init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
-      Target<V> x = load_target<V, TRAIN, TS>(a, t_lo, t_hi, wact ? unit_w : 0, lane, tcol + lane,
-                                              icol + lane, grouped ? wact : warp == 0);
-      x.active = x.active && wact;
-      // start from the unit's merged minimum so far (other chunks' atomicMin
-      // merges): a valid upper bound that lets the scan prune early
-      if constexpr (!kGeneric) {
-        if (x.active) {
-          const V* key = keys + (size_t)x.t * C;
-#pragma unroll
-          for (int c = 0; c < CMAX; ++c)
-            if (c < C) best[c] = __ldcg(key + c);
-        }
-      }
-      // sources [s0, s1) must be final; the target data and the key seeds
-      // above do not depend on them, so their latency hides behind the wait
-      if (!wait_level(p, item.w)) break;
-      tr1 = p.trace ? globaltimer() : 0;
-      if (grouped) {
-        __syncwarp();
-        if (p.stage) {
-          const SrcView<V> sv = stage_sources<V>(a, s0, s1, C, st_area);  // (CTA barrier)
-          if (wact)
-            nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX, 0, true>(
-                a, x, s0, s1, 1, tcol + lane, icol + lane, best, colv, sv);
-        } else if (wact) {
-          nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
-              a, x, s0, s1, 1, tcol + lane, icol + lane, best, colv);
-        }
-      } else {
-        if (s0 < 0)
-          nested_total += scan_covers<V, LP1, KP1MAX, TRAIN, TS, CX>(a, x, warp, kWarps,
-                                                                     tcol + lane, icol + lane,
-                                                                     best, colv);
-        else if (p.stage)
-          nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX, 0, true>(
-              a, x, s0 + warp, s1, kWarps, tcol + lane, icol + lane, best, colv,
-              stage_sources<V>(a, s0, s1, C, st_area));
-        else
-          nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
-              a, x, s0 + warp, s1, kWarps, tcol + lane, icol + lane, best, colv);
-        // merge the 4 warps into warp 0 through the merge buffer
-        for (int src = 1; src < kWarps; ++src) {
-          __syncthreads();
-          if (warp == src) {
-            if (!kGeneric) {
-#pragma unroll
-              for (int c = 0; c < CMAX; ++c)
-                if (c < C) m_val[c * TS + lane] = best[c];
-            } else {
-              for (int c = 0; c < C; ++c) m_val[c * TS + lane] = colv[c * TS];
-            }
-          }
-          __syncthreads();
-          if (warp == 0) {
-            if (!kGeneric) {
-#pragma unroll
-              for (int c = 0; c < CMAX; ++c)
-                if (c < C) best[c] = min(best[c], m_val[c * TS + lane]);
-            } else {
-              for (int c = 0; c < C; ++c) colv[c * TS] = min(colv[c * TS], m_val[c * TS + lane]);
-            }
-          }
-        }
-      }
-      if (grouped ? wact : warp == 0) {
-        // chunks of a unit merge in L2 with a value atomicMin; the last
-        // arriving chunk finalizes the unit (this warp alone)
-        if (x.active) {
-          V* key = keys + (size_t)x.t * C;
-          if (!kGeneric) {
-#pragma unroll
-            for (int c = 0; c < CMAX; ++c)
-              if (c < C && best[c] != INF) atomic_min_v(key + c, best[c]);
-          } else {
-            for (int c = 0; c < C; ++c)
-              if (colv[c * TS] != INF) atomic_min_v(key + c, colv[c * TS]);
-          }
-        }
-        any_last = arrive_finalize_unit<V, LP1, CMAX>(a, p, s, unit_w, t_lo, T, chunks, lane, best,
-                                                      colv, keys, C);
-      }
-      if (any_last) s_any_last = 1;
-    } else {
-      // ------------------------------------ lanes own sources
-      // Every mode-1 chunk has <= 128 sources (capi.cu), one per thread.
-      // The block costs (K2+K3) are static, so they run before the
-      // dependency wait; after it only the row loads and the min-max update
-      // remain.  The newest chunk (c = chunks-1, the one that gates the
-      // level) is the target's finisher: it waits for the other chunks'
-      // key merges, folds its own minima in and finalizes — no atomic merge
-      // or arrival round trip on the critical path.  The item list puts it
-      // after the target's other chunks, so its wait cannot deadlock.
-      init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
-      const int64_t t = t_lo + unit;
-      const bool fin = chunk == chunks - 1;
-      for (int w = tid; w < a.AW; w += kTileTargets) {
-        s_tgt[w] = __ldg(a.abits + (size_t)t * a.AW + w);
-        if (TRAIN && w < W) s_int[w] = __ldg(a.intbits + (size_t)t * W + w);
-      }
-      const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
-      V* key = keys + (size_t)t * C;
-      __syncthreads();
-      // this thread's source: s0 + tid (old chunk) or the target's cover tid
-      int64_t my = s0 + tid;
-      bool has = my < s1;
-      if (fin) {
-        const int64_t c0 = __ldg(a.cov_off + t), c1 = __ldg(a.cov_off + t + 1);
-        has = c0 + tid < c1;
-        my = has ? (int64_t)__ldg(a.cov + c0 + tid) : 0;
-      }
-      PrePair<V> q{};
-      if (has) q = pre_pair<V, TRAIN, 1>(a, x, my, s_tgt, s_int);
-      // the finisher first waits for its target's other chunks (they depend
-      // on older levels and are usually done long before level s-1), and
-      // loads their merged minima (cell tid) before the level wait, so
-      // neither round trip sits on the level-to-level chain
-      if (fin && chunks > 1 &&
-          !wait_count(p, p.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1)))
-        break;
-      V kv = INF;
-      if (fin && tid < C) kv = __ldcg(key + tid);
-      if (!wait_level(p, item.w, true)) break;  // acquire (ends with __syncthreads)
-      tr1 = p.trace ? globaltimer() : 0;
-      if (has) post_pair<V, LP1, KP1MAX, TS, CX>(a, q, my, best, colv);
-      nested_total += q.nested ? 1u : 0u;
-      if (fin) {
-        // targets with more than 128 lower covers (DAG width > 128)
-        const int64_t c0 = __ldg(a.cov_off + t), c1 = __ldg(a.cov_off + t + 1);
-        for (int64_t j = c0 + tid + kTileTargets; j < c1; j += kTileTargets) {
-          const int64_t src = __ldg(a.cov + j);
-          const PrePair<V> q2 = pre_pair<V, TRAIN, 1>(a, x, src, s_tgt, s_int);
-          post_pair<V, LP1, KP1MAX, TS, CX>(a, q2, src, best, colv);
-          nested_total += 1u;
-        }
-      }
-      // lanes -> warp (shuffle min) -> CTA (shared memory)
-      if (!kGeneric) {
-#pragma unroll
-        for (int c = 0; c < CMAX; ++c) {
-          if (c < C) {
-            const V v = warp_min(best[c]);
-            if (lane == 0) m_val[c * TS + warp] = v;
-          }
-        }
-      } else {
-        for (int c = 0; c < C; ++c) {
-          const V v = warp_min(colv[c * TS]);
-          if (lane == 0) m_val[c * TS + warp] = v;
-        }
-      }
-      __syncthreads();
-      // threads over cells: merge into the keys (value atomicMin), or, for
-      // the finisher, fold in the merged keys
-      for (int c = tid; c < C; c += kTileTargets) {
-        V v = m_val[c * TS];
-#pragma unroll
-        for (int w = 1; w < kWarps; ++w) v = min(v, m_val[c * TS + w]);
-        if (fin) m_val[c * TS] = min(v, c == tid ? kv : __ldcg(key + c));
-        else if (v != INF) atomic_min_v(key + c, v);
-      }
-      __syncthreads();
-      if (!fin) {
-        if (tid == 0) {
-          __threadfence();  // cumulative release of this CTA's merges
-          atomicAdd(p.tile_count + p.tile_base[s] + unit, 1u);
-        }
-      } else if (tid == 0) {
-        if (!kGeneric) {
-#pragma unroll
-          for (int c = 0; c < CMAX; ++c)
-            if (c < C) best[c] = m_val[c * TS];
-          monotone_regs<V, LP1, CMAX>(best, C);
-          for (int r = 0; r < p.world; ++r) {
-            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
-#pragma unroll
-            for (int c = 0; c < CMAX; ++c)
-              if (c < C) dpt[c] = best[c];
-          }
-        } else {
-          monotone_strided(m_val, TS, a.K, a.L);
-          for (int r = 0; r < p.world; ++r) {
-            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
-            for (int c = 0; c < C; ++c) dpt[c] = m_val[c * TS];
-          }
-        }
-        release_done(p, s, 1u);
-        s_any_last = 1;
-      }
-    }
-    __syncthreads();
-    const uint64_t tr2 = p.trace ? globaltimer() : 0;
-    if (p.trace && tid == 0) {
-      uint64_t* tr = p.trace + gi * 4;
-      tr[0] = tr0;
-      tr[1] = tr1;
-      tr[2] = tr2;
-      tr[3] = globaltimer() | (s_any_last ? (1ull << 63) : 0ull);
-    }
-    if (tid == 0) s_any_last = 0;
-    if (tid == 0) s_gi = (long long)next_gi;
-    __syncthreads();
-  }
-  for (int off = 16; off > 0; off >>= 1)
-    nested_total += __shfl_xor_sync(0xffffffffu, nested_total, off);
-  if (lane == 0 && nested_total) atomicAdd(a.pair_counter, (unsigned long long)nested_total);
-}
-
-template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
-__global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const LevelLaunch a,
-                                                                         const PersistPlan p) {
-  persistent_body<V, LP1, KP1MAX, TRAIN, WT, CX>(a, p);
-}
-
-// exact variants: register budget for kMinBlocksExact resident CTAs per SM
-template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
-__global__ void __launch_bounds__(kTileTargets,
-                                  LP1 * KP1MAX <= 9 ? kMinBlocksExact : kMinBlocksExactBig)
-    persistent_levels_kernel_x(const LevelLaunch a, const PersistPlan p) {
-  persistent_body<V, LP1, KP1MAX, TRAIN, WT, CX>(a, p);
-}
-
-}  // namespace
-
-// Grouped items (experimental, env DSG_GROUPING=1): measured slower than
-// split items on C2/C3 — the 4x longer items delay the start of the
-// critical items when a level completes — so off by default.
-bool grouping_enabled(const LevelLaunch& L) {
-  const char* e = std::getenv("DSG_GROUPING");
-  return L.AW <= kGroupMaxAW && e && std::atoi(e) != 0;
-}
-
-namespace {
-
-size_t persist_smem(const LevelLaunch& L, const PersistPlan* P, bool generic, size_t vsz,
-                    bool grouped) {
-  const size_t G = grouped ? kWarps : 1;
-  size_t s = G * kGroup * sizeof(uint64_t) * (L.AW + (L.training ? L.W : 0));  // targets
-  s += (size_t)L.C * kGroup * vsz;                                           // merge buffer
-  if (generic) s += (size_t)kWarps * L.C * kGroup * vsz;
-  if (P && P->stage) {
-    // one old chunk: bitset rows, records, dp rows (+ alignment slack)
-    const size_t n = (size_t)max(P->chunk_len0, P->chunk_len1);
-    s += 16 + n * L.AW * 8 + n * sizeof(SrcRec) + n * L.C * vsz + 32;
-  }
-  return s;
-}
-
-template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT = 0, bool CX = false>
-void run_variant(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
-  const size_t smem = persist_smem(L, P, LP1 == 0, sizeof(V), grouping_enabled(L));
-  void (*kern)(const LevelLaunch, const PersistPlan);
-  if constexpr (CX) kern = persistent_levels_kernel_x<V, LP1, KP1MAX, TRAIN, WT, CX>;
-  else kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN, WT, CX>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTileTargets, smem);
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int full = per_sm * sms;
-  info->per_sm = per_sm;
-  if (info->query_only) {
-    info->blocks = full;
-    return;
-  }
-  int blocks = info->blocks > 0 ? info->blocks : full;
-  if (blocks > full) blocks = full;
-  if (blocks < 1) blocks = 1;
-  LevelLaunch la = L;
-  PersistPlan pa = *P;
-  void* args[] = {&la, &pa};
-  info->launch_error = (int)cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks),
-                                                        dim3(kTileTargets), args, smem, st);
-  info->blocks = blocks;
-}
-
-template <typename V, bool TRAIN>
-void dispatch_cells(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
-  const int lp1 = L.L + 1, kp1 = L.K + 1;
-  if (L.repl) return run_variant<V, 0, 0, TRAIN>(L, P, st, info);  // replication: generic cells
-  // small bitsets: target words in registers (32-bit values, the common case)
-  if constexpr (sizeof(V) == 4) {
-    if (lp1 == 1 && kp1 == 9) {
-      // exact words and cells: no predicates in the hot loop (C2: K=8, L=0)
-      if (L.AW == 2) return run_variant<V, 1, 9, TRAIN, 2, true>(L, P, st, info);
-      if (L.AW == 4) return run_variant<V, 1, 9, TRAIN, 4, true>(L, P, st, info);
-      if (L.AW == 6) return run_variant<V, 1, 9, TRAIN, 6, true>(L, P, st, info);
-      if (L.AW == 8) return run_variant<V, 1, 9, TRAIN, 8, true>(L, P, st, info);
-    }
-    if (lp1 == 3 && kp1 == 7) {  // C3: K=6, L=2
-      if (L.AW == 2) return run_variant<V, 3, 7, TRAIN, 2, true>(L, P, st, info);
-      if (L.AW == 4) return run_variant<V, 3, 7, TRAIN, 4, true>(L, P, st, info);
-    }
-    if (L.W <= 8) {
-      if (lp1 == 1 && kp1 <= 9) return run_variant<V, 1, 9, TRAIN, 8>(L, P, st, info);
-      if (lp1 == 1 && kp1 <= 17) return run_variant<V, 1, 17, TRAIN, 8>(L, P, st, info);
-      if (lp1 == 2 && kp1 <= 9) return run_variant<V, 2, 9, TRAIN, 8>(L, P, st, info);
-    }
-  }
-  if (lp1 == 1 && kp1 <= 9) return run_variant<V, 1, 9, TRAIN>(L, P, st, info);
-  if (lp1 == 1 && kp1 <= 17) return run_variant<V, 1, 17, TRAIN>(L, P, st, info);
-  if (lp1 == 2 && kp1 <= 9) return run_variant<V, 2, 9, TRAIN>(L, P, st, info);
-  if (lp1 == 3 && kp1 <= 9) return run_variant<V, 3, 9, TRAIN>(L, P, st, info);
-  if (lp1 == 5 && kp1 <= 9) return run_variant<V, 5, 9, TRAIN>(L, P, st, info);
-  return run_variant<V, 0, 0, TRAIN>(L, P, st, info);
-}
-
 void dispatch(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
   if (L.value_bits == 32) {
-    if (L.training) dispatch_cells<int32_t, true>(L, P, st, info);
-    else dispatch_cells<int32_t, false>(L, P, st, info);
+    if (L.training) {
+      if (!dispatch_exact_i32_train(L, P, st, info)) dispatch_general_i32_train(L, P, st, info);
+    } else {
+      if (!dispatch_exact_i32_inf(L, P, st, info)) dispatch_general_i32_inf(L, P, st, info);
+    }
   } else {
-    if (L.training) dispatch_cells<int64_t, true>(L, P, st, info);
-    else dispatch_cells<int64_t, false>(L, P, st, info);
+    if (L.training) dispatch_general_i64_train(L, P, st, info);
+    else dispatch_general_i64_inf(L, P, st, info);
   }
 }
 
 // ---- item list on the device
 struct PairInfo {
   int s, dep, bucket;
-  bool grouped;    // one item per 4 units (old mode-0 chunk)
   int64_t c, units_r, n_items;
 };
 
@@ -769,12 +51,11 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
   r.dep = s1 < 0 ? lo - 1 : p.level_of[s1 - 1];  // the cover chunk waits for level s-1
   const int64_t units = mode == 0 ? (T + kGroup - 1) / kGroup : T;
   r.units_r = b.world > 1 ? (units > b.rank ? (units - b.rank + b.world - 1) / b.world : 0) : units;
-  r.grouped = b.grouped && mode == 0 && r.dep < lo - b.group_slack;
   // scheduling bucket: a chunk for a far-future level waits in the list until
   // `lag` levels before its target, so each bucket holds a bounded amount of
   // near-term work and the critical items are not queued behind the future
   r.bucket = max(r.dep, lo - b.lag);
-  r.n_items = r.grouped ? (r.units_r + kWarps - 1) / kWarps : r.units_r;
+  r.n_items = r.units_r;
   return r;
 }
 
@@ -843,13 +124,8 @@ __global__ void item_fill_kernel(const PersistPlan p, const ItemBuild b) {
   const unsigned long long pos =
       atomicAdd(b.cnt + item_key(p, b, r), (unsigned long long)r.n_items);
   for (int64_t k = 0; k < r.n_items; ++k) {
-    if (r.grouped) {
-      // own-unit indices [4k, 4k+4): warp w takes 4k + w
-      b.items[pos + k] = make_int4(r.s, (int)(k * kWarps), (int)r.c | (1 << 30), r.dep);
-    } else {
-      const int64_t u = b.world > 1 ? b.rank + k * b.world : k;
-      b.items[pos + k] = make_int4(r.s, (int)u, (int)r.c, r.dep);
-    }
+    const int64_t u = b.world > 1 ? b.rank + k * b.world : k;
+    b.items[pos + k] = make_int4(r.s, (int)u, (int)r.c, r.dep);
   }
 }
 

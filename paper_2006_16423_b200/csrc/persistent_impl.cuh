@@ -1,0 +1,734 @@
+#pragma once
+// persistent_impl.cuh — every DP level in ONE cooperative launch, as a dataflow
+// wavefront (no grid barriers).
+//
+// The reference walks targets in ordinal order (MaxloadDp::run,
+// /root/reference/proj/src/dp_solver.cpp:319-330).  dp[I] depends only on
+// dp[I'] for I' ⊊ I, all in earlier levels, so:
+//
+//   * the work is a list of items (host plan, capi.cu) sorted by readiness;
+//     CTAs claim the next item from one atomic counter;
+//   * an item scans one chunk of source ordinals for a unit of targets of
+//     level s and first waits (spin on the per-level completion counter)
+//     only until the last level its chunk covers is finished — levels
+//     complete in order, and the chunks that cover old levels start long
+//     before level s-1 is done, so levels overlap;
+//   * every item merges its per-target cell minima (value-only: the argmin
+//     is recovered for the optimal path during traceback); the item that
+//     arrives last for a unit (atomic arrival counter) applies monotone_pass
+//     (dp_solver.cpp:180-193) in registers, writes the dp rows — into every
+//     rank's table when the solve is sharded over GPUs — and bumps the
+//     level's completion counter (release).
+//
+// Two item shapes:
+//   mode 0, lanes own targets (levels with >= 16 targets): item = (group of
+//     32 targets, chunk); each lane owns one target and the 4 warps take
+//     every 4th source of the chunk, so all lanes of a warp read the same
+//     source (broadcast loads, warp-uniform frontier loop).  The warps merge
+//     in shared memory; chunks merge with a value atomicMin.
+//   mode 1, lanes own sources (levels with few targets, e.g. the long chains
+//     of C4): item = (one target, chunk); the CTA's 128 threads each take
+//     sources i, i+128, ...; a warp-shuffle min + shared memory combine them
+//     into one partial per (target, chunk, cell).
+// All CTAs are co-resident (cooperative launch) and items only wait on
+// strictly earlier levels, so the spin waits cannot deadlock; a watchdog
+// aborts (flag) instead of hanging.
+#include <climits>
+#include <cstdint>
+#include <cstdlib>
+
+#include "scan.cuh"
+
+namespace dsg {
+
+namespace {
+
+using namespace scan;
+
+constexpr int kWarps = kTileTargets / 32;  // warps per CTA (4)
+constexpr int kGroup = 32;                 // targets per mode-0 item
+// The exact-word/exact-cell variants (the C2 hot loop) are held to 64
+// registers so 8 CTAs fit per SM (measured: 7.4 ms vs 8.0 ms at 80
+// registers on C2; the few spills sit off the source loop).  The other
+// variants keep their natural allocation (bounding them spills the hot loop).
+constexpr int kMinBlocksExact = 8;
+#ifndef DSG_MIN_BLOCKS_BIG
+#define DSG_MIN_BLOCKS_BIG 6
+#endif
+// more register cells (e.g. C3's 3x7): a softer cap
+constexpr int kMinBlocksExactBig = DSG_MIN_BLOCKS_BIG;
+constexpr uint64_t kWatchdogNs = 20000000000ull;
+
+template <typename V>
+__device__ __forceinline__ V warp_min(V v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = min(v, (V)__shfl_xor_sync(0xffffffffu, v, off));
+  return v;
+}
+
+__device__ __forceinline__ void atomic_min_v(int32_t* p, int32_t v) { atomicMin(p, v); }
+__device__ __forceinline__ void atomic_min_v(int64_t* p, int64_t v) {
+  atomicMin(reinterpret_cast<long long*>(p), (long long)v);
+}
+
+// Implicit mode-0 chunk boundaries.  An item's latency under full load
+// grows with its length, and an item whose last source is in level s-1-d
+// has d levels of slack before it gates level s.  So the recent levels are
+// chunked short, graded by that slack: level s-1-d (d = 1..grade) in chunks
+// of min(len0, len1 << (d-1)); everything older (levels <= s-2-grade) in
+// chunks of len0; the last chunk is the cover chunk (each target's lower
+// covers, all in level s-1): s0 = s1 = -1.
+__device__ __forceinline__ void mode0_chunk(const PersistPlan& p, int s, int64_t c, int64_t& s0,
+                                            int64_t& s1) {
+  const int G = min(p.grade, s - 1);
+  const int64_t Rg = p.level_off[s - 1 - G];
+  const int64_t n_old = (Rg + p.chunk_len0 - 1) / p.chunk_len0;
+  if (c < n_old) {
+    s0 = c * p.chunk_len0;
+    s1 = min(s0 + p.chunk_len0, Rg);
+    return;
+  }
+  c -= n_old;
+  for (int d = G; d >= 1; --d) {
+    const int64_t lo = p.level_off[s - 1 - d], hi = p.level_off[s - d];
+    const int64_t len = min((int64_t)p.chunk_len0, (int64_t)p.chunk_len1 << (d - 1));
+    const int64_t n = (hi - lo + len - 1) / len;
+    if (c < n) {
+      s0 = lo + c * len;
+      s1 = min(s0 + len, hi);
+      return;
+    }
+    c -= n;
+  }
+  s0 = s1 = -1;
+}
+
+// Mode 0 cover chunk: lane = target, warp w takes covers w, w+4, ... of it.
+// Per-lane trip counts differ, so no warp collectives in here.
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool CX>
+__device__ __forceinline__ unsigned scan_covers(const LevelLaunch& a, const Target<V>& x, int first,
+                                                int step, const uint64_t* tA, const uint64_t* tInt,
+                                                V* best, V* colv, const void* dpm) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr bool kGeneric = LP1 == 0;
+  constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
+  constexpr V NEG = (V)(-INF - 1);
+  if (!x.active) return 0;
+  const int C = CX ? CMAX : a.C;
+  const int64_t c0 = __ldg(a.cov_off + x.t), c1 = __ldg(a.cov_off + x.t + 1);
+  unsigned n = 0;
+  for (int64_t j = c0 + first; j < c1; j += step) {
+    const int64_t src = __ldg(a.cov + j);
+    ++n;
+    bool gated;
+    V acc, cpu, mem_blk;
+    const V* sdp = (const V*)dpm + (size_t)src * C;
+    V row[CMAX > 1 ? CMAX - 1 : 1];
+    if constexpr (!kGeneric) {
+#pragma unroll
+      for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? ld_row<false>(sdp + c) : INF;
+      auto need = [&](V proc) {
+        V thr = NEG;
+#pragma unroll
+        for (int c = LP1; c < CMAX; ++c)
+          if (c < C) thr = vmax(thr, row[c - LP1] < best[c] ? best[c] : NEG);
+        return proc < thr;
+      };
+      pair_cost<V, TRAIN, TS>(a, x, src, tA, tInt, gated, acc, cpu, mem_blk, need);
+    } else {
+      pair_cost<V, TRAIN, TS>(a, x, src, tA, tInt, gated, acc, cpu, mem_blk);
+    }
+    if (gated) continue;
+    k4_update<V, LP1, KP1MAX, TS, CX>(a, sdp, row, acc, cpu, mem_blk, best, colv);
+  }
+  return n;
+}
+
+// Release-add without an L1 invalidation (atom.release: MEMBAR.ALL + ATOM;
+// __threadfence() + atomicAdd would add CCTL.IVALL, which discards the L1
+// of every CTA on the SM).  ATOM, not RED: a counter others spin on should
+// reach L2 at once.
+__device__ __forceinline__ unsigned atom_release_add(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// This CTA's rank-local tables (shared memory, set once per kernel): the
+// launch's own (world == 1 or one process per GPU) or, for virtual shards,
+// those of rank blockIdx.x % world (PersistPlan::vrank).
+struct CtaView {
+  const int4* items;
+  int64_t total_items;
+  unsigned long long* next;
+  unsigned* tile_count;
+  void* keys;
+  const void* dp;  // the dp replica this CTA's sources are read from
+  unsigned* done;
+  int* stop;
+  int rank;
+};
+
+// Stop every rank (deadline, watchdog): a peer spinning on a level the
+// stopping rank will never finish must see it instead of its watchdog.
+__device__ __forceinline__ void raise_stop(const PersistPlan& p, const CtaView& v, bool err) {
+  for (int r = 0; r < p.world; ++r) {
+    int* ctl = reinterpret_cast<int*>(p.world > 1 ? p.peer_done[r] - 32 : v.done - 32);
+    if (err) atomicExch_system(ctl + 1, 1);
+    atomicExch_system(ctl, 1);
+  }
+}
+
+// Wait until level j is complete (then so are all levels below it: every
+// unit of level j consumes all of level j-1).  Returns false on stop/err.
+__device__ bool wait_level(const PersistPlan& p, const CtaView& v, int j, bool acquire = false) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    s_ok = 1;
+    const unsigned need = (unsigned)(p.level_off[j + 1] - p.level_off[j]);
+    if (ld_relaxed_sys(v.done + j) < need) {
+      // polite polling: back off up to ~1 us so the spinning warp does not
+      // steal issue slots from the co-resident CTAs doing the real work
+      unsigned ns = 32, polls = 0;
+      const uint64_t t0 = globaltimer();
+      while (ld_relaxed_sys(v.done + j) < need) {
+        __nanosleep(ns);
+        ns = ns < p.poll_ns_max ? ns * 2 : p.poll_ns_max;
+        if ((++polls & 63) != 0) continue;
+        if (ld_relaxed_sys((const unsigned*)v.stop) != 0) {
+          s_ok = 0;
+          break;
+        }
+        if (globaltimer() - t0 > kWatchdogNs) {
+          raise_stop(p, v, true);
+          s_ok = 0;
+          break;
+        }
+      }
+    }
+    // world == 1: no acquire fence — every later read of data produced in
+    // this kernel (dp rows, keys) goes to L2 (ld.global.cg / cp.async.cg)
+    // and is control-dependent on the counter value just observed, and the
+    // producers released (MEMBAR) before bumping it.  An acquire would
+    // invalidate the whole L1 of the SM (CCTL.IVALL) on every item.
+    // Mode-1 items (one source row per thread: the rows share L1 lines, so
+    // L1-cached loads are much cheaper than per-cell L2 loads) acquire
+    // instead, which invalidates the L1.
+    if (p.world > 1) __threadfence_system();  // peers' NVLink stores
+    else if (acquire) __threadfence();
+    asm volatile("" ::: "memory");
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// Wait until this GPU's counter *c reaches need (the finisher of a mode-1
+// target waits for the target's other chunks).  Returns false on stop/err.
+__device__ bool wait_count(const PersistPlan& p, const CtaView& v, const unsigned* c,
+                           unsigned need) {
+  __shared__ int s_ok2;
+  if (threadIdx.x == 0) {
+    s_ok2 = 1;
+    if (ld_relaxed(c) < need) {
+      unsigned ns = 32, polls = 0;
+      const uint64_t t0 = globaltimer();
+      while (ld_relaxed(c) < need) {
+        __nanosleep(ns);
+        ns = ns < p.poll_ns_max ? ns * 2 : p.poll_ns_max;
+        if ((++polls & 63) != 0) continue;
+        if (ld_relaxed_sys((const unsigned*)v.stop) != 0) {
+          s_ok2 = 0;
+          break;
+        }
+        if (globaltimer() - t0 > kWatchdogNs) {
+          raise_stop(p, v, true);
+          s_ok2 = 0;
+          break;
+        }
+      }
+    }
+    asm volatile("" ::: "memory");  // keys are read at L2 (see wait_level)
+  }
+  __syncthreads();
+  return s_ok2 != 0;
+}
+
+// Level s gained n finished targets: release their rows, bump the level
+// counter on every rank (system scope when peers read it over NVLink).
+__device__ __forceinline__ void release_done(const PersistPlan& p, int s, unsigned n) {
+  if (p.world == 1) {
+    atom_release_add(p.peer_done[0] + s, n);  // release the rows
+  } else {
+    __threadfence_system();  // rows reached every peer before its counter moves
+    for (int r = 0; r < p.world; ++r) atomicAdd_system(p.peer_done[r] + s, n);
+  }
+}
+
+// Mode 0, one warp: this chunk of `unit` has merged its minima into the
+// keys; count the arrival, and if it is the unit's last chunk apply
+// monotone_pass (dp_solver.cpp:180-193) to the merged cells, store the rows
+// into every rank's table and release them.  Returns whether it finalized.
+template <typename V, int LP1, int CMAX>
+__device__ bool arrive_finalize_unit(const LevelLaunch& a, const PersistPlan& p, const CtaView& v,
+                                     int s, int64_t unit, int64_t t_lo, int64_t T, int64_t chunks,
+                                     int lane, V* best, V* colv, const V* keys, int C) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr bool kGeneric = LP1 == 0;
+  constexpr int TS = kGroup;
+  unsigned last = 0;
+  __syncwarp();
+  if (lane == 0) {
+    // release this warp's merges; the last arriver reads the others' at L2
+    last = atom_release_add(v.tile_count + p.tile_base[s] + unit, 1u) == chunks - 1;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return false;
+  const int64_t n_act = min((int64_t)TS, T - unit * TS);
+  if (lane < n_act) {
+    const int64_t t = t_lo + unit * TS + lane;
+    const V* key = keys + (size_t)t * C;
+    if (!kGeneric) {
+#pragma unroll
+      for (int c = 0; c < CMAX; ++c)
+        if (c < C) best[c] = __ldcg(key + c);
+      monotone_regs<V, LP1, CMAX>(best, C);
+      for (int r = 0; r < p.world; ++r) {
+        V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c)
+          if (c < C) dpt[c] = best[c];
+      }
+    } else {
+      for (int c = 0; c < C; ++c) colv[c * TS] = __ldcg(key + c);
+      monotone_strided(colv, TS, a.K, a.L);
+      for (int r = 0; r < p.world; ++r) {
+        V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+        for (int c = 0; c < C; ++c) dpt[c] = colv[c * TS];
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) release_done(p, s, (unsigned)n_act);
+  return true;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+// Stage a mode-0 old chunk's sources [s0, s1) — bitset rows, records and
+// (16-byte aligned superset of the) dp rows, all contiguous in HBM — into
+// shared memory with 16-byte async copies from all 128 threads: the chunk's
+// loads are in flight at once instead of one dependent round trip per
+// source iteration.  Ends with the CTA barrier.
+template <typename V>
+__device__ __forceinline__ SrcView<V> stage_sources(const LevelLaunch& a, const void* dpm,
+                                                    int64_t s0, int64_t s1, int C,
+                                                    unsigned char* st) {
+  const int tid = threadIdx.x;
+  const int64_t n = s1 - s0;
+  const size_t nb = (size_t)n * a.AW * 8, nr = (size_t)n * sizeof(SrcRec);
+  const char* gb = reinterpret_cast<const char*>(a.abits + (size_t)s0 * a.AW);
+  const char* gr = reinterpret_cast<const char*>(a.srec + s0);
+  const size_t d0 = (size_t)s0 * C * sizeof(V), d1 = (size_t)s1 * C * sizeof(V);
+  const size_t da = d0 & ~(size_t)15, de = (d1 + 15) & ~(size_t)15;
+  const char* gd = reinterpret_cast<const char*>(dpm) + da;
+  unsigned char* sb = st;
+  unsigned char* sr = sb + nb;
+  unsigned char* sd = sr + nr;
+  for (size_t i = (size_t)tid * 16; i < nb; i += kTileTargets * 16) cp_async16(sb + i, gb + i);
+  for (size_t i = (size_t)tid * 16; i < nr; i += kTileTargets * 16) cp_async16(sr + i, gr + i);
+  for (size_t i = (size_t)tid * 16; i < de - da; i += kTileTargets * 16) cp_async16(sd + i, gd + i);
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  SrcView<V> v;
+  v.bits = reinterpret_cast<const uint64_t*>(sb);
+  v.rec = reinterpret_cast<const SrcRec*>(sr);
+  v.dp = reinterpret_cast<const V*>(sd + (d0 - da));
+  v.base = s0;
+  return v;
+}
+
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
+__device__ __forceinline__ void persistent_body(const LevelLaunch& a, const PersistPlan& p) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr bool kGeneric = LP1 == 0;
+  constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
+  constexpr int TS = kGroup;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_last, s_any_last;
+  const int W = a.W, C = CX ? CMAX : a.C;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // shared: target columns [AW][32] (padded, pad word 0) + interior
+  // [W][32] (mode 1 uses column 0), merge buffer [C][32], generic cells
+  // [4 warps][C][32]
+  uint64_t* s_tgt = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* s_int = s_tgt + (size_t)a.AW * TS;
+  V* m_val = reinterpret_cast<V*>(s_int + (TRAIN ? (size_t)W * TS : 0));
+  V* g_val = m_val + (size_t)C * TS;
+  V* colv = g_val + (size_t)warp * C * TS + lane;
+  // staging area for one old chunk's sources (16-byte aligned)
+  unsigned char* st_area = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(g_val + (kGeneric ? (size_t)kWarps * C * TS : 0)) + 15) &
+      ~(uintptr_t)15);
+  unsigned nested_total = 0;
+  // this CTA's rank-local tables (virtual shards: rank blockIdx.x % world)
+  __shared__ CtaView cv;
+  if (tid == 0) {
+    if (p.virt) {
+      const int r = (int)(blockIdx.x % (unsigned)p.world);
+      const VRank vr = p.vrank[r];
+      cv.items = vr.items;
+      cv.total_items = vr.total_items;
+      cv.next = reinterpret_cast<unsigned long long*>(vr.ctl + 2);
+      cv.tile_count = vr.tile_count;
+      cv.keys = vr.keys;
+      cv.dp = vr.dp;
+      cv.done = vr.ctl + 32;
+      cv.stop = reinterpret_cast<int*>(vr.ctl);
+      cv.rank = r;
+    } else {
+      cv.items = p.items;
+      cv.total_items = p.total_items;
+      cv.next = p.next;
+      cv.tile_count = p.tile_count;
+      cv.keys = p.keys;
+      cv.dp = a.dp;
+      cv.done = p.done;
+      cv.stop = p.stop;
+      cv.rank = p.rank;
+    }
+  }
+  __syncthreads();
+  // Roles: with crit_ctas > 0 the list starts with the cover items (they gate
+  // the levels) and the first crit_ctas CTAs claim only those, so a level's
+  // critical work never queues behind ready background work; the other CTAs
+  // claim the rest.  Every item still waits only for items listed before it
+  // in its own queue or for cover items, which the critical CTAs run in level
+  // order, so neither queue can deadlock.  (Virtual shards: one queue.)
+  const bool crit_role = (int)blockIdx.x < p.crit_ctas;
+  const int64_t n_crit = p.crit_ctas > 0 ? (int64_t)*p.crit_end : 0;
+  unsigned long long* ctr = crit_role ? p.crit_next : cv.next;
+  const int64_t q_lo = crit_role ? 0 : n_crit, q_hi = crit_role ? n_crit : cv.total_items;
+  __shared__ long long s_gi;
+  if (tid == 0) {
+    s_gi = q_lo + (long long)atomicAdd(ctr, 1ull);
+    s_any_last = 0;
+  }
+  __syncthreads();
+
+  while (true) {
+    const int64_t gi = s_gi;
+    if (gi >= q_hi) break;
+    const int4 item = __ldg(cv.items + gi);
+    // claim the next item now; its latency hides behind this one
+    unsigned long long next_gi = 0;
+    if (tid == 0) next_gi = q_lo + atomicAdd(ctr, 1ull);
+    const int s = item.x;
+    const int64_t unit = item.y;
+    const int64_t chunk = item.z;
+    const int64_t t_lo = p.level_off[s], t_hi = p.level_off[s + 1];
+    const int64_t T = t_hi - t_lo;
+    const int64_t chunks = p.n_chunks[s];
+    const int mode = p.mode[s];
+    int64_t s0, s1;
+    if (mode == 0) {
+      mode0_chunk(p, s, chunk, s0, s1);
+    } else if (chunk < chunks - 1) {
+      s0 = p.chunk_lo[p.chunk_base[s] + chunk];
+      s1 = p.chunk_lo[p.chunk_base[s] + chunk + 1];
+    } else {
+      s0 = s1 = -1;  // the cover chunk
+    }
+    const uint64_t tr0 = p.trace ? globaltimer() : 0;
+    uint64_t tr1 = 0;
+    if (blockIdx.x == 0 && tid == 0 && p.deadline_ns && globaltimer() > (uint64_t)p.deadline_ns)
+      raise_stop(p, cv, false);
+    V best[CMAX];
+    bool any_last = false;  // trace: some unit of this item finalized
+    if (mode == 0) {
+      // ------------------------------------ lanes own targets
+      // the four warps share one unit and split the chunk's sources
+      init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
+      const Target<V> x = load_target<V, TRAIN, TS>(a, t_lo, t_hi, unit, lane, s_tgt + lane,
+                                                    s_int + lane, warp == 0);
+      // start from the unit's merged minimum so far (other chunks' atomicMin
+      // merges): a valid upper bound that lets the scan prune early
+      if constexpr (!kGeneric) {
+        if (x.active) {
+          const V* key = reinterpret_cast<const V*>(cv.keys) + (size_t)x.t * C;
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c)
+            if (c < C) best[c] = __ldcg(key + c);
+        }
+      }
+      // sources [s0, s1) must be final; the target data and the key seeds
+      // above do not depend on them, so their latency hides behind the wait
+      if (!wait_level(p, cv, item.w)) break;
+      tr1 = p.trace ? globaltimer() : 0;
+      if (s0 < 0)
+        nested_total += scan_covers<V, LP1, KP1MAX, TRAIN, TS, CX>(a, x, warp, kWarps, s_tgt + lane,
+                                                                   s_int + lane, best, colv, cv.dp);
+      else if (p.stage)
+        nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX, 0, true>(
+            a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv,
+            stage_sources<V>(a, cv.dp, s0, s1, C, st_area));
+      else
+        nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
+            a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv, SrcView<V>{},
+            cv.dp);
+      // merge the 4 warps into warp 0 through the merge buffer
+      for (int src = 1; src < kWarps; ++src) {
+        __syncthreads();
+        if (warp == src) {
+          if (!kGeneric) {
+#pragma unroll
+            for (int c = 0; c < CMAX; ++c)
+              if (c < C) m_val[c * TS + lane] = best[c];
+          } else {
+            for (int c = 0; c < C; ++c) m_val[c * TS + lane] = colv[c * TS];
+          }
+        }
+        __syncthreads();
+        if (warp == 0) {
+          if (!kGeneric) {
+#pragma unroll
+            for (int c = 0; c < CMAX; ++c)
+              if (c < C) best[c] = min(best[c], m_val[c * TS + lane]);
+          } else {
+            for (int c = 0; c < C; ++c) colv[c * TS] = min(colv[c * TS], m_val[c * TS + lane]);
+          }
+        }
+      }
+      if (warp == 0) {
+        // chunks of a unit merge in L2 with a value atomicMin; the last
+        // arriving chunk finalizes the unit (this warp alone)
+        if (x.active) {
+          V* key = reinterpret_cast<V*>(cv.keys) + (size_t)x.t * C;
+          if (!kGeneric) {
+#pragma unroll
+            for (int c = 0; c < CMAX; ++c)
+              if (c < C && best[c] != INF) atomic_min_v(key + c, best[c]);
+          } else {
+            for (int c = 0; c < C; ++c)
+              if (colv[c * TS] != INF) atomic_min_v(key + c, colv[c * TS]);
+          }
+        }
+        any_last = arrive_finalize_unit<V, LP1, CMAX>(a, p, cv, s, unit, t_lo, T, chunks, lane,
+                                                      best, colv,
+                                                      reinterpret_cast<const V*>(cv.keys), C);
+      }
+      if (any_last) s_any_last = 1;
+    } else {
+      // ------------------------------------ lanes own sources
+      // Every mode-1 chunk has <= 128 sources (capi.cu), one per thread.
+      // The block costs (K2+K3) are static, so they run before the
+      // dependency wait; after it only the row loads and the min-max update
+      // remain.  The newest chunk (c = chunks-1, the one that gates the
+      // level) is the target's finisher: it waits for the other chunks'
+      // key merges, folds its own minima in and finalizes — no atomic merge
+      // or arrival round trip on the critical path.  The item list puts it
+      // after the target's other chunks, so its wait cannot deadlock.
+      init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
+      const int64_t t = t_lo + unit;
+      const bool fin = chunk == chunks - 1;
+      for (int w = tid; w < a.AW; w += kTileTargets) {
+        s_tgt[w] = __ldg(a.abits + (size_t)t * a.AW + w);
+        if (TRAIN && w < W) s_int[w] = __ldg(a.intbits + (size_t)t * W + w);
+      }
+      const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
+      V* key = reinterpret_cast<V*>(cv.keys) + (size_t)t * C;
+      __syncthreads();
+      // this thread's source: s0 + tid (old chunk) or the target's cover tid
+      int64_t my = s0 + tid;
+      bool has = my < s1;
+      if (fin) {
+        const int64_t c0 = __ldg(a.cov_off + t), c1 = __ldg(a.cov_off + t + 1);
+        has = c0 + tid < c1;
+        my = has ? (int64_t)__ldg(a.cov + c0 + tid) : 0;
+      }
+      PrePair<V> q{};
+      if (has) q = pre_pair<V, TRAIN, 1>(a, x, my, s_tgt, s_int);
+      // the finisher first waits for its target's other chunks (they depend
+      // on older levels and are usually done long before level s-1), and
+      // loads their merged minima (cell tid) before the level wait, so
+      // neither round trip sits on the level-to-level chain
+      if (fin && chunks > 1 &&
+          !wait_count(p, cv, cv.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1)))
+        break;
+      V kv = INF;
+      if (fin && tid < C) kv = __ldcg(key + tid);
+      if (!wait_level(p, cv, item.w, true)) break;  // acquire (ends with __syncthreads)
+      tr1 = p.trace ? globaltimer() : 0;
+      if (has) post_pair<V, LP1, KP1MAX, TS, CX>(a, q, my, best, colv, cv.dp);
+      nested_total += q.nested ? 1u : 0u;
+      if (fin) {
+        // targets with more than 128 lower covers (DAG width > 128)
+        const int64_t c0 = __ldg(a.cov_off + t), c1 = __ldg(a.cov_off + t + 1);
+        for (int64_t j = c0 + tid + kTileTargets; j < c1; j += kTileTargets) {
+          const int64_t src = __ldg(a.cov + j);
+          const PrePair<V> q2 = pre_pair<V, TRAIN, 1>(a, x, src, s_tgt, s_int);
+          post_pair<V, LP1, KP1MAX, TS, CX>(a, q2, src, best, colv, cv.dp);
+          nested_total += 1u;
+        }
+      }
+      // lanes -> warp (shuffle min) -> CTA (shared memory)
+      if (!kGeneric) {
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c) {
+          if (c < C) {
+            const V v = warp_min(best[c]);
+            if (lane == 0) m_val[c * TS + warp] = v;
+          }
+        }
+      } else {
+        for (int c = 0; c < C; ++c) {
+          const V v = warp_min(colv[c * TS]);
+          if (lane == 0) m_val[c * TS + warp] = v;
+        }
+      }
+      __syncthreads();
+      // threads over cells: merge into the keys (value atomicMin), or, for
+      // the finisher, fold in the merged keys
+      for (int c = tid; c < C; c += kTileTargets) {
+        V v = m_val[c * TS];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) v = min(v, m_val[c * TS + w]);
+        if (fin) m_val[c * TS] = min(v, c == tid ? kv : __ldcg(key + c));
+        else if (v != INF) atomic_min_v(key + c, v);
+      }
+      __syncthreads();
+      if (!fin) {
+        if (tid == 0) {
+          __threadfence();  // cumulative release of this CTA's merges
+          atomicAdd(cv.tile_count + p.tile_base[s] + unit, 1u);
+        }
+      } else if (tid == 0) {
+        if (!kGeneric) {
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c)
+            if (c < C) best[c] = m_val[c * TS];
+          monotone_regs<V, LP1, CMAX>(best, C);
+          for (int r = 0; r < p.world; ++r) {
+            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+#pragma unroll
+            for (int c = 0; c < CMAX; ++c)
+              if (c < C) dpt[c] = best[c];
+          }
+        } else {
+          monotone_strided(m_val, TS, a.K, a.L);
+          for (int r = 0; r < p.world; ++r) {
+            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
+            for (int c = 0; c < C; ++c) dpt[c] = m_val[c * TS];
+          }
+        }
+        release_done(p, s, 1u);
+        s_any_last = 1;
+      }
+    }
+    __syncthreads();
+    const uint64_t tr2 = p.trace ? globaltimer() : 0;
+    if (p.trace && tid == 0) {
+      uint64_t* tr = p.trace + gi * 4;
+      tr[0] = tr0;
+      tr[1] = tr1;
+      tr[2] = tr2;
+      tr[3] = globaltimer() | (s_any_last ? (1ull << 63) : 0ull);
+    }
+    if (tid == 0) s_any_last = 0;
+    if (tid == 0) s_gi = (long long)next_gi;
+    __syncthreads();
+  }
+  for (int off = 16; off > 0; off >>= 1)
+    nested_total += __shfl_xor_sync(0xffffffffu, nested_total, off);
+  if (lane == 0 && nested_total) atomicAdd(a.pair_counter, (unsigned long long)nested_total);
+}
+
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
+__global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const LevelLaunch a,
+                                                                         const PersistPlan p) {
+  persistent_body<V, LP1, KP1MAX, TRAIN, WT, CX>(a, p);
+}
+
+// exact variants: register budget for kMinBlocksExact resident CTAs per SM
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
+__global__ void __launch_bounds__(kTileTargets,
+                                  LP1 * KP1MAX <= 9 ? kMinBlocksExact : kMinBlocksExactBig)
+    persistent_levels_kernel_x(const LevelLaunch a, const PersistPlan p) {
+  persistent_body<V, LP1, KP1MAX, TRAIN, WT, CX>(a, p);
+}
+
+size_t persist_smem(const LevelLaunch& L, const PersistPlan* P, bool generic, size_t vsz) {
+  size_t s = kGroup * sizeof(uint64_t) * (L.AW + (L.training ? L.W : 0));  // targets
+  s += (size_t)L.C * kGroup * vsz;                                           // merge buffer
+  if (generic) s += (size_t)kWarps * L.C * kGroup * vsz;
+  if (P && P->stage) {
+    // one old chunk: bitset rows, records, dp rows (+ alignment slack)
+    const size_t n = (size_t)max(P->chunk_len0, P->chunk_len1);
+    s += 16 + n * L.AW * 8 + n * sizeof(SrcRec) + n * L.C * vsz + 32;
+  }
+  return s;
+}
+
+template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT = 0, bool CX = false>
+void run_variant(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, PersistInfo* info) {
+  const size_t smem = persist_smem(L, P, LP1 == 0, sizeof(V));
+  void (*kern)(const LevelLaunch, const PersistPlan);
+  if constexpr (CX) kern = persistent_levels_kernel_x<V, LP1, KP1MAX, TRAIN, WT, CX>;
+  else kern = persistent_levels_kernel<V, LP1, KP1MAX, TRAIN, WT, CX>;
+  // the attribute is per device context: set it on every call (cheap), and
+  // report 0 resident CTAs when the shared memory cannot fit at all (the
+  // host then falls back to the per-level driver)
+  int dev = 0, sms = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int per_sm = 0;
+  if (smem <= (size_t)optin &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+          cudaSuccess &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTileTargets, smem) !=
+          cudaSuccess)
+    per_sm = 0;
+  cudaGetLastError();  // a failed query must not poison the next launch check
+  const int full = per_sm * sms;
+  info->per_sm = per_sm;
+  if (info->query_only) {
+    info->blocks = full;
+    return;
+  }
+  if (full < 1) {
+    info->blocks = 0;
+    info->launch_error = (int)cudaErrorInvalidConfiguration;
+    return;
+  }
+  int blocks = info->blocks > 0 ? info->blocks : full;
+  if (blocks > full) blocks = full;
+  if (blocks < 1) blocks = 1;
+  LevelLaunch la = L;
+  PersistPlan pa = *P;
+  void* args[] = {&la, &pa};
+  info->launch_error = (int)cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks),
+                                                        dim3(kTileTargets), args, smem, st);
+  info->blocks = blocks;
+}
+
+}  // namespace
+
+// Kernel variants, compiled in separate translation units (persistent_v*.cu)
+// so nvcc builds them in parallel.  dispatch_exact_*: the int32 exact-word /
+// exact-cell and small-W register variants (false: none applies);
+// dispatch_general_*: register cells by (L+1, K+1) bound, else generic.
+#define DSG_PV_DECL(V, T)                                                                     \
+  bool dispatch_exact_##V##_##T(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st,  \
+                                PersistInfo* info);                                           \
+  void dispatch_general_##V##_##T(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, \
+                                  PersistInfo* info);
+DSG_PV_DECL(i32, inf)
+DSG_PV_DECL(i32, train)
+DSG_PV_DECL(i64, inf)
+DSG_PV_DECL(i64, train)
+#undef DSG_PV_DECL
+
+}  // namespace dsg

@@ -306,10 +306,14 @@ __device__ __forceinline__ bool pair_cost(const LevelLaunch& a, const Target<V>&
 }
 
 // replicated_load (dp_solver.cpp:100-108) for r >= 2 on exactly scaled values
+// Every value carries the factor S = lcm(1..K)·|b_num| (capi.cu prepare), so
+// mem_blk / |b_num| and then / rr are exact; dividing before multiplying keeps
+// every intermediate <= the final sync term, which the host's value-width
+// bound covers (multiplying by (rr-1)·b_den first can wrap the 32-bit path).
 template <typename V>
 __device__ __forceinline__ V replicated(const LevelLaunch& a, V acc, V mem_blk, int rr) {
   const V divided = acc / (V)rr;
-  const V sync = (V)a.repl_sign * ((mem_blk / (V)a.repl_bn) * (V)a.repl_bd * (V)(rr - 1) / (V)rr);
+  const V sync = (V)a.repl_sign * (((mem_blk / (V)a.repl_bn) / (V)rr) * (V)(rr - 1) * (V)a.repl_bd);
   return a.repl_combine == 0 ? (V)(divided + sync) : vmax(divided, sync);
 }
 
@@ -391,7 +395,8 @@ template <typename V, int LP1, int KP1MAX, bool TRAIN, int TS, bool UNIFORM, int
 __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Target<V>& x,
                                                  int64_t s0, int64_t s1, int step,
                                                  const uint64_t* tA, const uint64_t* tInt, V* best,
-                                                 V* colv, SrcView<V> sv = SrcView<V>{}) {
+                                                 V* colv, SrcView<V> sv = SrcView<V>{},
+                                                 const void* dpo = nullptr) {
   constexpr V INF = VTraits<V>::INF;
   constexpr bool kGeneric = LP1 == 0;
   constexpr int CMAX = kGeneric ? 1 : LP1 * KP1MAX;
@@ -399,7 +404,8 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
   const int W = (CX && WT > 0) ? WT : a.W;  // exact: W rounded up, pad word 0
   const int AWp = (CX && WT > 0) ? WT : a.AW;  // row pitch (a compile-time constant when exact)
   const int C = CX ? CMAX : a.C;
-  const V* dp = (const V*)a.dp;
+  // dpo: the dp replica this CTA reads (a virtual shard's own table)
+  const V* dp = (const V*)(dpo ? dpo : a.dp);
   unsigned nested_cnt = 0;
   // L == 0 (accelerator cells only): a pair can change a cell only through
   // max(dp[I'][k-1], acc) < best[k], and acc >= proc, so it is a candidate
@@ -538,12 +544,12 @@ __device__ __forceinline__ PrePair<V> pre_pair(const LevelLaunch& a, const Targe
 
 template <typename V, int LP1, int KP1MAX, int CS, bool CX>
 __device__ __forceinline__ void post_pair(const LevelLaunch& a, const PrePair<V>& q, int64_t s,
-                                          V* best, V* colv) {
+                                          V* best, V* colv, const void* dpo) {
   constexpr V INF = VTraits<V>::INF;
   constexpr int CMAX = LP1 == 0 ? 1 : LP1 * KP1MAX;
   if (!q.ok) return;
   const int C = CX ? CMAX : a.C;
-  const V* sdp = (const V*)a.dp + (size_t)s * C;
+  const V* sdp = (const V*)dpo + (size_t)s * C;
   V row[CMAX > 1 ? CMAX - 1 : 1];
   if constexpr (LP1 != 0) {
 #pragma unroll

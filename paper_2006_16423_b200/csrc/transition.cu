@@ -18,6 +18,7 @@
 // in ordinal order (dp_solver.cpp:205-230); traceback_decide then replays
 // monotone_pass's strict tests to tell a block from a waste move (kinds
 // 3/4) and steps to the predecessor.
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 
@@ -109,6 +110,15 @@ __global__ void fill_inf_kernel(V* p, int64_t n) {
 }
 
 __global__ void read_globaltimer_kernel(uint64_t* out) { *out = globaltimer(); }
+
+__global__ void compare_tables_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                      size_t n, int* bad) {
+  bool diff = false;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    diff |= a[i] != b[i];
+  if (__syncthreads_or(diff) && threadIdx.x == 0) atomicExch(bad, 1);
+}
 
 __global__ void fill_u32_kernel(unsigned* p, int64_t n, unsigned value) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -317,18 +327,17 @@ void launch_tile(const LevelLaunch& L, dim3 grid, cudaStream_t st) {
   size_t smem = (size_t)(L.AW + (TRAIN ? L.W : 0)) * kTileTargets * sizeof(uint64_t);
   if (LP1 == 0) smem += (size_t)L.C * kTileTargets * sizeof(V);
   auto kern = transition_kernel<V, LP1, KP1MAX, TRAIN>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
+  // per device context: set on every launch (a second device needs it too)
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, kTileTargets, smem, st>>>(L);
 }
 
 template <typename V, bool TRAIN>
 void dispatch_tile(const LevelLaunch& L, dim3 grid, cudaStream_t st) {
   const int lp1 = L.L + 1, kp1 = L.K + 1;
-  if (L.repl) return launch_tile<V, 0, 0, TRAIN>(L, grid, st);  // replication: generic cells
+  // replication and unprunable weights: generic cells (no pruning)
+  if (L.repl || L.no_prune) return launch_tile<V, 0, 0, TRAIN>(L, grid, st);
   if (lp1 == 1 && kp1 <= 9) return launch_tile<V, 1, 9, TRAIN>(L, grid, st);
   if (lp1 == 1 && kp1 <= 17) return launch_tile<V, 1, 17, TRAIN>(L, grid, st);
   if (lp1 == 2 && kp1 <= 9) return launch_tile<V, 2, 9, TRAIN>(L, grid, st);
@@ -405,6 +414,13 @@ void launch_level_of(const int64_t* level_off, int n_levels, int64_t I, int32_t*
 
 void launch_fill_u32(unsigned* p, int64_t n, unsigned value, cudaStream_t st) {
   fill_u32_kernel<<<1, 256, 0, st>>>(p, n, value);
+  count_launch();
+}
+
+void launch_compare_tables(const void* a, const void* b, size_t bytes, int* bad, cudaStream_t st) {
+  const size_t n = bytes / 4;  // tables are whole int32 / int64 rows
+  const unsigned blocks = (unsigned)std::min<size_t>(1024, (n + 255) / 256 + 1);
+  compare_tables_kernel<<<blocks, 256, 0, st>>>((const uint32_t*)a, (const uint32_t*)b, n, bad);
   count_launch();
 }
 

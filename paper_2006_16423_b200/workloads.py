@@ -274,15 +274,38 @@ SWEEP_POINTS = [
 ]
 
 
-def standin(name: str, seed: int = 1) -> Workload:
-    """The BASELINE.json config stand-ins C1..C4."""
+def standin(name: str, seed: int = 1, decimals: int = 1) -> Workload:
+    """The BASELINE.json config stand-ins C1..C4.  seed /
+    decimals select the weight draw (decimals=3: D = 1000 weights)."""
     spec = SPECS[name]
     c = CONFIGS[name]
-    g = module_chain(spec, seed=seed)
+    g = module_chain(spec, seed=seed, decimals=decimals)
     if c["training"]:
         g = mirror_training(g)
     cfg = DeviceConfig(accelerators=c["k"], cpus=c["l"], memory_limit=_mem_limit(g, c["k"]))
-    return Workload(name, g, cfg, c["training"], spec, c["desc"])
+    tag = name + (f"@seed{seed}" if seed != 1 else "") + (f"@D{10 ** decimals}" if decimals != 1 else "")
+    return Workload(tag, g, cfg, c["training"], spec, c["desc"])
+
+
+def by_name(name: str) -> Workload:
+    """Workload names used by bench.py and the tools: C1..C4, optionally
+    suffixed @seedN / @D1000 (weight draw), or C5:w,c,M,stem (sweep point)."""
+    if name.startswith("C5"):
+        pt = tuple(int(x) for x in name[3:].split(","))
+        return sweep(*pt)
+    base, *tags = name.split("@")
+    seed, decimals = 1, 1
+    for t in tags:
+        if t.startswith("seed"):
+            seed = int(t[4:])
+        elif t.startswith("D"):
+            d = int(t[1:])
+            decimals = len(str(d)) - 1
+            if 10 ** decimals != d:
+                raise ValueError(f"weight denominator must be a power of 10: {name}")
+        else:
+            raise ValueError(f"unknown workload tag {t!r} in {name!r}")
+    return standin(base, seed=seed, decimals=decimals)
 
 
 def sweep(width: int, chain: int, modules: int, stem: int, k: int = 8, l: int = 0,

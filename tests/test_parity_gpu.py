@@ -74,29 +74,6 @@ def test_driver_variants_match_golden(gpu, flags, max_blocks):
         assert got == rat_from_json(case["objective"]), case["name"]
 
 
-@pytest.mark.parametrize("max_blocks", [0, 2])
-def test_grouped_items_match_golden(gpu, monkeypatch, max_blocks):
-    """The experimental grouped items (DSG_GROUPING=1: one CTA item per four
-    32-target units over old chunks, one warp each) agree with the goldens."""
-    monkeypatch.setenv("DSG_GROUPING", "1")
-    monkeypatch.setenv("DSG_GROUP_SLACK", "2")
-    for case in CORPUS[::4]:
-        g = graph_from_json(case["graph"])
-        cfg = config_from_case(case)
-        f = solver.solve_maxload_training if case["mode"] == 1 else solver.solve_maxload_inference
-        try:
-            got = f(g, cfg, solver.SolveOptions(max_blocks=max_blocks)).objective_value
-        except InfeasibleError:
-            got = INF
-        assert got == rat_from_json(case["objective"]), case["name"]
-    w = wl.standin("C1")
-    base = device_solve(1, w.graph, w.config)
-    monkeypatch.delenv("DSG_GROUPING")
-    again = device_solve(1, w.graph, w.config)
-    assert base.objective_value == again.objective_value
-    assert base.stats["n_pairs"] == again.stats["n_pairs"]
-
-
 def test_standin_driver_variants_agree(gpu):
     w = wl.standin("C3")
     base = device_solve(1, w.graph, w.config)
@@ -316,3 +293,86 @@ def test_sharded_protocol_single_rank(gpu):
     except InfeasibleError:
         got = INF
     assert got == ob.objective_or_inf("port", 0, g, cfg)
+
+
+def test_replication_sync_term_no_overflow(gpu):
+    """the sync term (r-1)/r * mem / B formed (mem*(r-1)) before
+    dividing and wrapped the 32-bit path at K >= 8.  One node, cpu = acc = 1,
+    mem = 300, K = 16, bandwidth 1: the reference answer is 1."""
+    from fractions import Fraction
+    g = wl.Graph([wl.make_node(1, 1, 1, 0, 300)])
+    for k in (8, 12, 16):
+        cfg = DeviceConfig(k, 0, INF, bandwidth=Fraction(1))
+        want = ob.dp("port", 2, g, cfg).objective
+        assert want == 1
+        s = solver.solve_maxload_replicated(g, cfg)
+        assert s.objective_value == want, k
+    for seed in range(8):
+        gr, cfg = random_dag(7100 + seed, n_lo=4, n_hi=9)
+        cfg.accelerators = 9 + seed % 8
+        cfg.bandwidth = [Fraction(1), Fraction(3, 2), Fraction(1, 7)][seed % 3]
+        for nd in gr.nodes():
+            nd.mem_size = nd.mem_size * 50
+        gr = wl.Graph(gr.nodes(), gr.edges(), gr.artificial_edges())
+        cfg.memory_limit = INF
+        try:
+            got = solver.solve_maxload_replicated(gr, cfg).objective_value
+        except InfeasibleError:
+            got = INF
+        assert got == ob.objective_or_inf("port", 2, gr, cfg), seed
+
+
+def test_negative_comm_under_sum(gpu):
+    """the exact pruning assumes acc(B) >= proc(B); negative comm
+    weights under Interleaving::Sum break that, so those solves run unpruned
+    and still equal the oracle."""
+    from fractions import Fraction
+    for seed in range(12):
+        g, cfg = random_dag(7300 + seed, n_lo=5, n_hi=12)
+        for i, nd in enumerate(g.nodes()):
+            if nd.comm_time != INF and i % 2 == 0:
+                nd.comm_time = -nd.comm_time - Fraction(1, 2)
+        g = wl.Graph(g.nodes(), g.edges(), g.artificial_edges())
+        for mode in (Interleaving.Sum, Interleaving.HalfDuplexMax):
+            cfg.interleaving = mode
+            want = ob.objective_or_inf("port", 0, g, cfg)
+            try:
+                got = device_solve(0, g, cfg).objective_value
+            except InfeasibleError:
+                got = INF
+            assert got == want, (seed, mode)
+
+
+def test_large_cell_grid_falls_back(gpu):
+    """replicated K=16, L=8 (153 cells) with 64-bit values needs
+    more shared memory than a persistent CTA has; the solve must fall back to
+    the per-level driver instead of failing the launch."""
+    from fractions import Fraction
+    g, cfg = random_dag(7400, n_lo=6, n_hi=10)
+    cfg.accelerators, cfg.cpus = 16, 8
+    cfg.bandwidth = Fraction(3, 2)
+    want = ob.objective_or_inf("port", 2, g, cfg)
+    try:
+        got = solver.solve_maxload_replicated(
+            g, cfg, solver.SolveOptions(flags=_abi.DSG_FLAG_FORCE_INT64)).objective_value
+    except InfeasibleError:
+        got = INF
+    assert got == want
+
+
+HOST_REF = os.path.join(GOLDEN, "host_reference.json")
+
+
+@pytest.mark.skipif(not os.path.exists(HOST_REF), reason="host_reference.json not generated")
+def test_full_size_objectives_match_reference(gpu):
+    """Objectives of the unmodified reference on full workloads, solved on the
+    bench host (tools/cpu_ref_host.sh): the C5 top point (943.5M transitions),
+    the 3 %-dense sweep point (16,1,1,300), a second weight seed and D = 1000
+    weights for C2, and C1-C4."""
+    for row in json.load(open(HOST_REF)):
+        w = wl.by_name(row["workload"])
+        split = device_solve(1 if w.training else 0, w.graph, w.config)
+        assert str(split.objective_value) == row["objective"], row["workload"]
+        assert split.stats["n_ideals"] == row["ideals"]
+        assert split.stats["n_pairs"] == row["pairs_closed_form"]
+        assert not verify_split(w.graph, w.config, split, training=w.training)
