@@ -825,6 +825,11 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   LL.n_nodes = P.n;
   LL.cov_off = cov_off;
   LL.cov = cov;
+  {
+    int64_t* cmax = ctx.get_t<int64_t>(pfx + "d.cmax", 4 * (size_t)((I + kChunkMaxLen - 1) / kChunkMaxLen) + 4);
+    launch_chunk_max(D.srec, I, cmax, st);
+    LL.cmax = cmax;
+  }
   LL.dp = ctx.get(pfx + "dp.values", (size_t)I * C * vsz + 64);  // + staging slack
   LL.bp = nullptr;  // values only; the traceback re-derives the argmins
   LL.pair_counter = ctx.get_t<unsigned long long>(pfx + "dp.pairs", 1);
@@ -964,6 +969,9 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.stage = 1;
   if (const char* e = std::getenv("DSG_STAGE")) PP.stage = std::atoi(e) != 0;
   PP.chunk_len1 = (int)chunk_len1;
+  PP.dead_skip = 1;
+  if (const char* e = std::getenv("DSG_DEAD_SKIP")) PP.dead_skip = std::atoi(e) != 0;
+
   PP.grade = grade;
   PP.poll_ns_max = poll_ns_max;
   // work items in readiness order, built on the device (launch_build_items):

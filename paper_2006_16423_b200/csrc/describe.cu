@@ -22,6 +22,7 @@
 //
 // Pass 1 counts table sizes per ideal, a scan turns them into offsets,
 // pass 2 fills the pools.
+#include <climits>
 #include <cstdint>
 
 #include "dsg_device.cuh"
@@ -260,6 +261,42 @@ __global__ void __launch_bounds__(1024) scan_counts_kernel(int64_t* counts, int6
 }
 
 }  // namespace
+
+// Per aligned block of kChunkMaxLen source ordinals: the maxima of the
+// prefix sums acc / mem / cpu over the block.  With them an item can tell,
+// before touching a single source, that no source of its chunk can give any
+// of its targets a feasible, improving block (the per-pair tests of
+// scan_sources, taken over the block's extreme values) — such chunks only
+// count their nested pairs.
+__global__ void chunk_max_kernel(const SrcRec* __restrict__ srec, int64_t I, int64_t* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (c * kChunkMaxLen >= I) return;
+  long long ma = LLONG_MIN, mm = LLONG_MIN, mc = LLONG_MIN;
+  for (int64_t o = c * kChunkMaxLen + lane; o < min(I, (c + 1) * kChunkMaxLen); o += 32) {
+    ma = max(ma, (long long)srec[o].acc);
+    mm = max(mm, (long long)srec[o].mem);
+    mc = max(mc, (long long)srec[o].cpu);
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, off));
+    mm = max(mm, __shfl_xor_sync(0xffffffffu, mm, off));
+    mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, off));
+  }
+  if (lane == 0) {
+    out[4 * c] = ma;
+    out[4 * c + 1] = mm;
+    out[4 * c + 2] = mc;
+    out[4 * c + 3] = 0;
+  }
+}
+
+void launch_chunk_max(const SrcRec* srec, int64_t I, int64_t* out, cudaStream_t st) {
+  const int64_t n = (I + kChunkMaxLen - 1) / kChunkMaxLen;
+  if (n <= 0) return;
+  chunk_max_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(srec, I, out);
+  count_launch();
+}
 
 void launch_describe(const DescribeLaunch& L, bool fill, cudaStream_t st) {
   int threads = 128;

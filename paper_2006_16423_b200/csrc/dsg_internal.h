@@ -92,6 +92,10 @@ struct DescribeLaunch {
 };
 
 void launch_describe(const DescribeLaunch& L, bool fill, cudaStream_t st);
+// maxima of the source prefix sums (acc, mem, cpu, pad) per aligned block of
+// kChunkMaxLen ordinals: out[4 * block + {0, 1, 2}]
+constexpr int kChunkMaxLen = 64;
+void launch_chunk_max(const SrcRec* srec, int64_t I, int64_t* out, cudaStream_t st);
 void launch_scan_counts(int64_t* counts, int64_t I, int n_arrays, cudaStream_t st);
 
 // ------------------------------------------------------- transition
@@ -142,6 +146,8 @@ struct LevelLaunch {
   // lower covers of every ideal: ordinals one level down, CSR over ordinals
   const int64_t* cov_off;     // [I + 1]
   const int32_t* cov;
+  // [ceil(I / kChunkMaxLen)][4] maxima of the source prefix sums (launch_chunk_max)
+  const int64_t* cmax;
   // dp
   void* dp;                   // V[I][C]
   int32_t* bp;                // [I][C]
@@ -180,6 +186,7 @@ struct PersistPlan {
   int chunk_len0, chunk_len1;
   int grade;                 // recent levels chunked by slack (see mode0_chunk)
   int stage;                 // stage old mode-0 chunks in shared memory
+  int dead_skip;             // count-only scans of chunks that cannot change a cell
   unsigned poll_ns_max;      // dependency-wait backoff cap
   const int64_t* chunk_lo;
   const int64_t* chunk_base;

@@ -325,7 +325,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 template <typename V>
 __device__ __forceinline__ SrcView<V> stage_sources(const LevelLaunch& a, const void* dpm,
                                                     int64_t s0, int64_t s1, int C,
-                                                    unsigned char* st) {
+                                                    unsigned char* st, bool bits_only = false) {
   const int tid = threadIdx.x;
   const int64_t n = s1 - s0;
   const size_t nb = (size_t)n * a.AW * 8, nr = (size_t)n * sizeof(SrcRec);
@@ -338,8 +338,10 @@ __device__ __forceinline__ SrcView<V> stage_sources(const LevelLaunch& a, const 
   unsigned char* sr = sb + nb;
   unsigned char* sd = sr + nr;
   for (size_t i = (size_t)tid * 16; i < nb; i += kTileTargets * 16) cp_async16(sb + i, gb + i);
-  for (size_t i = (size_t)tid * 16; i < nr; i += kTileTargets * 16) cp_async16(sr + i, gr + i);
-  for (size_t i = (size_t)tid * 16; i < de - da; i += kTileTargets * 16) cp_async16(sd + i, gd + i);
+  if (!bits_only) {
+    for (size_t i = (size_t)tid * 16; i < nr; i += kTileTargets * 16) cp_async16(sr + i, gr + i);
+    for (size_t i = (size_t)tid * 16; i < de - da; i += kTileTargets * 16) cp_async16(sd + i, gd + i);
+  }
   asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
   __syncthreads();
   SrcView<V> v;
@@ -361,7 +363,7 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
   const int W = a.W, C = CX ? CMAX : a.C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // shared: target columns [AW][32] (padded, pad word 0) + interior
-  // [W][32] (mode 1 uses column 0), merge buffer [C][32], generic cells
+  // [W][32] (mode 1 uses column 0), merge column [C][32], generic cells
   // [4 warps][C][32]
   uint64_t* s_tgt = reinterpret_cast<uint64_t*>(smem);
   uint64_t* s_int = s_tgt + (size_t)a.AW * TS;
@@ -451,6 +453,11 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       // ------------------------------------ lanes own targets
       // the four warps share one unit and split the chunk's sources
       init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
+      if (!kGeneric && warp == 0) {  // the merge column (read back after the scan)
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c)
+          if (c < C) m_val[c * TS + lane] = INF;
+      }
       const Target<V> x = load_target<V, TRAIN, TS>(a, t_lo, t_hi, unit, lane, s_tgt + lane,
                                                     s_int + lane, warp == 0);
       // start from the unit's merged minimum so far (other chunks' atomicMin
@@ -463,32 +470,53 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
             if (c < C) best[c] = __ldcg(key + c);
         }
       }
+      // a chunk none of whose pairs can change a cell of any of the unit's
+      // targets (chunk_live over the block maxima) only counts its nested
+      // pairs; CTA-uniform (the warps' seeds may differ by a late merge)
+      bool dead = false;
+      if constexpr (!kGeneric) {
+        if (s0 >= 0 && p.dead_skip)
+          dead = !__syncthreads_or(chunk_live<V, LP1, CMAX>(a, x, best, s0, s1, C));
+      }
       // sources [s0, s1) must be final; the target data and the key seeds
       // above do not depend on them, so their latency hides behind the wait
       if (!wait_level(p, cv, item.w)) break;
       tr1 = p.trace ? globaltimer() : 0;
-      if (s0 < 0)
-        nested_total += scan_covers<V, LP1, KP1MAX, TRAIN, TS, CX>(a, x, warp, kWarps, s_tgt + lane,
-                                                                   s_int + lane, best, colv, cv.dp);
-      else if (p.stage)
-        nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX, 0, true>(
-            a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv,
-            stage_sources<V>(a, cv.dp, s0, s1, C, st_area));
-      else
-        nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
-            a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv, SrcView<V>{},
-            cv.dp);
-      // merge the 4 warps into warp 0 through the merge buffer
-      for (int src = 1; src < kWarps; ++src) {
-        __syncthreads();
-        if (warp == src) {
-          if (!kGeneric) {
+      if (dead) {
+        if (p.stage) {
+          const SrcView<V> sv = stage_sources<V>(a, cv.dp, s0, s1, C, st_area, true);
+          nested_total += count_nested<TS, WT, CX, true>(a, x.active, s0 + warp, s1, kWarps,
+                                                         s_tgt + lane, sv.bits, sv.base);
+        } else {
+          nested_total += count_nested<TS, WT, CX, false>(a, x.active, s0 + warp, s1, kWarps,
+                                                          s_tgt + lane, nullptr, 0);
+        }
+        // the cells are unchanged: no warp merge, no key merge, only the
+        // chunk's arrival
+        if (warp == 0)
+          any_last = arrive_finalize_unit<V, LP1, CMAX>(a, p, cv, s, unit, t_lo, T, chunks, lane,
+                                                        best, colv,
+                                                        reinterpret_cast<const V*>(cv.keys), C);
+      } else {
+        if (s0 < 0) {
+          nested_total += scan_covers<V, LP1, KP1MAX, TRAIN, TS, CX>(a, x, warp, kWarps, s_tgt + lane,
+                                                                     s_int + lane, best, colv, cv.dp);
+        } else if (p.stage) {
+          nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX, 0, true>(
+              a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv,
+              stage_sources<V>(a, cv.dp, s0, s1, C, st_area));
+        } else {
+          nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
+              a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv, SrcView<V>{},
+              cv.dp);
+        }
+        // merge the 4 warps into warp 0: one barrier (shared-memory atomicMin
+        // into the merge column warp 0 reset at the item's start; generic
+        // cells are already per-warp columns in shared memory)
+        if (!kGeneric && warp != 0) {
 #pragma unroll
-            for (int c = 0; c < CMAX; ++c)
-              if (c < C) m_val[c * TS + lane] = best[c];
-          } else {
-            for (int c = 0; c < C; ++c) m_val[c * TS + lane] = colv[c * TS];
-          }
+          for (int c = 0; c < CMAX; ++c)
+            if (c < C && best[c] != INF) atomic_min_v(m_val + c * TS + lane, best[c]);
         }
         __syncthreads();
         if (warp == 0) {
@@ -497,27 +525,27 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
             for (int c = 0; c < CMAX; ++c)
               if (c < C) best[c] = min(best[c], m_val[c * TS + lane]);
           } else {
-            for (int c = 0; c < C; ++c) colv[c * TS] = min(colv[c * TS], m_val[c * TS + lane]);
+            for (int w = 1; w < kWarps; ++w)
+              for (int c = 0; c < C; ++c)
+                colv[c * TS] = min(colv[c * TS], g_val[((size_t)w * C + c) * TS + lane]);
           }
-        }
-      }
-      if (warp == 0) {
-        // chunks of a unit merge in L2 with a value atomicMin; the last
-        // arriving chunk finalizes the unit (this warp alone)
-        if (x.active) {
-          V* key = reinterpret_cast<V*>(cv.keys) + (size_t)x.t * C;
-          if (!kGeneric) {
+          // chunks of a unit merge in L2 with a value atomicMin; the last
+          // arriving chunk finalizes the unit (this warp alone)
+          if (x.active) {
+            V* key = reinterpret_cast<V*>(cv.keys) + (size_t)x.t * C;
+            if (!kGeneric) {
 #pragma unroll
-            for (int c = 0; c < CMAX; ++c)
-              if (c < C && best[c] != INF) atomic_min_v(key + c, best[c]);
-          } else {
-            for (int c = 0; c < C; ++c)
-              if (colv[c * TS] != INF) atomic_min_v(key + c, colv[c * TS]);
+              for (int c = 0; c < CMAX; ++c)
+                if (c < C && best[c] != INF) atomic_min_v(key + c, best[c]);
+            } else {
+              for (int c = 0; c < C; ++c)
+                if (colv[c * TS] != INF) atomic_min_v(key + c, colv[c * TS]);
+            }
           }
+          any_last = arrive_finalize_unit<V, LP1, CMAX>(a, p, cv, s, unit, t_lo, T, chunks, lane,
+                                                        best, colv,
+                                                        reinterpret_cast<const V*>(cv.keys), C);
         }
-        any_last = arrive_finalize_unit<V, LP1, CMAX>(a, p, cv, s, unit, t_lo, T, chunks, lane,
-                                                      best, colv,
-                                                      reinterpret_cast<const V*>(cv.keys), C);
       }
       if (any_last) s_any_last = 1;
     } else {
@@ -527,9 +555,9 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       // dependency wait; after it only the row loads and the min-max update
       // remain.  The newest chunk (c = chunks-1, the one that gates the
       // level) is the target's finisher: it waits for the other chunks'
-      // key merges, folds its own minima in and finalizes — no atomic merge
-      // or arrival round trip on the critical path.  The item list puts it
-      // after the target's other chunks, so its wait cannot deadlock.
+      // key merges and finalizes — no atomic merge or arrival round trip on
+      // the critical path.  The item list puts it after the target's other
+      // chunks, so its wait cannot deadlock.
       init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
       const int64_t t = t_lo + unit;
       const bool fin = chunk == chunks - 1;
@@ -540,91 +568,123 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
       V* key = reinterpret_cast<V*>(cv.keys) + (size_t)t * C;
       __syncthreads();
-      // this thread's source: s0 + tid (old chunk) or the target's cover tid
-      int64_t my = s0 + tid;
-      bool has = my < s1;
       if (fin) {
+        // The finisher, threads over cells: thread j evaluates cover j's
+        // static block cost (before any wait), then, once level s-1 is
+        // final, thread c folds every cover's candidates for cell c into the
+        // other chunks' merged minimum (one L2 round trip for the rows), and
+        // monotone_pass (dp_solver.cpp:180-193: in place, k then l
+        // ascending) is the 2-D prefix minimum over the (k, l) grid, one
+        // thread per cell.
         const int64_t c0 = __ldg(a.cov_off + t), c1 = __ldg(a.cov_off + t + 1);
-        has = c0 + tid < c1;
-        my = has ? (int64_t)__ldg(a.cov + c0 + tid) : 0;
-      }
-      PrePair<V> q{};
-      if (has) q = pre_pair<V, TRAIN, 1>(a, x, my, s_tgt, s_int);
-      // the finisher first waits for its target's other chunks (they depend
-      // on older levels and are usually done long before level s-1), and
-      // loads their merged minima (cell tid) before the level wait, so
-      // neither round trip sits on the level-to-level chain
-      if (fin && chunks > 1 &&
-          !wait_count(p, cv, cv.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1)))
-        break;
-      V kv = INF;
-      if (fin && tid < C) kv = __ldcg(key + tid);
-      if (!wait_level(p, cv, item.w, true)) break;  // acquire (ends with __syncthreads)
-      tr1 = p.trace ? globaltimer() : 0;
-      if (has) post_pair<V, LP1, KP1MAX, TS, CX>(a, q, my, best, colv, cv.dp);
-      nested_total += q.nested ? 1u : 0u;
-      if (fin) {
-        // targets with more than 128 lower covers (DAG width > 128)
-        const int64_t c0 = __ldg(a.cov_off + t), c1 = __ldg(a.cov_off + t + 1);
-        for (int64_t j = c0 + tid + kTileTargets; j < c1; j += kTileTargets) {
-          const int64_t src = __ldg(a.cov + j);
-          const PrePair<V> q2 = pre_pair<V, TRAIN, 1>(a, x, src, s_tgt, s_int);
-          post_pair<V, LP1, KP1MAX, TS, CX>(a, q2, src, best, colv, cv.dp);
-          nested_total += 1u;
+        __shared__ int32_t f_src[kTileTargets];
+        __shared__ V f_acc[kTileTargets], f_cpu[kTileTargets], f_mem[kTileTargets];
+        const int lp1 = a.L + 1;
+        const V* dpm = reinterpret_cast<const V*>(cv.dp);
+        bool ok = true;
+        for (int64_t b0 = c0; b0 < c1 || b0 == c0; b0 += kTileTargets) {
+          const int nb = (int)min((int64_t)kTileTargets, c1 - b0);
+          if (tid < nb) {
+            const int64_t src = __ldg(a.cov + b0 + tid);
+            const PrePair<V> q = pre_pair<V, TRAIN, 1>(a, x, src, s_tgt, s_int);
+            f_src[tid] = q.ok ? (int32_t)src : -1;
+            f_acc[tid] = q.acc;
+            f_cpu[tid] = q.cpu;
+            f_mem[tid] = q.mem_blk;
+            ++nested_total;  // every lower cover is a nested pair
+          }
+          if (b0 == c0) {
+            // the other chunks' merges, then the level wait (both barriers)
+            if (chunks > 1 &&
+                !wait_count(p, cv, cv.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1))) {
+              ok = false;
+              break;
+            }
+            if (tid < C) m_val[tid] = __ldcg(key + tid);
+            for (int c = tid + kTileTargets; c < C; c += kTileTargets) m_val[c] = __ldcg(key + c);
+            if (!wait_level(p, cv, item.w)) {
+              ok = false;
+              break;
+            }
+            tr1 = p.trace ? globaltimer() : 0;
+          } else {
+            __syncthreads();
+          }
+          for (int c = tid; c < C; c += kTileTargets) {
+            const int k = c / lp1, l = c % lp1;
+            V v = m_val[c];
+            for (int j = 0; j < nb; ++j) {
+              const int32_t src = f_src[j];
+              if (src < 0) continue;
+              const V* row = dpm + (size_t)src * C;
+              const V acc = f_acc[j];
+              if (k >= 1 && acc != INF) {
+                if (kGeneric && a.repl) {
+                  for (int rr = 1; rr <= k; ++rr) {
+                    const V load = rr == 1 ? acc : replicated<V>(a, acc, f_mem[j], rr);
+                    v = min(v, vmax(__ldcg(row + c - rr * lp1), load));
+                  }
+                } else {
+                  v = min(v, vmax(__ldcg(row + c - lp1), acc));
+                }
+              }
+              if (l >= 1) v = min(v, vmax(__ldcg(row + c - 1), f_cpu[j]));
+            }
+            m_val[c] = v;
+          }
+          __syncthreads();
+          if (b0 + kTileTargets >= c1) break;
         }
-      }
-      // lanes -> warp (shuffle min) -> CTA (shared memory)
-      if (!kGeneric) {
+        if (!ok) break;
+        for (int c = tid; c < C; c += kTileTargets) {
+          const int k = c / lp1, l = c % lp1;
+          V v = m_val[c];
+          for (int kk = 0; kk <= k; ++kk)
+            for (int ll = 0; ll <= l; ++ll) v = min(v, m_val[kk * lp1 + ll]);
+          for (int r = 0; r < p.world; ++r) ((V*)p.peer_dp[r])[(size_t)t * C + c] = v;
+        }
+        __syncthreads();  // every cell stored before the (cumulative) release
+        if (tid == 0) {
+          release_done(p, s, 1u);
+          s_any_last = 1;
+        }
+      } else {
+        // an old chunk: thread tid takes source s0 + tid
+        const int64_t my = s0 + tid;
+        const bool has = my < s1;
+        PrePair<V> q{};
+        if (has) q = pre_pair<V, TRAIN, 1>(a, x, my, s_tgt, s_int);
+        if (!wait_level(p, cv, item.w, true)) break;  // acquire (ends with __syncthreads)
+        tr1 = p.trace ? globaltimer() : 0;
+        if (has) post_pair<V, LP1, KP1MAX, TS, CX>(a, q, my, best, colv, cv.dp);
+        nested_total += q.nested ? 1u : 0u;
+        // lanes -> warp (shuffle min) -> CTA (shared memory) -> keys
+        if (!kGeneric) {
 #pragma unroll
-        for (int c = 0; c < CMAX; ++c) {
-          if (c < C) {
-            const V v = warp_min(best[c]);
+          for (int c = 0; c < CMAX; ++c) {
+            if (c < C) {
+              const V v = warp_min(best[c]);
+              if (lane == 0) m_val[c * TS + warp] = v;
+            }
+          }
+        } else {
+          for (int c = 0; c < C; ++c) {
+            const V v = warp_min(colv[c * TS]);
             if (lane == 0) m_val[c * TS + warp] = v;
           }
         }
-      } else {
-        for (int c = 0; c < C; ++c) {
-          const V v = warp_min(colv[c * TS]);
-          if (lane == 0) m_val[c * TS + warp] = v;
-        }
-      }
-      __syncthreads();
-      // threads over cells: merge into the keys (value atomicMin), or, for
-      // the finisher, fold in the merged keys
-      for (int c = tid; c < C; c += kTileTargets) {
-        V v = m_val[c * TS];
+        __syncthreads();
+        for (int c = tid; c < C; c += kTileTargets) {
+          V v = m_val[c * TS];
 #pragma unroll
-        for (int w = 1; w < kWarps; ++w) v = min(v, m_val[c * TS + w]);
-        if (fin) m_val[c * TS] = min(v, c == tid ? kv : __ldcg(key + c));
-        else if (v != INF) atomic_min_v(key + c, v);
-      }
-      __syncthreads();
-      if (!fin) {
+          for (int w = 1; w < kWarps; ++w) v = min(v, m_val[c * TS + w]);
+          if (v != INF) atomic_min_v(key + c, v);
+        }
+        __syncthreads();
         if (tid == 0) {
           __threadfence();  // cumulative release of this CTA's merges
           atomicAdd(cv.tile_count + p.tile_base[s] + unit, 1u);
         }
-      } else if (tid == 0) {
-        if (!kGeneric) {
-#pragma unroll
-          for (int c = 0; c < CMAX; ++c)
-            if (c < C) best[c] = m_val[c * TS];
-          monotone_regs<V, LP1, CMAX>(best, C);
-          for (int r = 0; r < p.world; ++r) {
-            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
-#pragma unroll
-            for (int c = 0; c < CMAX; ++c)
-              if (c < C) dpt[c] = best[c];
-          }
-        } else {
-          monotone_strided(m_val, TS, a.K, a.L);
-          for (int r = 0; r < p.world; ++r) {
-            V* dpt = (V*)p.peer_dp[r] + (size_t)t * C;
-            for (int c = 0; c < C; ++c) dpt[c] = m_val[c * TS];
-          }
-        }
-        release_done(p, s, 1u);
-        s_any_last = 1;
       }
     }
     __syncthreads();
@@ -661,7 +721,7 @@ __global__ void __launch_bounds__(kTileTargets,
 
 size_t persist_smem(const LevelLaunch& L, const PersistPlan* P, bool generic, size_t vsz) {
   size_t s = kGroup * sizeof(uint64_t) * (L.AW + (L.training ? L.W : 0));  // targets
-  s += (size_t)L.C * kGroup * vsz;                                           // merge buffer
+  s += (size_t)L.C * kGroup * vsz;                                          // merge column
   if (generic) s += (size_t)kWarps * L.C * kGroup * vsz;
   if (P && P->stage) {
     // one old chunk: bitset rows, records, dp rows (+ alignment slack)

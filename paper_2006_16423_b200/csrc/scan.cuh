@@ -507,6 +507,78 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
   return nested_cnt;
 }
 
+// Chunk-level liveness of one lane's target against the sources [s0, s1):
+// with the block maxima of the source prefix sums (describe.cu
+// chunk_max_kernel), the smallest block any source of the chunk can give is
+// proc >= x.acc - max acc, mem >= x.mem - max mem, cpu >= x.cpu - max cpu.
+// If even those cannot pass the per-pair tests of scan_sources — memory over
+// the limit or proc above every accelerator cell's running minimum, and cpu
+// above every CPU cell's — no pair of the chunk can change a cell of this
+// target (acc(B) >= proc(B), as for the per-pair pruning).
+template <typename V, int LP1, int CMAX>
+__device__ __forceinline__ bool chunk_live(const LevelLaunch& a, const Target<V>& x, const V* best,
+                                           int64_t s0, int64_t s1, int C) {
+  constexpr V INF = VTraits<V>::INF;
+  constexpr V NEG = (V)(-INF - 1);
+  if (!x.active) return false;
+  int64_t ma = LLONG_MIN, mm = LLONG_MIN, mc = LLONG_MIN;
+  for (int64_t b = s0 / kChunkMaxLen; b <= (s1 - 1) / kChunkMaxLen; ++b) {
+    const longlong2 m0 = __ldg(reinterpret_cast<const longlong2*>(a.cmax) + 2 * b);
+    const long long m2 = __ldg(reinterpret_cast<const long long*>(a.cmax) + 4 * b + 2);
+    ma = max(ma, (int64_t)m0.x);
+    mm = max(mm, (int64_t)m0.y);
+    mc = max(mc, (int64_t)m2);
+  }
+  V mb_acc = NEG, mb_cpu = NEG;
+#pragma unroll
+  for (int c = 0; c < CMAX; ++c) {
+    if (c < C) {
+      if (c >= LP1) mb_acc = vmax(mb_acc, best[c]);
+      if (LP1 > 1 && (c % LP1) != 0) mb_cpu = vmax(mb_cpu, best[c]);
+    }
+  }
+  bool acc_live = a.K > 0 && (V)(x.acc - (V)ma) < mb_acc;
+  if (a.memcheck) acc_live = acc_live && !((V)(x.mem - (V)mm) > (V)a.mlim);
+  const bool cpu_live = LP1 > 1 && (V)(x.cpu - (V)mc) < mb_cpu;
+  return acc_live || cpu_live;
+}
+
+// Count-only scan for a chunk no pair of which can change a cell: the K2
+// subset test alone (the pairs still count as transitions, dp_solver.cpp:
+// 256-317 visits them).  Target words in registers when W is exact.
+template <int TS, int WT, bool CX, bool STAGED>
+__device__ __forceinline__ unsigned count_nested(const LevelLaunch& a, bool active, int64_t s0,
+                                                 int64_t s1, int step, const uint64_t* tA,
+                                                 const uint64_t* sbits, int64_t sbase) {
+  unsigned n = 0;
+  if (!active) return 0;
+  if constexpr (CX && WT > 0) {
+    uint64_t tw[WT];
+#pragma unroll
+    for (int j = 0; j < WT; ++j) tw[j] = tA[j * TS];
+    for (int64_t s = s0; s < s1; s += step) {
+      const ulonglong2* sA2 = reinterpret_cast<const ulonglong2*>(
+          STAGED ? sbits + (size_t)(s - sbase) * WT : a.abits + (size_t)s * WT);
+      uint64_t stray = 0;
+#pragma unroll
+      for (int j = 0; j < WT / 2; ++j) {
+        const ulonglong2 v = STAGED ? sA2[j] : __ldg(sA2 + j);
+        stray |= (v.x & ~tw[2 * j]) | (v.y & ~tw[2 * j + 1]);
+      }
+      n += stray == 0ull ? 1u : 0u;
+    }
+  } else {
+    const int W = a.W, AW = a.AW;
+    for (int64_t s = s0; s < s1; s += step) {
+      const uint64_t* sA = STAGED ? sbits + (size_t)(s - sbase) * AW : a.abits + (size_t)s * AW;
+      uint64_t stray = 0;
+      for (int w = 0; w < W; ++w) stray |= (STAGED ? sA[w] : __ldg(sA + w)) & ~tA[w * TS];
+      n += stray == 0ull ? 1u : 0u;
+    }
+  }
+  return n;
+}
+
 // Split K2+K3 / K4 for items whose sources may not be final yet (mode 1,
 // one source per thread): everything but the source's dp row is static, so
 // the subset test and the block cost run BEFORE the dependency wait and only
@@ -542,7 +614,7 @@ __device__ __forceinline__ PrePair<V> pre_pair(const LevelLaunch& a, const Targe
   return q;
 }
 
-template <typename V, int LP1, int KP1MAX, int CS, bool CX>
+template <typename V, int LP1, int KP1MAX, int CS, bool CX, bool L1 = true>
 __device__ __forceinline__ void post_pair(const LevelLaunch& a, const PrePair<V>& q, int64_t s,
                                           V* best, V* colv, const void* dpo) {
   constexpr V INF = VTraits<V>::INF;
@@ -553,10 +625,11 @@ __device__ __forceinline__ void post_pair(const LevelLaunch& a, const PrePair<V>
   V row[CMAX > 1 ? CMAX - 1 : 1];
   if constexpr (LP1 != 0) {
 #pragma unroll
-    for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? sdp[c] : INF;
+    for (int c = 0; c + 1 < CMAX; ++c) row[c] = (c + 1 < C) ? ld_row<L1>(sdp + c) : INF;
   }
-  // plain (L1) loads: the caller's dependency wait acquired (L1 invalidated)
-  k4_update<V, LP1, KP1MAX, CS, CX, true>(a, sdp, row, q.acc, q.cpu, q.mem_blk, best, colv);
+  // L1: plain loads, the caller's dependency wait acquired (L1 invalidated);
+  // else L2 loads (ld.global.cg) after a wait without an acquire
+  k4_update<V, LP1, KP1MAX, CS, CX, L1>(a, sdp, row, q.acc, q.cpu, q.mem_blk, best, colv);
 }
 
 template <typename V, int LP1, int KP1MAX, int CS>

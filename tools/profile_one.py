@@ -5,7 +5,7 @@ from paper_2006_16423_b200 import solver, _abi, workloads as wl
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 flags = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-w = wl.standin(name) if not name.startswith("C5") else wl.sweep(*map(int, name[3:].split(",")))
+w = wl.by_name(name)
 s = solver.Session(1 if w.training else 0, w.graph, w.config, solver.SolveOptions(flags=flags))
 for _ in range(reps):
     r = s.run()
