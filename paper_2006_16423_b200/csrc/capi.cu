@@ -881,6 +881,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   int64_t chunk_len0 = 64, chunk_len1 = 64;
   int grade = 1;
   if (const char* e = std::getenv("DSG_GRADE")) grade = std::max(1, std::atoi(e));
+  int grade1 = 3;  // mode 1: recent old levels chunked per level
+  if (const char* e = std::getenv("DSG_GRADE1")) grade1 = std::max(0, std::atoi(e));
   unsigned poll_ns_max = 128;  // measured: 128 ns <= 256 ns (C1 -4 %, C3 -1 %, C4 -1 %, C2 =) and beats 1 us
   if (const char* e = std::getenv("DSG_CHUNK_LEN")) chunk_len0 = std::max(4, std::atoi(e));
   if (const char* e = std::getenv("DSG_CHUNK_LEN1")) chunk_len1 = std::max(4, std::atoi(e));
@@ -917,13 +919,27 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       chunk_base[s] = -1;
       pl.chunk_len[s] = chunk_len0;
     } else if (pl.persistent) {
+      // mode 1: sources below level s-1-G1 in cost-balanced chunks of <= 128
+      // (one per thread); each of the G1 most recent old levels s-1-G1 ..
+      // s-2 in chunks of its own, so the item that waits for level s-2 (on
+      // the level-to-level chain of a narrow lattice) holds only that
+      // level's few sources; then the cover chunk (the finisher)
+      const int G1 = std::max(0, std::min(grade1, s - 2));
       const int64_t R = s >= 2 ? lat.level_off[s - 1] : 0;
-      int64_t oc = (R + kTileTargets - 1) / kTileTargets;
-      const int64_t olen = oc ? (R + oc - 1) / oc : 1;
+      const int64_t Rg = s >= 2 ? lat.level_off[s - 1 - G1] : 0;
       chunk_base[s] = (int64_t)chunk_lo.size();
-      for (int64_t c = 0; c < oc; ++c) chunk_lo.push_back(std::min(R, c * olen));
+      const int64_t oc = (Rg + kTileTargets - 1) / kTileTargets;
+      const int64_t olen = oc ? (Rg + oc - 1) / oc : 1;
+      for (int64_t c = 0; c < oc; ++c) chunk_lo.push_back(std::min(Rg, c * olen));
+      chunks = oc;
+      for (int j = s - 1 - G1; j <= s - 2 && G1 > 0; ++j) {
+        const int64_t lo = lat.level_off[j], n = lat.level_off[j + 1] - lo;
+        const int64_t nc = (n + kTileTargets - 1) / kTileTargets, len = (n + nc - 1) / nc;
+        for (int64_t c = 0; c < nc; ++c) chunk_lo.push_back(lo + c * len);
+        chunks += nc;
+      }
       chunk_lo.push_back(R);
-      chunks = oc + 1;
+      chunks += 1;
       pl.chunk_len[s] = 0;
     } else {
       chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, S / min_chunk));

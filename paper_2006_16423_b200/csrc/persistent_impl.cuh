@@ -51,13 +51,20 @@ constexpr int kGroup = 32;                 // targets per mode-0 item
 // registers so 8 CTAs fit per SM (measured: 7.4 ms vs 8.0 ms at 80
 // registers on C2; the few spills sit off the source loop).  The other
 // variants keep their natural allocation (bounding them spills the hot loop).
-constexpr int kMinBlocksExact = 8;
+#ifndef DSG_MIN_BLOCKS_EXACT
+#define DSG_MIN_BLOCKS_EXACT 7  // measured: 7 (72 registers) < 8 (64) on C2 since r2
+#endif
+constexpr int kMinBlocksExact = DSG_MIN_BLOCKS_EXACT;
 #ifndef DSG_MIN_BLOCKS_BIG
 #define DSG_MIN_BLOCKS_BIG 6
 #endif
 // more register cells (e.g. C3's 3x7): a softer cap
 constexpr int kMinBlocksExactBig = DSG_MIN_BLOCKS_BIG;
 constexpr uint64_t kWatchdogNs = 20000000000ull;
+// mode-1 old chunks of more sources take the one-source-per-thread path
+// (row loads spread over all threads); fewer, and the finisher, fold with
+// threads over (cell, source group)
+constexpr int kCellwiseMax = 16;
 
 template <typename V>
 __device__ __forceinline__ V warp_min(V v) {
@@ -371,9 +378,11 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
   V* g_val = m_val + (size_t)C * TS;
   V* colv = g_val + (size_t)warp * C * TS + lane;
   // staging area for one old chunk's sources (16-byte aligned)
-  unsigned char* st_area = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(g_val + (kGeneric ? (size_t)kWarps * C * TS : 0)) + 15) &
-      ~(uintptr_t)15);
+  // (offset arithmetic on the shared array itself: a round trip through an
+  // integer would turn every staged load into a generic LD instead of LDS)
+  unsigned char* st_area =
+      smem + ((reinterpret_cast<unsigned char*>(g_val + (kGeneric ? (size_t)kWarps * C * TS : 0)) -
+               smem + 15) & ~(ptrdiff_t)15);
   unsigned nested_total = 0;
   // this CTA's rank-local tables (virtual shards: rank blockIdx.x % world)
   __shared__ CtaView cv;
@@ -550,15 +559,12 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       if (any_last) s_any_last = 1;
     } else {
       // ------------------------------------ lanes own sources
-      // Every mode-1 chunk has <= 128 sources (capi.cu), one per thread.
-      // The block costs (K2+K3) are static, so they run before the
-      // dependency wait; after it only the row loads and the min-max update
-      // remain.  The newest chunk (c = chunks-1, the one that gates the
-      // level) is the target's finisher: it waits for the other chunks'
-      // key merges and finalizes — no atomic merge or arrival round trip on
-      // the critical path.  The item list puts it after the target's other
-      // chunks, so its wait cannot deadlock.
-      init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
+      // Every mode-1 chunk has <= 128 sources (capi.cu).  The newest chunk
+      // (c = chunks-1, the one that gates the level) is the target's
+      // finisher: it waits for the other chunks' key merges and finalizes —
+      // no atomic merge or arrival round trip on the critical path.  The
+      // item list puts it after the target's other chunks, so its wait
+      // cannot deadlock.
       const int64_t t = t_lo + unit;
       const bool fin = chunk == chunks - 1;
       for (int w = tid; w < a.AW; w += kTileTargets) {
@@ -568,88 +574,17 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       const Target<V> x = target_scalars<V, TRAIN>(a, t, unit, true);
       V* key = reinterpret_cast<V*>(cv.keys) + (size_t)t * C;
       __syncthreads();
-      if (fin) {
-        // The finisher, threads over cells: thread j evaluates cover j's
-        // static block cost (before any wait), then, once level s-1 is
-        // final, thread c folds every cover's candidates for cell c into the
-        // other chunks' merged minimum (one L2 round trip for the rows), and
-        // monotone_pass (dp_solver.cpp:180-193: in place, k then l
-        // ascending) is the 2-D prefix minimum over the (k, l) grid, one
-        // thread per cell.
-        const int64_t c0 = __ldg(a.cov_off + t), c1 = __ldg(a.cov_off + t + 1);
-        __shared__ int32_t f_src[kTileTargets];
-        __shared__ V f_acc[kTileTargets], f_cpu[kTileTargets], f_mem[kTileTargets];
-        const int lp1 = a.L + 1;
-        const V* dpm = reinterpret_cast<const V*>(cv.dp);
-        bool ok = true;
-        for (int64_t b0 = c0; b0 < c1 || b0 == c0; b0 += kTileTargets) {
-          const int nb = (int)min((int64_t)kTileTargets, c1 - b0);
-          if (tid < nb) {
-            const int64_t src = __ldg(a.cov + b0 + tid);
-            const PrePair<V> q = pre_pair<V, TRAIN, 1>(a, x, src, s_tgt, s_int);
-            f_src[tid] = q.ok ? (int32_t)src : -1;
-            f_acc[tid] = q.acc;
-            f_cpu[tid] = q.cpu;
-            f_mem[tid] = q.mem_blk;
-            ++nested_total;  // every lower cover is a nested pair
-          }
-          if (b0 == c0) {
-            // the other chunks' merges, then the level wait (both barriers)
-            if (chunks > 1 &&
-                !wait_count(p, cv, cv.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1))) {
-              ok = false;
-              break;
-            }
-            if (tid < C) m_val[tid] = __ldcg(key + tid);
-            for (int c = tid + kTileTargets; c < C; c += kTileTargets) m_val[c] = __ldcg(key + c);
-            if (!wait_level(p, cv, item.w)) {
-              ok = false;
-              break;
-            }
-            tr1 = p.trace ? globaltimer() : 0;
-          } else {
-            __syncthreads();
-          }
-          for (int c = tid; c < C; c += kTileTargets) {
-            const int k = c / lp1, l = c % lp1;
-            V v = m_val[c];
-            for (int j = 0; j < nb; ++j) {
-              const int32_t src = f_src[j];
-              if (src < 0) continue;
-              const V* row = dpm + (size_t)src * C;
-              const V acc = f_acc[j];
-              if (k >= 1 && acc != INF) {
-                if (kGeneric && a.repl) {
-                  for (int rr = 1; rr <= k; ++rr) {
-                    const V load = rr == 1 ? acc : replicated<V>(a, acc, f_mem[j], rr);
-                    v = min(v, vmax(__ldcg(row + c - rr * lp1), load));
-                  }
-                } else {
-                  v = min(v, vmax(__ldcg(row + c - lp1), acc));
-                }
-              }
-              if (l >= 1) v = min(v, vmax(__ldcg(row + c - 1), f_cpu[j]));
-            }
-            m_val[c] = v;
-          }
-          __syncthreads();
-          if (b0 + kTileTargets >= c1) break;
-        }
-        if (!ok) break;
-        for (int c = tid; c < C; c += kTileTargets) {
-          const int k = c / lp1, l = c % lp1;
-          V v = m_val[c];
-          for (int kk = 0; kk <= k; ++kk)
-            for (int ll = 0; ll <= l; ++ll) v = min(v, m_val[kk * lp1 + ll]);
-          for (int r = 0; r < p.world; ++r) ((V*)p.peer_dp[r])[(size_t)t * C + c] = v;
-        }
-        __syncthreads();  // every cell stored before the (cumulative) release
-        if (tid == 0) {
-          release_done(p, s, 1u);
-          s_any_last = 1;
-        }
-      } else {
+      // One source per thread for the static part: thread j evaluates
+      // source j's subset test and block cost (K2+K3) before any wait.  Once
+      // the sources are final, threads over (cell, source group) fold the
+      // candidates (one L2 round trip for the rows), and the groups merge per
+      // cell.  The finisher starts from the other chunks' merged minima and
+      // ends with monotone_pass (dp_solver.cpp:180-193: in place, k then l
+      // ascending = the 2-D prefix minimum over the (k, l) grid, a row pass
+      // then a column pass); an old chunk merges into the keys and arrives.
+      if (!fin && s1 - s0 > kCellwiseMax) {
         // an old chunk: thread tid takes source s0 + tid
+        init_cells<V, LP1, KP1MAX, TS>(C, best, colv);
         const int64_t my = s0 + tid;
         const bool has = my < s1;
         PrePair<V> q{};
@@ -684,6 +619,109 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
         if (tid == 0) {
           __threadfence();  // cumulative release of this CTA's merges
           atomicAdd(cv.tile_count + p.tile_base[s] + unit, 1u);
+        }
+      } else {
+        const int64_t c0 = fin ? __ldg(a.cov_off + t) : s0;
+        const int64_t c1 = fin ? __ldg(a.cov_off + t + 1) : s1;
+        __shared__ int32_t f_src[kTileTargets];
+        __shared__ V f_acc[kTileTargets], f_cpu[kTileTargets], f_mem[kTileTargets];
+        __shared__ V f_part[kTileTargets];
+        const int lp1 = a.L + 1;
+        const V* dpm = reinterpret_cast<const V*>(cv.dp);
+        bool ok = true;
+        for (int64_t b0 = c0; b0 < c1 || b0 == c0; b0 += kTileTargets) {
+          const int nb = (int)min((int64_t)kTileTargets, c1 - b0);
+          // (cell, group) layout: G <= nb groups of C threads when C <= 128
+          const int G = C <= kTileTargets ? max(1, min(nb, kTileTargets / C)) : 1;
+          const int my_g = C <= kTileTargets ? tid / C : 0, my_c = C <= kTileTargets ? tid % C : tid;
+          if (tid < nb) {
+            const int64_t src = fin ? (int64_t)__ldg(a.cov + b0 + tid) : b0 + tid;
+            const PrePair<V> q = pre_pair<V, TRAIN, 1>(a, x, src, s_tgt, s_int);
+            f_src[tid] = q.ok ? (int32_t)src : -1;
+            f_acc[tid] = q.acc;
+            f_cpu[tid] = q.cpu;
+            f_mem[tid] = q.mem_blk;
+            nested_total += q.nested ? 1u : 0u;  // every lower cover is nested
+          }
+          if (b0 == c0) {
+            // the finisher: the other chunks' merges first (listed before it)
+            if (fin && chunks > 1 &&
+                !wait_count(p, cv, cv.tile_count + p.tile_base[s] + unit, (unsigned)(chunks - 1))) {
+              ok = false;
+              break;
+            }
+            for (int c = tid; c < C; c += kTileTargets) m_val[c] = fin ? __ldcg(key + c) : INF;
+            if (!wait_level(p, cv, item.w)) {  // rows below are read at L2
+              ok = false;
+              break;
+            }
+            tr1 = p.trace ? globaltimer() : 0;
+          } else {
+            __syncthreads();
+          }
+          for (int c = my_c; c < C && my_g < G; c += kTileTargets) {
+            const int k = c / lp1, l = c % lp1;
+            V v = INF;
+            for (int j = my_g; j < nb; j += G) {
+              const int32_t src = f_src[j];
+              if (src < 0) continue;
+              const V* row = dpm + (size_t)src * C;
+              const V acc = f_acc[j];
+              if (k >= 1 && acc != INF) {
+                if (kGeneric && a.repl) {
+                  for (int rr = 1; rr <= k; ++rr) {
+                    const V load = rr == 1 ? acc : replicated<V>(a, acc, f_mem[j], rr);
+                    v = min(v, vmax(__ldcg(row + c - rr * lp1), load));
+                  }
+                } else {
+                  v = min(v, vmax(__ldcg(row + c - lp1), acc));
+                }
+              }
+              if (l >= 1) v = min(v, vmax(__ldcg(row + c - 1), f_cpu[j]));
+            }
+            if (G > 1) f_part[tid] = v;
+            else m_val[c] = min(m_val[c], v);
+          }
+          __syncthreads();
+          if (G > 1) {
+            for (int c = tid; c < C; c += kTileTargets) {
+              V v = m_val[c];
+              for (int g = 0; g < G; ++g) v = min(v, f_part[g * C + c]);
+              m_val[c] = v;
+            }
+            __syncthreads();
+          }
+          if (b0 + kTileTargets >= c1) break;
+        }
+        if (!ok) break;
+        if (fin) {
+          V* tmp = m_val + C;  // row pass (over l), then column pass (over k)
+          for (int c = tid; c < C; c += kTileTargets) {
+            const int l = c % lp1;
+            V v = m_val[c];
+            for (int ll = 1; ll <= l; ++ll) v = min(v, m_val[c - ll]);
+            tmp[c] = v;
+          }
+          __syncthreads();
+          for (int c = tid; c < C; c += kTileTargets) {
+            const int k = c / lp1;
+            V v = tmp[c];
+            for (int kk = 1; kk <= k; ++kk) v = min(v, tmp[c - kk * lp1]);
+            for (int r = 0; r < p.world; ++r) ((V*)p.peer_dp[r])[(size_t)t * C + c] = v;
+          }
+          __syncthreads();  // every cell stored before the (cumulative) release
+          if (tid == 0) {
+            release_done(p, s, 1u);
+            s_any_last = 1;
+          }
+        } else {
+          for (int c = tid; c < C; c += kTileTargets)
+            if (m_val[c] != INF) atomic_min_v(key + c, m_val[c]);
+          __syncthreads();
+          if (tid == 0) {
+            __threadfence();  // cumulative release of this CTA's merges
+            atomicAdd(cv.tile_count + p.tile_base[s] + unit, 1u);
+          }
         }
       }
     }

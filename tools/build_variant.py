@@ -10,7 +10,7 @@ sys.path.insert(0, ROOT)
 from paper_2006_16423_b200 import _build as B
 
 name, src, defs = sys.argv[1], sys.argv[2], sys.argv[3:]
-out = os.path.join(ROOT, "variants", name)
+out = os.path.join(ROOT, os.environ.get("DSG_VARIANT_DIR", "variants"), name)
 os.makedirs(out, exist_ok=True)
 obj = os.path.join(out, src.replace(".cu", ".o"))
 subprocess.run([B.nvcc(), *B.NVCC_FLAGS, *defs, "-I", os.path.join(ROOT, "include"), "-I", B.CSRC,
