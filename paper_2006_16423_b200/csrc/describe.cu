@@ -44,172 +44,286 @@ __device__ __forceinline__ void for_bits(const uint64_t* s, int W, F&& f) {
   }
 }
 
+template <typename T>
+__device__ __forceinline__ T group_sum(T v, int G, unsigned gm) {
+  for (int off = G >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(gm, v, off);
+  return v;
+}
+
+__device__ __forceinline__ uint64_t group_or(uint64_t v, int G, unsigned gm) {
+  for (int off = G >> 1; off > 0; off >>= 1) v |= __shfl_xor_sync(gm, v, off);
+  return v;
+}
+
+constexpr int kDescThreads = 128;
+
+// Lanes per ideal: enough to cover the bitset words (a power of two <= 32),
+// so an ideal of n members costs O(n / G) dependent steps instead of O(n)
+// (one thread per ideal was 0.5 ms on C1's 242 ideals of ~350 members)
+// while small-W lattices keep most lanes busy.
+__host__ __device__ __forceinline__ int desc_group(int W) {
+  int G = 1;
+  while (G < W && G < 32) G <<= 1;
+  return G;
+}
+
+// shared words per group: A, F, T (chunk neighbours), P; then two rank arrays
+__host__ __device__ __forceinline__ size_t desc_smem(int W) {
+  const int groups = kDescThreads / desc_group(W);
+  return (size_t)groups * (4 * W * sizeof(uint64_t) + 2 * (W + 1) * sizeof(int32_t));
+}
+
 template <typename V, bool FILL>
-__global__ void __launch_bounds__(128) describe_kernel(DescribeLaunch a) {
-  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= a.I) return;
+__global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a) {
+  extern __shared__ uint64_t d_sh[];
   const DevGraph& g = a.g;
   const int W = g.W;
-  uint64_t A[kMaxWords], F[kMaxWords], T[kMaxWords];
+  // a group of G lanes per ideal (the lanes split the bitset words); the
+  // ranked outputs (frontier producers in index order, 64 per chunk; the
+  // training lists in index order) come from per-word popcount prefixes
+  const int G = desc_group(W), groups = kDescThreads / G;
+  const int gid = threadIdx.x / G, lane = threadIdx.x % G;
+  const unsigned gm = G == 32 ? 0xffffffffu : ((1u << G) - 1) << ((threadIdx.x & 31) & ~(G - 1));
+  const int64_t o = (int64_t)blockIdx.x * groups + gid;
+  if (o >= a.I) return;  // group-uniform
+  uint64_t* A = d_sh + (size_t)gid * 4 * W;
+  uint64_t* F = A + W;
+  uint64_t* T = F + W;
+  uint64_t* P = T + W;
+  int32_t* rF = reinterpret_cast<int32_t*>(d_sh + (size_t)groups * 4 * W) + (size_t)gid * 2 * (W + 1);
+  int32_t* rT = rF + W + 1;
   const uint64_t* J = a.sbits + (size_t)o * W;
-  for (int w = 0; w < W; ++w) A[w] = J[w];
-  if (a.training) {
-    for_bits(J, W, [&](int v) {
-      const uint64_t* tw = g.twins + (size_t)v * W;
-      for (int w = 0; w < W; ++w) A[w] |= tw[w];
-    });
+  for (int w = lane; w < W; w += G) {
+    A[w] = J[w];
+    F[w] = 0;
+    T[w] = 0;
+    P[w] = 0;
   }
-  // prefix sums, frontier F(A), Σ comm over F(A)
+  __syncwarp(gm);
+  if (a.training) {  // A = J ∪ paired backward nodes (dp_solver.cpp:235-250)
+    for (int w = lane; w < W; w += G) {
+      for (uint64_t x = J[w]; x; x &= x - 1) {
+        const int v = (w << 6) | (__ffsll((long long)x) - 1);
+        const uint64_t* tw = g.twins + (size_t)v * W;
+        for (int y = 0; y < W; ++y) {
+          const uint64_t t = tw[y];
+          if (t) atomicOr((unsigned long long*)&A[y], (unsigned long long)t);
+        }
+      }
+    }
+    __syncwarp(gm);
+  }
+  // prefix sums and the frontier F(A) (members with a real successor outside)
   int64_t cpu = 0, acc = 0, mem = 0, fwv = 0;
   int32_t un = 0, fwi = 0, nF = 0;
-  for (int w = 0; w < W; ++w) F[w] = 0;
-  for_bits(A, W, [&](int v) {
-    cpu += g.cpu[v];
-    acc += g.acc[v];
-    mem += g.mem[v];
-    un += g.unsup[v];
-    bool leaves = false;
-    for (int e = g.out_real_off[v]; e < g.out_real_off[v + 1] && !leaves; ++e)
-      leaves = !bit_of(A, g.out_real_adj[e]);
-    if (leaves) {
-      F[v >> 6] |= 1ull << (v & 63);
-      fwv += g.comm[v];
-      fwi += g.comminf[v];
-      ++nF;
+  for (int w = lane; w < W; w += G) {
+    uint64_t fw = 0;
+    for (uint64_t x = A[w]; x; x &= x - 1) {
+      const int b = __ffsll((long long)x) - 1, v = (w << 6) | b;
+      cpu += g.cpu[v];
+      acc += g.acc[v];
+      mem += g.mem[v];
+      un += g.unsup[v];
+      bool leaves = false;
+      for (int e = g.out_real_off[v]; e < g.out_real_off[v + 1] && !leaves; ++e)
+        leaves = !bit_of(A, g.out_real_adj[e]);
+      if (leaves) {
+        fw |= 1ull << b;
+        fwv += g.comm[v];
+        fwi += g.comminf[v];
+        ++nF;
+      }
     }
-  });
+    F[w] = fw;
+  }
+  cpu = group_sum(cpu, G, gm);
+  acc = group_sum(acc, G, gm);
+  mem = group_sum(mem, G, gm);
+  fwv = group_sum(fwv, G, gm);
+  un = group_sum(un, G, gm);
+  fwi = group_sum(fwi, G, gm);
+  nF = group_sum(nF, G, gm);
+  __syncwarp(gm);
+  if (lane == 0) {
+    int r = 0;
+    for (int w = 0; w < W; ++w) {
+      rF[w] = r;
+      r += __popcll(F[w]);
+    }
+  }
+  __syncwarp(gm);
   const int n_chunks = (nF + 63) / 64;
   int64_t* cnt = a.counts;
   const int64_t stride = a.I + 1;
   int64_t n_items = 0;
   // frontier chunks: producers ranked in index order, 64 per chunk
-  int64_t chunk_base = FILL ? cnt[kCntChunks * stride + o] : 0;
-  int64_t f_base = FILL ? cnt[kCntF * stride + o] : 0;
-  int64_t n_base = FILL ? cnt[kCntN * stride + o] : 0;
+  const int64_t chunk_base = FILL ? cnt[kCntChunks * stride + o] : 0;
+  const int64_t f_base = FILL ? cnt[kCntF * stride + o] : 0;
+  const int64_t n_base = FILL ? cnt[kCntN * stride + o] : 0;
   FChunk first{};
   for (int c = 0; c < n_chunks; ++c) {
-    int lo = c * 64;
-    int hi = min(nF, lo + 64);
-    // chunk members and their upper neighbours
-    for (int w = 0; w < W; ++w) T[w] = 0;
-    int rank = 0;
-    uint64_t infmask = 0;
-    for_bits(F, W, [&](int u) {
-      if (rank >= lo && rank < hi) {
+    const int lo = c * 64, hi = min(nF, lo + 64);
+    // the chunk's upper neighbours T (successors outside A), weights, ∞ mask
+    uint64_t infm = 0;
+    for (int w = lane; w < W; w += G) {
+      int r = rF[w];
+      for (uint64_t x = F[w]; x; x &= x - 1, ++r) {
+        if (r < lo || r >= hi) continue;
+        const int u = (w << 6) | (__ffsll((long long)x) - 1);
         for (int e = g.out_real_off[u]; e < g.out_real_off[u + 1]; ++e) {
-          int x = g.out_real_adj[e];
-          if (!bit_of(A, x)) T[x >> 6] |= 1ull << (x & 63);
+          const int y = g.out_real_adj[e];
+          if (!bit_of(A, y)) atomicOr((unsigned long long*)&T[y >> 6], 1ull << (y & 63));
         }
         if (FILL) {
-          V* fp = (V*)a.fpool;
-          fp[f_base + rank] = (V)g.comm[u];
-          if (g.comminf[u]) infmask |= 1ull << (rank - lo);
+          ((V*)a.fpool)[f_base + r] = (V)g.comm[u];
+          if (g.comminf[u]) infm |= 1ull << (r - lo);
         }
       }
-      ++rank;
-    });
+    }
+    infm = group_or(infm, G, gm);
+    __syncwarp(gm);
     int nN = 0;
-    for (int w = 0; w < W; ++w) nN += __popcll(T[w]);
+    for (int w = lane; w < W; w += G) nN += __popcll(T[w]);
+    nN = group_sum(nN, G, gm);
     if (FILL) {
-      int idx = 0;
-      for_bits(T, W, [&](int x) {
-        uint64_t pm = 0;
+      if (lane == 0) {
         int r = 0;
-        for_bits(F, W, [&](int u) {
-          if (r >= lo && r < hi && bit_of(g.succ_real + (size_t)u * W, x)) pm |= 1ull << (r - lo);
-          ++r;
-        });
-        NItem it;
-        it.word = (uint32_t)(x >> 6);
-        it.bit = (uint32_t)(x & 63);
-        it.predmask = pm;
-        a.nitems[n_base + n_items + idx] = it;
-        ++idx;
-      });
+        for (int w = 0; w < W; ++w) {
+          rT[w] = r;
+          r += __popcll(T[w]);
+        }
+      }
+      __syncwarp(gm);
+      // NItem per upper neighbour y: which chunk producers feed it
+      for (int w = lane; w < W; w += G) {
+        int r = rT[w];
+        for (uint64_t x = T[w]; x; x &= x - 1, ++r) {
+          const int y = (w << 6) | (__ffsll((long long)x) - 1);
+          uint64_t pm = 0;
+          for (int fw = 0; fw < W; ++fw) {
+            int q = rF[fw];
+            if (q >= hi || q + __popcll(F[fw]) <= lo) continue;
+            for (uint64_t z = F[fw]; z; z &= z - 1, ++q) {
+              if (q < lo || q >= hi) continue;
+              const int u = (fw << 6) | (__ffsll((long long)z) - 1);
+              if (bit_of(g.succ_real + (size_t)u * W, y)) pm |= 1ull << (q - lo);
+            }
+          }
+          NItem it;
+          it.word = (uint32_t)(y >> 6);
+          it.bit = (uint32_t)(y & 63);
+          it.predmask = pm;
+          a.nitems[n_base + n_items + r] = it;
+        }
+      }
       FChunk ch;
       ch.n_f = hi - lo;
       ch.n_n = nN;
       ch.off_f = (int32_t)(f_base + lo);
       ch.off_n = (int32_t)(n_base + n_items);
-      ch.infmask = infmask;
-      a.chunks[chunk_base + c] = ch;
+      ch.infmask = infm;
+      if (lane == 0) a.chunks[chunk_base + c] = ch;
       if (c == 0) first = ch;
     }
     n_items += nN;
+    __syncwarp(gm);
+    for (int w = lane; w < W; w += G) T[w] = 0;
+    __syncwarp(gm);
   }
   int64_t nP = 0, nLI = 0;
-  uint8_t up = 1;
+  int up = 1;
   if (a.training) {
     // P'(A) = L(A) = real predecessors of A outside A
-    for (int w = 0; w < W; ++w) T[w] = 0;
-    for_bits(A, W, [&](int v) {
-      for (int e = g.in_real_off[v]; e < g.in_real_off[v + 1]; ++e) {
-        int u = g.in_real_adj[e];
-        if (!bit_of(A, u)) T[u >> 6] |= 1ull << (u & 63);
-      }
-    });
-    int64_t p_base = FILL ? cnt[kCntP * stride + o] : 0;
-    int64_t l_base = FILL ? cnt[kCntL * stride + o] : 0;
-    int64_t li_base = FILL ? cnt[kCntLItems * stride + o] : 0;
-    for_bits(T, W, [&](int u) {
-      const uint64_t* su = g.succ_real + (size_t)u * W;
-      int items = 0;
-      for (int w = 0; w < W; ++w) {
-        uint64_t m = su[w] & A[w];
-        if (m) {
-          if (FILL) {
-            MaskItem mi;
-            mi.word = (uint32_t)w;
-            mi.pad = 0;
-            mi.mask = m;
-            a.litems[li_base + nLI + items] = mi;
-          }
-          ++items;
+    for (int w = lane; w < W; w += G) {
+      for (uint64_t x = A[w]; x; x &= x - 1) {
+        const int v = (w << 6) | (__ffsll((long long)x) - 1);
+        for (int e = g.in_real_off[v]; e < g.in_real_off[v + 1]; ++e) {
+          const int u = g.in_real_adj[e];
+          if (!bit_of(A, u)) atomicOr((unsigned long long*)&P[u >> 6], 1ull << (u & 63));
         }
       }
-      if (FILL) {
-        PItem pi;
-        pi.word = (uint32_t)(u >> 6);
-        pi.bit = (uint32_t)(u & 63);
-        pi.inf = g.comminf[u];
-        pi.pad = 0;
-        pi.weight = g.comm[u];
-        a.pitems[p_base + nP] = pi;
-        LEntry le;
-        le.n_items = items;
-        le.off_items = (int32_t)(li_base + nLI);
-        le.inf = g.comminf[u];
-        le.pad = 0;
-        le.weight = g.comm[u];
-        a.lentries[l_base + nP] = le;
+    }
+    __syncwarp(gm);
+    // per u: one MaskItem per word where succ(u) meets A
+    for (int w = lane; w < W; w += G) {
+      for (uint64_t x = P[w]; x; x &= x - 1) {
+        const int u = (w << 6) | (__ffsll((long long)x) - 1);
+        const uint64_t* su = g.succ_real + (size_t)u * W;
+        for (int y = 0; y < W; ++y) nLI += (su[y] & A[y]) ? 1 : 0;
+        ++nP;
       }
-      nLI += items;
-      ++nP;
-    });
+    }
+    nP = group_sum(nP, G, gm);
+    nLI = group_sum(nLI, G, gm);
+    if (FILL && lane == 0) {  // ranked outputs, in index order (|P'| is small)
+      const int64_t p_base = cnt[kCntP * stride + o];
+      const int64_t l_base = cnt[kCntL * stride + o];
+      const int64_t li_base = cnt[kCntLItems * stride + o];
+      int64_t np = 0, nli = 0;
+      for (int w = 0; w < W; ++w) {
+        for (uint64_t x = P[w]; x; x &= x - 1) {
+          const int u = (w << 6) | (__ffsll((long long)x) - 1);
+          const uint64_t* su = g.succ_real + (size_t)u * W;
+          int items = 0;
+          for (int y = 0; y < W; ++y) {
+            const uint64_t m = su[y] & A[y];
+            if (m) {
+              MaskItem mi;
+              mi.word = (uint32_t)y;
+              mi.pad = 0;
+              mi.mask = m;
+              a.litems[li_base + nli + items] = mi;
+              ++items;
+            }
+          }
+          PItem pi;
+          pi.word = (uint32_t)(u >> 6);
+          pi.bit = (uint32_t)(u & 63);
+          pi.inf = g.comminf[u];
+          pi.pad = 0;
+          pi.weight = g.comm[u];
+          a.pitems[p_base + np] = pi;
+          LEntry le;
+          le.n_items = items;
+          le.off_items = (int32_t)(li_base + nli);
+          le.inf = g.comminf[u];
+          le.pad = 0;
+          le.weight = g.comm[u];
+          a.lentries[l_base + np] = le;
+          nli += items;
+          ++np;
+        }
+      }
+    }
     // Φ(J) = A ∩ backward: an up-set of the backward part?
     if (a.has_bw) {
-      for_bits(A, W, [&](int b) {
-        if (!bit_of(g.bwset, b)) return;
-        const uint64_t* bs = g.bw_succ + (size_t)b * W;
-        for (int w = 0; w < W; ++w)
-          if (bs[w] & ~A[w]) up = 0;
-      });
+      for (int w = lane; w < W; w += G) {
+        for (uint64_t x = A[w] & g.bwset[w]; x; x &= x - 1) {
+          const int b = (w << 6) | (__ffsll((long long)x) - 1);
+          const uint64_t* bs = g.bw_succ + (size_t)b * W;
+          for (int y = 0; y < W; ++y)
+            if (bs[y] & ~A[y]) up = 0;
+        }
+      }
+      up = __all_sync(gm, up) ? 1 : 0;
     }
   }
   if (!FILL) {
-    cnt[kCntChunks * stride + o] = n_chunks;
-    cnt[kCntF * stride + o] = nF;
-    cnt[kCntN * stride + o] = n_items;
-    cnt[kCntP * stride + o] = nP;
-    cnt[kCntL * stride + o] = nP;
-    cnt[kCntLItems * stride + o] = nLI;
+    if (lane == 0) {
+      cnt[kCntChunks * stride + o] = n_chunks;
+      cnt[kCntF * stride + o] = nF;
+      cnt[kCntN * stride + o] = n_items;
+      cnt[kCntP * stride + o] = nP;
+      cnt[kCntL * stride + o] = nP;
+      cnt[kCntLItems * stride + o] = nLI;
+    }
     return;
   }
-  for (int w = 0; w < a.AW; ++w) a.abits[(size_t)o * a.AW + w] = w < W ? A[w] : 0ull;
-  if (a.training) {
-    for (int w = 0; w < W; ++w) a.intbits[(size_t)o * W + w] = A[w] & ~F[w];
-    a.upset[o] = up;
-  }
+  for (int w = lane; w < a.AW; w += G) a.abits[(size_t)o * a.AW + w] = w < W ? A[w] : 0ull;
+  if (a.training)
+    for (int w = lane; w < W; w += G) a.intbits[(size_t)o * W + w] = A[w] & ~F[w];
+  if (lane != 0) return;
+  if (a.training) a.upset[o] = (uint8_t)up;
   ((V*)a.pfx_cpu)[o] = (V)cpu;
   ((V*)a.pfx_acc)[o] = (V)acc;
   ((V*)a.pfx_mem)[o] = (V)mem;
@@ -299,14 +413,16 @@ void launch_chunk_max(const SrcRec* srec, int64_t I, int64_t* out, cudaStream_t 
 }
 
 void launch_describe(const DescribeLaunch& L, bool fill, cudaStream_t st) {
-  int threads = 128;
-  unsigned blocks = (unsigned)((L.I + threads - 1) / threads);
+  const int threads = kDescThreads, groups = kDescThreads / desc_group(L.g.W);
+  const unsigned blocks = (unsigned)((L.I + groups - 1) / groups);
+  const size_t smem = desc_smem(L.g.W);
+  if (blocks == 0) return;
   if (L.value_bits == 32) {
-    if (fill) describe_kernel<int32_t, true><<<blocks, threads, 0, st>>>(L);
-    else describe_kernel<int32_t, false><<<blocks, threads, 0, st>>>(L);
+    if (fill) describe_kernel<int32_t, true><<<blocks, threads, smem, st>>>(L);
+    else describe_kernel<int32_t, false><<<blocks, threads, smem, st>>>(L);
   } else {
-    if (fill) describe_kernel<int64_t, true><<<blocks, threads, 0, st>>>(L);
-    else describe_kernel<int64_t, false><<<blocks, threads, 0, st>>>(L);
+    if (fill) describe_kernel<int64_t, true><<<blocks, threads, smem, st>>>(L);
+    else describe_kernel<int64_t, false><<<blocks, threads, smem, st>>>(L);
   }
   count_launch();
 }
