@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define DSG_ABI_VERSION 1
+#define DSG_ABI_VERSION 2
 #define DSG_NO_PAIR INT32_MIN
 /* reference kDefaultIdealBudget, include/dagsplit/graph.hpp:251 */
 #define DSG_DEFAULT_IDEAL_BUDGET 5000000LL
@@ -141,6 +141,10 @@ typedef struct dsg_block {
   int32_t repl;      /* accelerator replica count (1 unless replicated) */
   int32_t n_members;
   int32_t offset;    /* into dsg_result::members */
+  int64_t load_num;  /* per-device load of the block (acc_cost / cpu_cost /
+                        replicated_load, graph.cpp:397-479) recomputed by the
+                        device at denominator dsg_result::denominator;
+                        INT64_MAX = infinite; valid iff dsg_result::block_loads */
 } dsg_block;
 
 typedef struct dsg_result {
@@ -170,7 +174,7 @@ typedef struct dsg_result {
   int64_t h2d_bytes;      /* host->device bytes copied by this call */
   int64_t d2h_bytes;      /* device->host bytes copied by this call */
   int32_t persistent_blocks; /* CTAs of the persistent level kernel (0: per-level launches) */
-  int32_t pad_;
+  int32_t block_loads;       /* 1: dsg_block::load_num is filled */
   /* DSG_FLAG_KEEP_TABLES: */
   int32_t words;            /* 64-bit words per ideal bitset */
   uint64_t* ideal_bits;     /* n_ideals * words, reference ordinal order */

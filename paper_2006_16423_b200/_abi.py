@@ -85,7 +85,7 @@ class dsg_options(C.Structure):
 
 class dsg_block(C.Structure):
     _fields_ = [("cpu", C.c_int32), ("repl", C.c_int32), ("n_members", C.c_int32),
-                ("offset", C.c_int32)]
+                ("offset", C.c_int32), ("load_num", C.c_int64)]
 
 
 class dsg_result(C.Structure):
@@ -116,7 +116,7 @@ class dsg_result(C.Structure):
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
         ("persistent_blocks", C.c_int32),
-        ("pad_", C.c_int32),
+        ("block_loads", C.c_int32),
         ("words", C.c_int32),
         ("ideal_bits", C.POINTER(C.c_uint64)),
         ("dp_values", C.POINTER(C.c_int64)),

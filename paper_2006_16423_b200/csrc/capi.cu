@@ -516,35 +516,70 @@ struct DeviceGraph {
   int32_t *pu_off, *pu_adj, *su_off, *su_adj;
 };
 
+// Every host array of the prepared graph packed into the context's pinned
+// staging buffer and moved with ONE host->device copy into one device buffer
+// (two dozen pageable cudaMemcpyAsync calls cost ~0.2 ms per solve).
+struct Packer {
+  std::vector<std::pair<const void*, size_t>> parts;
+  std::vector<size_t> offs;
+  size_t total = 0;
+  template <typename T>
+  size_t add(const std::vector<T>& v) {
+    const size_t off = total;
+    const size_t bytes = std::max<size_t>(v.size(), 1) * sizeof(T);
+    parts.push_back({v.empty() ? nullptr : v.data(), v.size() * sizeof(T)});
+    offs.push_back(off);
+    total = off + ((bytes + 15) & ~(size_t)15);
+    return off;
+  }
+};
+
 DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P, const std::string& prefix) {
+  Packer pk;
+  const size_t o_cpu = pk.add(P.cpu), o_acc = pk.add(P.acc), o_comm = pk.add(P.comm),
+               o_mem = pk.add(P.mem), o_unsup = pk.add(P.unsup), o_comminf = pk.add(P.comminf),
+               o_sr = pk.add(P.succ_real), o_pr = pk.add(P.pred_real), o_pu = pk.add(P.pred_u),
+               o_su = pk.add(P.succ_u), o_tw = pk.add(P.twins), o_bws = pk.add(P.bw_succ),
+               o_bwf = pk.add(P.bw_from), o_bwt = pk.add(P.bw_to), o_bwset = pk.add(P.bwset),
+               o_oo = pk.add(P.out_off), o_oa = pk.add(P.out_adj), o_io = pk.add(P.in_off),
+               o_ia = pk.add(P.in_adj), o_univ = pk.add(P.in_universe), o_puo = pk.add(P.pu_off),
+               o_pua = pk.add(P.pu_adj), o_suo = pk.add(P.su_off), o_sua = pk.add(P.su_adj);
+  char* host = static_cast<char*>(ctx.host(pk.total));
+  for (size_t i = 0; i < pk.parts.size(); ++i)
+    if (pk.parts[i].second) std::memcpy(host + pk.offs[i], pk.parts[i].first, pk.parts[i].second);
+  char* dev = static_cast<char*>(ctx.get(prefix + "graph", pk.total));
+  CK(cudaMemcpyAsync(dev, host, pk.total, cudaMemcpyHostToDevice, ctx.stream));
+  ctx.h2d_bytes += (int64_t)pk.total;
+  // the staging buffer is reused by the next solve: the copy must land first
+  CK(cudaStreamSynchronize(ctx.stream));
   DeviceGraph d;
   DevGraph& g = d.g;
   g.n = P.n;
   g.W = P.W;
-  g.cpu = upload(ctx, prefix + "cpu", P.cpu);
-  g.acc = upload(ctx, prefix + "acc", P.acc);
-  g.comm = upload(ctx, prefix + "comm", P.comm);
-  g.mem = upload(ctx, prefix + "mem", P.mem);
-  g.unsup = upload(ctx, prefix + "unsup", P.unsup);
-  g.comminf = upload(ctx, prefix + "comminf", P.comminf);
-  g.succ_real = upload(ctx, prefix + "succ_real", P.succ_real);
-  g.pred_real = upload(ctx, prefix + "pred_real", P.pred_real);
-  g.pred_u = upload(ctx, prefix + "pred_u", P.pred_u);
-  g.succ_u = upload(ctx, prefix + "succ_u", P.succ_u);
-  g.twins = upload(ctx, prefix + "twins", P.twins);
-  g.bw_succ = upload(ctx, prefix + "bw_succ", P.bw_succ);
-  g.bw_from = upload(ctx, prefix + "bw_from", P.bw_from);
-  g.bw_to = upload(ctx, prefix + "bw_to", P.bw_to);
-  g.bwset = upload(ctx, prefix + "bwset", P.bwset);
-  g.out_real_off = upload(ctx, prefix + "out_off", P.out_off);
-  g.out_real_adj = upload(ctx, prefix + "out_adj", P.out_adj);
-  g.in_real_off = upload(ctx, prefix + "in_off", P.in_off);
-  g.in_real_adj = upload(ctx, prefix + "in_adj", P.in_adj);
-  d.in_universe = upload(ctx, prefix + "in_universe", P.in_universe);
-  d.pu_off = upload(ctx, prefix + "pu_off", P.pu_off);
-  d.pu_adj = upload(ctx, prefix + "pu_adj", P.pu_adj);
-  d.su_off = upload(ctx, prefix + "su_off", P.su_off);
-  d.su_adj = upload(ctx, prefix + "su_adj", P.su_adj);
+  g.cpu = reinterpret_cast<const int64_t*>(dev + o_cpu);
+  g.acc = reinterpret_cast<const int64_t*>(dev + o_acc);
+  g.comm = reinterpret_cast<const int64_t*>(dev + o_comm);
+  g.mem = reinterpret_cast<const int64_t*>(dev + o_mem);
+  g.unsup = reinterpret_cast<const uint8_t*>(dev + o_unsup);
+  g.comminf = reinterpret_cast<const uint8_t*>(dev + o_comminf);
+  g.succ_real = reinterpret_cast<const uint64_t*>(dev + o_sr);
+  g.pred_real = reinterpret_cast<const uint64_t*>(dev + o_pr);
+  g.pred_u = reinterpret_cast<const uint64_t*>(dev + o_pu);
+  g.succ_u = reinterpret_cast<const uint64_t*>(dev + o_su);
+  g.twins = reinterpret_cast<const uint64_t*>(dev + o_tw);
+  g.bw_succ = reinterpret_cast<const uint64_t*>(dev + o_bws);
+  g.bw_from = reinterpret_cast<const uint64_t*>(dev + o_bwf);
+  g.bw_to = reinterpret_cast<const uint64_t*>(dev + o_bwt);
+  g.bwset = reinterpret_cast<const uint64_t*>(dev + o_bwset);
+  g.out_real_off = reinterpret_cast<const int32_t*>(dev + o_oo);
+  g.out_real_adj = reinterpret_cast<const int32_t*>(dev + o_oa);
+  g.in_real_off = reinterpret_cast<const int32_t*>(dev + o_io);
+  g.in_real_adj = reinterpret_cast<const int32_t*>(dev + o_ia);
+  d.in_universe = reinterpret_cast<uint8_t*>(dev + o_univ);
+  d.pu_off = reinterpret_cast<int32_t*>(dev + o_puo);
+  d.pu_adj = reinterpret_cast<int32_t*>(dev + o_pua);
+  d.su_off = reinterpret_cast<int32_t*>(dev + o_suo);
+  d.su_adj = reinterpret_cast<int32_t*>(dev + o_sua);
   return d;
 }
 
@@ -1273,6 +1308,7 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
   TraceState tb{};
   std::vector<int32_t> cpus(maxb);
   std::vector<uint64_t> bbits((size_t)maxb * W);
+  std::vector<int64_t> loads(maxb, 0);
   if (do_traceback) {
     TraceBuffers tbuf;
     tbuf.state = ctx.get_t<TraceState>(pl.pfx + "tb.state", 1);
@@ -1283,10 +1319,12 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
     tbuf.prevs = ctx.get_t<int64_t>(pl.pfx + "tb.prevs", maxb);
     tbuf.kinds = ctx.get_t<int32_t>(pl.pfx + "tb.kinds", maxb);
     tbuf.block_bits = ctx.get_t<uint64_t>(pl.pfx + "tb.bits", (size_t)maxb * W);
+    tbuf.loads = ctx.get_t<int64_t>(pl.pfx + "tb.loads", maxb);
     launch_traceback(LL, pl.level_of_d, pl.level_off_d, I, ctx.sm_count, tbuf, st);
     D2H(&tb, tbuf.state, sizeof tb);
     D2H(cpus.data(), tbuf.kinds, sizeof(int32_t) * maxb);
     D2H(bbits.data(), tbuf.block_bits, sizeof(uint64_t) * maxb * W);
+    D2H(loads.data(), tbuf.loads, sizeof(int64_t) * maxb);
   }
   if (flags & DSG_FLAG_KEEP_TABLES) {
     res->words = W;
@@ -1336,6 +1374,7 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
   res->objective.num = tb.best_value / (g ? g : 1);
   res->objective.den = P.D / (g ? g : 1);
   res->best_k = tb.best_k;
+  res->block_loads = 1;
   res->best_l = tb.best_l;
   res->n_blocks = tb.n_blocks;
   res->blocks = (dsg_block*)std::calloc((size_t)std::max(1, tb.n_blocks), sizeof(dsg_block));
@@ -1346,6 +1385,7 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
     blk.cpu = cpus[b] & 1;
     blk.repl = cpus[b] >> 1;
     blk.offset = off;
+    blk.load_num = loads[b];
     for (int w = 0; w < W; ++w) {
       uint64_t x = bbits[(size_t)b * W + w];
       while (x) {

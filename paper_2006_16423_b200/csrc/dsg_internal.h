@@ -282,6 +282,7 @@ struct TraceBuffers {
   int64_t* prevs;
   int32_t* kinds;        // cpu | repl << 1
   uint64_t* block_bits;  // [K+L+1][W]
+  int64_t* loads;        // [K+L+1] per-device load of each block (INT64_MAX = inf)
 };
 
 void launch_traceback(const LevelLaunch& L, const int32_t* level_of, const int64_t* level_off,

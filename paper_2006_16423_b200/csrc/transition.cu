@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(256) traceback_search_kernel(const LevelLaunch
                                                                V* part_v, int32_t* part_g,
                                                                int64_t* ords, int64_t* prevs,
                                                                int32_t* kinds,
-                                                               uint64_t* block_bits) {
+                                                               uint64_t* block_bits,
+                                                               int64_t* loads) {
   constexpr V INF = VTraits<V>::INF;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ V red_v[256];
@@ -264,8 +265,20 @@ __global__ void __launch_bounds__(256) traceback_search_kernel(const LevelLaunch
   }
   if (threadIdx.x == 0) {
     st->arrivals = 0;
+    const int nb = st->n_blocks;
     traceback_decide<V>(a.K, a.L, a.W, a.AW, dp, a.abits, red_v[0], red_g[0], st, ords, prevs,
                         kinds, block_bits);
+    if (st->n_blocks > nb) {
+      // the block's per-device load, recomputed from the closed forms (what
+      // make_canonical_split reports, graph.cpp:573-621)
+      bool gated;
+      V acc, cpu, mem_blk;
+      pair_cost<V, TRAIN, 1>(a, x, prevs[nb], tA, tInt, gated, acc, cpu, mem_blk);
+      const int kind = kinds[nb];
+      V load = (kind & 1) ? cpu : acc;
+      if (!(kind & 1) && (kind >> 1) > 1 && acc != INF) load = replicated<V>(a, acc, mem_blk, kind >> 1);
+      loads[nb] = load == INF ? INT64_MAX : (int64_t)load;
+    }
   }
 }
 
@@ -357,11 +370,11 @@ void traceback_t(const LevelLaunch& L, const int32_t* level_of, const int64_t* l
     if (L.training)
       traceback_search_kernel<V, true><<<grid, 256, smem, st>>>(
           L, b.state, level_of, level_off, (V*)b.part_v, b.part_g, b.ords, b.prevs, b.kinds,
-          b.block_bits);
+          b.block_bits, b.loads);
     else
       traceback_search_kernel<V, false><<<grid, 256, smem, st>>>(
           L, b.state, level_of, level_off, (V*)b.part_v, b.part_g, b.ords, b.prevs, b.kinds,
-          b.block_bits);
+          b.block_bits, b.loads);
     count_launch();
   }
   (void)sm_count;

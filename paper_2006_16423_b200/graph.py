@@ -228,6 +228,7 @@ class SplitBlock:
     cpu: bool
     members: List[int]
     repl: int = 1
+    load: Optional[Num] = None  # per-device load recomputed by the device, if reported
 
 
 # ---------------------------------------------------------------- costs
@@ -320,10 +321,14 @@ def make_canonical_split(g: Graph, config: DeviceConfig, blocks: List[SplitBlock
         pl = Placement.cpu(next_cpu) if b.cpu else Placement.acc(next_acc)
         for v in b.members:
             split.assignment[g.id_of(v)] = pl
-        load = cpu_cost(g, b.members) if b.cpu else acc_cost(g, b.members, config)
+        if b.load is not None:
+            load = b.load  # recomputed on the device (dsg_block::load_num)
+        else:
+            load = cpu_cost(g, b.members) if b.cpu else acc_cost(g, b.members, config)
+            if not b.cpu and b.repl > 1:
+                mem = _fsum(g.node(v).mem_size for v in b.members)
+                load = _replicated(load, mem, b.repl, config)
         if not b.cpu and b.repl > 1:
-            mem = _fsum(g.node(v).mem_size for v in b.members)
-            load = _replicated(load, mem, b.repl, config)
             split.replication[pl.label()] = b.repl
             for r in range(b.repl):
                 split.per_device_loads.append((Placement.acc(next_acc + r).label(), load))

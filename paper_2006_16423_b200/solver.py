@@ -15,7 +15,11 @@ import numpy as np
 
 from . import _abi
 from .errors import DeviceError, raise_for_status
-from .graph import DeviceConfig, Graph, SplitBlock, make_canonical_split
+from fractions import Fraction
+
+from .graph import INF, DeviceConfig, Graph, SplitBlock, make_canonical_split
+
+_I64_MAX = (1 << 63) - 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # DSG_B200_LIB: an alternative build of the same library (kernel variants
@@ -98,7 +102,10 @@ def _raw_from(res, config: DeviceConfig) -> RawResult:
     for b in range(res.n_blocks):
         blk = res.blocks[b]
         members = [res.members[blk.offset + i] for i in range(blk.n_members)]
-        blocks.append(SplitBlock(cpu=bool(blk.cpu), members=members, repl=blk.repl))
+        load = None
+        if res.block_loads:
+            load = INF if blk.load_num == _I64_MAX else Fraction(blk.load_num, res.denominator)
+        blocks.append(SplitBlock(cpu=bool(blk.cpu), members=members, repl=blk.repl, load=load))
     stats = {k: getattr(res, k) for k in STAT_FIELDS}
     return RawResult(_abi.from_dsg_rat(res.objective), blocks, res.best_k, res.best_l,
                      res.n_ideals, res.n_pairs, res.n_levels, res.value_bits, res.denominator,

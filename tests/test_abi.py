@@ -39,7 +39,7 @@ def test_struct_sizes_match_the_header_layout():
     assert C.sizeof(_abi.dsg_rat) == 16
     assert C.sizeof(_abi.dsg_graph) == 4 + 4 + 8 * 7 + 4 + 4 + 16 + 4 + 4 + 16
     assert C.sizeof(_abi.dsg_options) == 32
-    assert C.sizeof(_abi.dsg_block) == 16
+    assert C.sizeof(_abi.dsg_block) == 24
 
 
 def test_version_string():

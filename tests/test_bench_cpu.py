@@ -19,7 +19,7 @@ def test_bench_compiles():
 @pytest.mark.skipif(not os.path.exists(REF), reason="oracle/_ref not built")
 def test_reference_arm_prints_one_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                          "--steps", "1", "--warmup", "0", "--workload", "C1"], capture_output=True, text=True,
                          timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stderr
     line = json.loads(out.stdout.strip().splitlines()[-1])
