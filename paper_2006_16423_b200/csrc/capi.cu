@@ -64,6 +64,18 @@ struct Fail {
       throw Fail{DSG_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)};     \
   } while (0)
 
+// DSG_DEBUG_SYNC=1: synchronise after a launch group and name it in the
+// error (debugging aid; the sanitizer is not available on the GPU pool)
+#define debug_sync(ctx, what)                                                              \
+  do {                                                                                     \
+    static const bool on_ = std::getenv("DSG_DEBUG_SYNC") != nullptr;                      \
+    if (on_) {                                                                             \
+      cudaError_t e_ = cudaStreamSynchronize((ctx).stream);                                \
+      if (e_ != cudaSuccess)                                                               \
+        throw Fail{DSG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e_)};     \
+    }                                                                                      \
+  } while (0)
+
 double ms_since(Clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
 }
@@ -637,6 +649,7 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
     CK(cudaMemsetAsync(st_d, 0, sizeof(EnumStatus), ctx.stream));
     launch_enumerate(L, ctx.stream);
     CK(cudaGetLastError());
+    debug_sync(ctx, "enumerate");
     EnumStatus st;
     D2H(&st, st_d, sizeof st);
     CK(cudaStreamSynchronize(ctx.stream));
@@ -657,8 +670,15 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
     D2H(lat.level_off.data(), lvl_d, sizeof(int64_t) * (lat.n_levels + 1));
     lat.sbits = ctx.get_t<uint64_t>(pfx + "lat.sbits", (size_t)lat.I * W);
     lat.smax = ctx.get_t<uint64_t>(pfx + "lat.smax", (size_t)lat.I * W);
-    launch_lex_rank(W, lat.I, L.bits, L.maxm, L.level_of, lvl_d, lat.sbits, lat.smax, ctx.stream);
+    int64_t max_level = 0;
+    for (int s = 0; s < lat.n_levels; ++s)
+      max_level = std::max(max_level, lat.level_off[s + 1] - lat.level_off[s]);
+    int64_t* perm_a = ctx.get_t<int64_t>("enum.perm_a", (size_t)lat.I);
+    int64_t* perm_b = ctx.get_t<int64_t>("enum.perm_b", (size_t)lat.I);
+    launch_lex_rank(W, lat.I, L.bits, L.maxm, L.level_of, lvl_d, lat.sbits, lat.smax, max_level,
+                    perm_a, perm_b, ctx.stream);
     CK(cudaGetLastError());
+    debug_sync(ctx, "lex rank");
     CK(cudaStreamSynchronize(ctx.stream));
     return lat;
   }

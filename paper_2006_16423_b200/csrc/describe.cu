@@ -59,17 +59,19 @@ constexpr int kDescThreads = 128;
 
 // Lanes per ideal: enough to cover the bitset words (a power of two <= 32),
 // so an ideal of n members costs O(n / G) dependent steps instead of O(n)
-// (one thread per ideal was 0.5 ms on C1's 242 ideals of ~350 members)
-// while small-W lattices keep most lanes busy.
-__host__ __device__ __forceinline__ int desc_group(int W) {
+// (one thread per ideal was 0.5 ms on C1's 242 ideals of ~350 members) —
+// but no more lanes than about one full wave of threads needs: large
+// lattices keep all lanes busy with fewer lanes per ideal.
+__host__ __device__ __forceinline__ int desc_group(int W, int64_t I) {
   int G = 1;
   while (G < W && G < 32) G <<= 1;
+  while (G > 1 && I * G > 148 * 8 * kDescThreads) G >>= 1;
   return G;
 }
 
 // shared words per group: A, F, T (chunk neighbours), P; then two rank arrays
-__host__ __device__ __forceinline__ size_t desc_smem(int W) {
-  const int groups = kDescThreads / desc_group(W);
+__host__ __device__ __forceinline__ size_t desc_smem(int W, int64_t I) {
+  const int groups = kDescThreads / desc_group(W, I);
   return (size_t)groups * (4 * W * sizeof(uint64_t) + 2 * (W + 1) * sizeof(int32_t));
 }
 
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
   // a group of G lanes per ideal (the lanes split the bitset words); the
   // ranked outputs (frontier producers in index order, 64 per chunk; the
   // training lists in index order) come from per-word popcount prefixes
-  const int G = desc_group(W), groups = kDescThreads / G;
+  const int G = desc_group(W, a.I), groups = kDescThreads / G;
   const int gid = threadIdx.x / G, lane = threadIdx.x % G;
   const unsigned gm = G == 32 ? 0xffffffffu : ((1u << G) - 1) << ((threadIdx.x & 31) & ~(G - 1));
   const int64_t o = (int64_t)blockIdx.x * groups + gid;
@@ -413,9 +415,9 @@ void launch_chunk_max(const SrcRec* srec, int64_t I, int64_t* out, cudaStream_t 
 }
 
 void launch_describe(const DescribeLaunch& L, bool fill, cudaStream_t st) {
-  const int threads = kDescThreads, groups = kDescThreads / desc_group(L.g.W);
+  const int threads = kDescThreads, groups = kDescThreads / desc_group(L.g.W, L.I);
   const unsigned blocks = (unsigned)((L.I + groups - 1) / groups);
-  const size_t smem = desc_smem(L.g.W);
+  const size_t smem = desc_smem(L.g.W, L.I);
   if (blocks == 0) return;
   if (L.value_bits == 32) {
     if (fill) describe_kernel<int32_t, true><<<blocks, threads, smem, st>>>(L);

@@ -49,9 +49,12 @@ struct EnumLaunch {
 };
 
 void launch_enumerate(const EnumLaunch& L, cudaStream_t st);
+// level order (size-major, NodeSet::lex_less within a level); max_level =
+// the largest level size, perm_a / perm_b: [total] scratch for large levels
 void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
                      const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,
-                     uint64_t* out_maxm, cudaStream_t st);
+                     uint64_t* out_maxm, int64_t max_level, int64_t* perm_a, int64_t* perm_b,
+                     cudaStream_t st);
 // lower covers of every ideal (ordinals one level down), CSR over ordinals
 void launch_cover_count(int W, int64_t I, const uint64_t* smax, int64_t* cnt, cudaStream_t st);
 void launch_cover_fill(int W, int64_t I, const uint64_t* sbits, const uint64_t* smax,

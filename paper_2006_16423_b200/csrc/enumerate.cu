@@ -23,6 +23,7 @@
 // between levels: no host round trip and no grid barrier per level.
 #include <cooperative_groups.h>
 #include <cooperative_groups/reduce.h>
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -679,6 +680,85 @@ __device__ __forceinline__ bool lex_less(const uint64_t* a, const uint64_t* b, i
 constexpr int kRankRows = 64;   // ideals ranked per CTA
 constexpr int kRankParts = 4;   // threads per ideal (each takes every 4th row)
 
+// Levels above kRankDirect ideals are ordered by chunk-local ranks (the
+// all-pairs count inside aligned chunks of kRankDirect) followed by
+// merge-path passes (each element's position in the merged run = its
+// position in its own run + a binary search in the partner run): O(T log T)
+// comparisons instead of the direct rank's O(T^2) (a 12,870-ideal level of
+// the 3 %-dense sweep point cost 2.4 ms that way).
+constexpr int64_t kRankDirect = 1024;
+constexpr int64_t kRankChunk = 256;  // chunk-local ranks, then merges from this width
+
+// a before b in the level order (NodeSet::lex_less, graph.cpp:62-72): the
+// set holding the smallest differing index comes first = the larger
+// bit-reversed word at the first difference
+__device__ __forceinline__ bool lex_before(const uint64_t* a, const uint64_t* b, int W) {
+  for (int w = 0; w < W; ++w) {
+    const uint64_t x = __brevll(__ldg(a + w)), y = __brevll(__ldg(b + w));
+    if (x != y) return x > y;
+  }
+  return false;
+}
+
+__global__ void rank_chunk_kernel(int W, int64_t total, const uint64_t* __restrict__ bits,
+                                  const int32_t* __restrict__ level_of,
+                                  const int64_t* __restrict__ level_off, int64_t* __restrict__ perm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int s = level_of[i];
+  const int64_t lo = level_off[s], hi = level_off[s + 1];
+  if (hi - lo <= kRankDirect) return;
+  const int64_t c0 = lo + (i - lo) / kRankChunk * kRankChunk, c1 = min(hi, c0 + kRankChunk);
+  const uint64_t* bi = bits + (size_t)i * W;
+  int64_t r = 0;
+  for (int64_t j = c0; j < c1; ++j) r += lex_before(bits + (size_t)j * W, bi, W) ? 1 : 0;
+  perm[c0 + r] = i;
+}
+
+__global__ void merge_pass_kernel(int W, int64_t total, int64_t width,
+                                  const uint64_t* __restrict__ bits,
+                                  const int32_t* __restrict__ level_of,
+                                  const int64_t* __restrict__ level_off,
+                                  const int64_t* __restrict__ in, int64_t* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= total) return;
+  const int s = level_of[p];  // positions keep their level
+  const int64_t lo = level_off[s], hi = level_off[s + 1];
+  if (hi - lo <= kRankDirect) return;
+  const int64_t run = (p - lo) / width, r0 = lo + run * width;
+  const int64_t q0 = lo + (run ^ 1) * width, q1 = min(hi, q0 + width);
+  const int64_t e = in[p];
+  if (q0 >= hi) {  // no partner run (the odd last one): stays in place
+    out[p] = e;
+    return;
+  }
+  const uint64_t* be = bits + (size_t)e * W;
+  int64_t a = q0, b = q1;  // partner elements before e
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (lex_before(bits + (size_t)in[m] * W, be, W)) a = m + 1;
+    else b = m;
+  }
+  out[min(r0, q0) + (p - r0) + (a - q0)] = e;
+}
+
+__global__ void scatter_perm_kernel(int W, int64_t total, const uint64_t* __restrict__ bits,
+                                    const uint64_t* __restrict__ maxm,
+                                    const int32_t* __restrict__ level_of,
+                                    const int64_t* __restrict__ level_off,
+                                    const int64_t* __restrict__ perm, uint64_t* __restrict__ out_bits,
+                                    uint64_t* __restrict__ out_maxm) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= total) return;
+  const int s = level_of[p];
+  if (level_off[s + 1] - level_off[s] <= kRankDirect) return;
+  const int64_t e = perm[p];
+  for (int w = 0; w < W; ++w) {
+    out_bits[(size_t)p * W + w] = bits[(size_t)e * W + w];
+    out_maxm[(size_t)p * W + w] = maxm[(size_t)e * W + w];
+  }
+}
+
 __global__ void __launch_bounds__(kRankRows* kRankParts)
     lex_rank_scatter_kernel(int W, int64_t total, const uint64_t* __restrict__ bits,
                             const uint64_t* __restrict__ maxm, const int32_t* __restrict__ level_of,
@@ -689,10 +769,11 @@ __global__ void __launch_bounds__(kRankRows* kRankParts)
   const int row = threadIdx.x % kRankRows, part = threadIdx.x / kRankRows;
   const int64_t i0 = (int64_t)blockIdx.x * kRankRows;
   const int64_t i = i0 + row;
-  const bool act = i < total;
   const int64_t il = min(i, total - 1);
   const int s = level_of[il];
   const int64_t lo = level_off[s], hi = level_off[s + 1];
+  // levels above kRankDirect: rank_chunk + merge passes instead
+  const bool act = i < total && hi - lo <= kRankDirect;
   const uint64_t* bi = bits + (size_t)il * W;
   int rank = 0;
   if (W <= 8) {
@@ -702,8 +783,19 @@ __global__ void __launch_bounds__(kRankRows* kRankParts)
     // The CTA tiles the union of its rows' levels through shared memory.
     uint64_t key[8];
     for (int w = 0; w < W; ++w) key[w] = __brevll(bi[w]);
-    const int64_t il_last = min(i0 + kRankRows, total) - 1;
-    const int64_t ulo = level_off[level_of[i0]], uhi = level_off[level_of[il_last] + 1];
+    // the union of the (direct-ranked) levels of this CTA's rows
+    __shared__ unsigned long long s_ulo, s_uhi;
+    if (threadIdx.x == 0) {
+      s_ulo = ~0ull;
+      s_uhi = 0;
+    }
+    __syncthreads();
+    if (part == 0 && act) {
+      atomicMin(&s_ulo, (unsigned long long)lo);
+      atomicMax(&s_uhi, (unsigned long long)hi);
+    }
+    __syncthreads();
+    const int64_t uhi = (int64_t)s_uhi, ulo = uhi ? (int64_t)s_ulo : 0;  // none: empty range
     const int tile = kRankRows * kRankParts;
     for (int64_t t0 = ulo; t0 < uhi; t0 += tile) {
       const int n = (int)min((int64_t)tile, uhi - t0);
@@ -719,7 +811,7 @@ __global__ void __launch_bounds__(kRankRows* kRankParts)
         rank += bj[w] > key[w] ? 1 : 0;
       }
     }
-  } else {
+  } else if (act) {
     for (int64_t j = lo + part; j < hi; j += kRankParts)
       rank += lex_less(bits + (size_t)j * W, bi, W) ? 1 : 0;
   }
@@ -833,11 +925,24 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
 
 void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
                      const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,
-                     uint64_t* out_maxm, cudaStream_t st) {
+                     uint64_t* out_maxm, int64_t max_level, int64_t* perm_a, int64_t* perm_b,
+                     cudaStream_t st) {
   const int64_t blocks = (total + kRankRows - 1) / kRankRows;
   const size_t smem = W <= 8 ? (size_t)kRankRows * kRankParts * W * sizeof(uint64_t) : 0;
   lex_rank_scatter_kernel<<<(unsigned)blocks, kRankRows * kRankParts, smem, st>>>(
       W, total, bits, maxm, level_of, level_off, out_bits, out_maxm);
+  count_launch();
+  if (max_level <= kRankDirect) return;
+  const unsigned g = (unsigned)((total + 255) / 256);
+  rank_chunk_kernel<<<g, 256, 0, st>>>(W, total, bits, level_of, level_off, perm_a);
+  count_launch();
+  for (int64_t width = kRankChunk; width < max_level; width *= 2) {
+    merge_pass_kernel<<<g, 256, 0, st>>>(W, total, width, bits, level_of, level_off, perm_a, perm_b);
+    count_launch();
+    std::swap(perm_a, perm_b);
+  }
+  scatter_perm_kernel<<<g, 256, 0, st>>>(W, total, bits, maxm, level_of, level_off, perm_a,
+                                         out_bits, out_maxm);
   count_launch();
 }
 
