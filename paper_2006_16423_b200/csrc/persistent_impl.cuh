@@ -319,21 +319,55 @@ __device__ bool arrive_finalize_unit(const LevelLaunch& a, const PersistPlan& p,
   return true;
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+// mbarrier + bulk-copy (TMA engine, 1-D) helpers
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile(
+      "{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// global -> shared bulk copy (bytes % 16 == 0, both ends 16-byte aligned),
+// completing on the CTA's mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // Stage a mode-0 old chunk's sources [s0, s1) — bitset rows, records and
 // (16-byte aligned superset of the) dp rows, all contiguous in HBM — into
-// shared memory with 16-byte async copies from all 128 threads: the chunk's
-// loads are in flight at once instead of one dependent round trip per
-// source iteration.  Ends with the CTA barrier.
+// shared memory with up to three bulk copies issued by one thread on the
+// TMA engine, completing on the CTA's mbarrier (phase `ph`, flipped here);
+// every thread then waits on the barrier.  The rows were produced by other
+// CTAs through the generic proxy and released before the level counter the
+// caller observed; the async proxy's reads are ordered after that by a proxy
+// fence.
 template <typename V>
 __device__ __forceinline__ SrcView<V> stage_sources(const LevelLaunch& a, const void* dpm,
                                                     int64_t s0, int64_t s1, int C,
-                                                    unsigned char* st, bool bits_only = false) {
-  const int tid = threadIdx.x;
+                                                    unsigned char* st, uint64_t* bar,
+                                                    unsigned& ph, bool bits_only = false) {
   const int64_t n = s1 - s0;
   const size_t nb = (size_t)n * a.AW * 8, nr = (size_t)n * sizeof(SrcRec);
   const char* gb = reinterpret_cast<const char*>(a.abits + (size_t)s0 * a.AW);
@@ -344,13 +378,17 @@ __device__ __forceinline__ SrcView<V> stage_sources(const LevelLaunch& a, const 
   unsigned char* sb = st;
   unsigned char* sr = sb + nb;
   unsigned char* sd = sr + nr;
-  for (size_t i = (size_t)tid * 16; i < nb; i += kTileTargets * 16) cp_async16(sb + i, gb + i);
-  if (!bits_only) {
-    for (size_t i = (size_t)tid * 16; i < nr; i += kTileTargets * 16) cp_async16(sr + i, gr + i);
-    for (size_t i = (size_t)tid * 16; i < de - da; i += kTileTargets * 16) cp_async16(sd + i, gd + i);
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mbar_arrive_expect_tx(bar, (unsigned)(bits_only ? nb : nb + nr + (de - da)));
+    bulk_g2s(sb, gb, (unsigned)nb, bar);
+    if (!bits_only) {
+      bulk_g2s(sr, gr, (unsigned)nr, bar);
+      bulk_g2s(sd, gd, (unsigned)(de - da), bar);
+    }
   }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
-  __syncthreads();
+  mbar_wait(bar, ph);
+  ph ^= 1u;
   SrcView<V> v;
   v.bits = reinterpret_cast<const uint64_t*>(sb);
   v.rec = reinterpret_cast<const SrcRec*>(sr);
@@ -384,6 +422,13 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       smem + ((reinterpret_cast<unsigned char*>(g_val + (kGeneric ? (size_t)kWarps * C * TS : 0)) -
                smem + 15) & ~(ptrdiff_t)15);
   unsigned nested_total = 0;
+  // the staging area's mbarrier (one arrival: the issuing thread's expect_tx)
+  __shared__ __align__(8) uint64_t s_stage_bar;
+  unsigned stage_ph = 0;
+  if (tid == 0) {
+    mbar_init(&s_stage_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   // this CTA's rank-local tables (virtual shards: rank blockIdx.x % world)
   __shared__ CtaView cv;
   if (tid == 0) {
@@ -493,7 +538,7 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       tr1 = p.trace ? globaltimer() : 0;
       if (dead) {
         if (p.stage) {
-          const SrcView<V> sv = stage_sources<V>(a, cv.dp, s0, s1, C, st_area, true);
+          const SrcView<V> sv = stage_sources<V>(a, cv.dp, s0, s1, C, st_area, &s_stage_bar, stage_ph, true);
           nested_total += count_nested<TS, WT, CX, true>(a, x.active, s0 + warp, s1, kWarps,
                                                          s_tgt + lane, sv.bits, sv.base);
         } else {
@@ -513,7 +558,7 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
         } else if (p.stage) {
           nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX, 0, true>(
               a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv,
-              stage_sources<V>(a, cv.dp, s0, s1, C, st_area));
+              stage_sources<V>(a, cv.dp, s0, s1, C, st_area, &s_stage_bar, stage_ph));
         } else {
           nested_total += scan_sources<V, LP1, KP1MAX, TRAIN, TS, true, TS, WT, CX>(
               a, x, s0 + warp, s1, kWarps, s_tgt + lane, s_int + lane, best, colv, SrcView<V>{},
