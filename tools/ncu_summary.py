@@ -26,6 +26,38 @@ METRICS = [
 ]
 
 
+def stall_top(report, n=8):
+    """Top warp-stall reasons (pc sampling) of the first kernel in the report."""
+    out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, r = rows[0], rows[2]
+    pre = "smsp__pcsamp_warps_issue_stalled_"
+    vals = []
+    for i, h in enumerate(hdr):
+        if h.startswith(pre) and not h.endswith("_not_issued"):
+            try:
+                vals.append((float(r[i].replace(",", "")), h[len(pre):]))
+            except ValueError:
+                pass
+    tot = sum(v for v, _ in vals) or 1.0
+    return [(k, v / tot * 100) for v, k in sorted(vals, reverse=True)[:n]]
+
+
+def clocks(path):
+    """nvidia-smi samples taken while ncu ran: SM clock under load, reasons."""
+    rows = list(csv.reader(open(path)))[1:]
+    load = [r for r in rows if len(r) > 6 and r[1].strip().split()[0].isdigit()
+            and int(r[1].strip().split()[0]) > 500]
+    if not load:
+        return None
+    sm = sorted(int(r[1].strip().split()[0]) for r in load)
+    mx = max(int(r[2].strip().split()[0]) for r in load)
+    reasons = sorted({r[6].strip() for r in load})
+    return {"samples_under_load": len(load), "sm_mhz_median": sm[len(sm) // 2],
+            "sm_mhz_min": sm[0], "sm_max_mhz": mx, "reason_masks": reasons}
+
+
 def raw(report):
     out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
@@ -68,7 +100,7 @@ def launches(path):
 
 def main():
     tag, report = sys.argv[1], sys.argv[2]
-    lpath = sys.argv[3] if len(sys.argv) > 3 else None
+    lpath = sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] else None
     workload = sys.argv[4] if len(sys.argv) > 4 else "C2"
     prof = raw(report)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
@@ -113,6 +145,17 @@ def main():
         json.dump(mdata, open(mj, "w"), indent=1)
         md.append(f"DRAM traffic per launch (read + write): **{traffic / 1e6:.2f} MB**.")
         md.append("")
+    if prof:
+        md += ["## Warp stall reasons (pc sampling, share of samples)", "",
+               "| reason | share |", "|---|---|"]
+        for k, v in stall_top(report):
+            md.append(f"| {k} | {v:.1f}% |")
+        md.append("")
+    cpath = report.replace(".ncu-rep", "_clocks.csv")
+    if os.path.exists(cpath):
+        c = clocks(cpath)
+        md += ["## Clock record (nvidia-smi every 200 ms while ncu ran; --clock-control none)", "",
+               f"`{json.dumps(c)}`", ""]
     if lpath:
         tot = launches(lpath)
         s = sum(v[0] for v in tot.values())
