@@ -938,6 +938,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   if (const char* e = std::getenv("DSG_GRADE")) grade = std::max(1, std::atoi(e));
   int grade1 = 3;  // mode 1: recent old levels chunked per level
   if (const char* e = std::getenv("DSG_GRADE1")) grade1 = std::max(0, std::atoi(e));
+  int64_t fin_fold_max = 32;  // mode 1: the finisher folds level s-2 up to this size
+  if (const char* e = std::getenv("DSG_FIN_FOLD")) fin_fold_max = std::max(0, std::atoi(e));
   unsigned poll_ns_max = 128;  // measured: 128 ns <= 256 ns (C1 -4 %, C3 -1 %, C4 -1 %, C2 =) and beats 1 us
   if (const char* e = std::getenv("DSG_CHUNK_LEN")) chunk_len0 = std::max(4, std::atoi(e));
   if (const char* e = std::getenv("DSG_CHUNK_LEN1")) chunk_len1 = std::max(4, std::atoi(e));
@@ -987,13 +989,17 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       const int64_t olen = oc ? (Rg + oc - 1) / oc : 1;
       for (int64_t c = 0; c < oc; ++c) chunk_lo.push_back(std::min(Rg, c * olen));
       chunks = oc;
-      for (int j = s - 1 - G1; j <= s - 2 && G1 > 0; ++j) {
+      // a small level s-2 is folded by the finisher itself (mode 2): no
+      // separate item — and no arrival round trip — between level s-2 and s
+      const bool fold2 = G1 >= 1 && lat.level_off[s - 1] - lat.level_off[s - 2] <= fin_fold_max;
+      if (fold2) pl.mode[s] = 2;
+      for (int j = s - 1 - G1; j <= (fold2 ? s - 3 : s - 2) && G1 > 0; ++j) {
         const int64_t lo = lat.level_off[j], n = lat.level_off[j + 1] - lo;
         const int64_t nc = (n + kTileTargets - 1) / kTileTargets, len = (n + nc - 1) / nc;
         for (int64_t c = 0; c < nc; ++c) chunk_lo.push_back(lo + c * len);
         chunks += nc;
       }
-      chunk_lo.push_back(R);
+      chunk_lo.push_back(fold2 ? lat.level_off[s - 2] : R);
       chunks += 1;
       pl.chunk_len[s] = 0;
     } else {
@@ -1193,6 +1199,9 @@ void reset_tables(DeviceCtx& ctx, const Prepared& P, Pipeline& pl) {
   cudaStream_t st = ctx.stream;
   const int vb = P.value_bits;
   CK(cudaMemsetAsync(pl.LL.pair_counter, 0, sizeof(unsigned long long), st));
+  // persistent: every row PENDING until final (narrow-level items poll the
+  // cells they read instead of a level counter), then the empty ideal's row
+  if (pl.persistent) launch_fill_pending(vb, pl.LL.dp, pl.I * P.C, st);
   launch_init_empty(vb, P.K, P.L, pl.LL.dp, st);
   if (pl.persistent) {
     CK(cudaMemsetAsync(pl.PP.tile_count, 0, sizeof(unsigned) * (pl.total_tiles + 1), st));
@@ -1203,6 +1212,7 @@ void reset_tables(DeviceCtx& ctx, const Prepared& P, Pipeline& pl) {
     // virtual ranks 1..world-1: the same per-rank reset every GPU does
     for (size_t r = 1; pl.virt && r < pl.vranks.size(); ++r) {
       const VRank& v = pl.vranks[r];
+      launch_fill_pending(vb, v.dp, pl.I * P.C, st);
       launch_init_empty(vb, P.K, P.L, v.dp, st);
       CK(cudaMemsetAsync(v.tile_count, 0, sizeof(unsigned) * (pl.total_tiles + 1), st));
       CK(cudaMemsetAsync(v.ctl, 0, sizeof(unsigned) * pl.ctl_words, st));

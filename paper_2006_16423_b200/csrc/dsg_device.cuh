@@ -25,13 +25,18 @@ namespace dsg {
 
 template <typename V>
 struct VTraits;
+// INF: +infinity.  PENDING: a dp cell not yet final inside the persistent
+// kernel (tables are reset to it before every solve; no finite value can
+// reach it — the host bounds |values| below 2^30 / 2^62).
 template <>
 struct VTraits<int32_t> {
   static constexpr int32_t INF = 0x7fffffff;
+  static constexpr int32_t PENDING = (int32_t)0x80000000;
 };
 template <>
 struct VTraits<int64_t> {
   static constexpr int64_t INF = 0x7fffffffffffffffLL;
+  static constexpr int64_t PENDING = (int64_t)0x8000000000000000ULL;
 };
 
 constexpr int kMaxWords = 64;       // bitset words supported (4096 nodes)

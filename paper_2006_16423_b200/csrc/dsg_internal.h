@@ -262,6 +262,8 @@ void launch_init_empty(int value_bits, int K, int L, void* dp, cudaStream_t st);
 // *bad = 1 if the two tables differ anywhere (virtual-shard replicas)
 void launch_compare_tables(const void* a, const void* b, size_t bytes, int* bad, cudaStream_t st);
 void launch_fill_inf(int value_bits, void* p, int64_t n, cudaStream_t st);
+// dp cells -> VTraits<V>::PENDING (rows polled by narrow-level items)
+void launch_fill_pending(int value_bits, void* p, int64_t n, cudaStream_t st);
 void launch_level_of(const int64_t* level_off, int n_levels, int64_t I, int32_t* level_of,
                      cudaStream_t st);
 

@@ -71,7 +71,7 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
 __device__ __forceinline__ int item_key(const PersistPlan& p, const ItemBuild& b,
                                         const PairInfo& r) {
   const bool crit = r.s == r.dep + 1;
-  const int cls = crit ? ((p.mode[r.s] == 1 && r.c == p.n_chunks[r.s] - 1) ? 1 : 0)
+  const int cls = crit ? ((p.mode[r.s] != 0 && r.c == p.n_chunks[r.s] - 1) ? 1 : 0)
                        : (r.s == r.dep + 2 ? 2 : 3);
   if (!b.split) return 4 * r.bucket + cls;
   return crit ? 2 * r.bucket + cls : 2 * b.n_levels + 2 * r.bucket + (cls - 2);

@@ -260,6 +260,49 @@ __device__ bool wait_count(const PersistPlan& p, const CtaView& v, const unsigne
   return s_ok2 != 0;
 }
 
+template <typename V>
+__device__ __forceinline__ V ld_relaxed_v(const V* p);
+template <>
+__device__ __forceinline__ int32_t ld_relaxed_v<int32_t>(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ int64_t ld_relaxed_v<int64_t>(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// A dp cell read by a narrow-level item (mode 1, threads over cells): the
+// row is polled cell by cell until it is no longer PENDING instead of
+// waiting for the level counter — each cell is one aligned store, so a
+// non-PENDING value is final, and the producer's fence + counter release
+// are off the level-to-level chain.  On stop / watchdog: bail (INF).
+template <typename V>
+__device__ __forceinline__ V ld_final(const PersistPlan& p, const CtaView& cv, const V* q,
+                                      bool& bail) {
+  V v = __ldcg(q);
+  if (v != VTraits<V>::PENDING) return v;
+  unsigned ns = 32, polls = 0;
+  const uint64_t t0 = globaltimer();
+  while (true) {
+    __nanosleep(ns);
+    ns = ns < p.poll_ns_max ? ns * 2 : p.poll_ns_max;
+    v = ld_relaxed_v<V>(q);
+    if (v != VTraits<V>::PENDING) return v;
+    if ((++polls & 63) != 0) continue;
+    if (ld_relaxed_sys((const unsigned*)cv.stop) != 0) break;
+    if (globaltimer() - t0 > kWatchdogNs) {
+      raise_stop(p, cv, true);
+      break;
+    }
+  }
+  bail = true;
+  return VTraits<V>::INF;
+}
+
 // Level s gained n finished targets: release their rows, bump the level
 // counter on every rank (system scope when peers read it over NVLink).
 __device__ __forceinline__ void release_done(const PersistPlan& p, int s, unsigned n) {
@@ -667,7 +710,11 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
         }
       } else {
         const int64_t c0 = fin ? __ldg(a.cov_off + t) : s0;
-        const int64_t c1 = fin ? __ldg(a.cov_off + t + 1) : s1;
+        const int64_t ncov = fin ? __ldg(a.cov_off + t + 1) - c0 : 0;
+        // mode 2: the finisher also folds level s-2 (a short range)
+        const int64_t ex0 = (fin && mode == 2) ? p.level_off[s - 2] : 0;
+        const int64_t ex1 = (fin && mode == 2) ? p.level_off[s - 1] : 0;
+        const int64_t c1 = fin ? c0 + ncov + (ex1 - ex0) : s1;
         __shared__ int32_t f_src[kTileTargets];
         __shared__ V f_acc[kTileTargets], f_cpu[kTileTargets], f_mem[kTileTargets];
         __shared__ V f_part[kTileTargets];
@@ -680,7 +727,8 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
           const int G = C <= kTileTargets ? max(1, min(nb, kTileTargets / C)) : 1;
           const int my_g = C <= kTileTargets ? tid / C : 0, my_c = C <= kTileTargets ? tid % C : tid;
           if (tid < nb) {
-            const int64_t src = fin ? (int64_t)__ldg(a.cov + b0 + tid) : b0 + tid;
+            const int64_t j = b0 + tid;
+            const int64_t src = !fin ? j : (j - c0 < ncov ? (int64_t)__ldg(a.cov + j) : ex0 + (j - c0 - ncov));
             const PrePair<V> q = pre_pair<V, TRAIN, 1>(a, x, src, s_tgt, s_int);
             f_src[tid] = q.ok ? (int32_t)src : -1;
             f_acc[tid] = q.acc;
@@ -696,38 +744,65 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
               break;
             }
             for (int c = tid; c < C; c += kTileTargets) m_val[c] = fin ? __ldcg(key + c) : INF;
-            if (!wait_level(p, cv, item.w)) {  // rows below are read at L2
-              ok = false;
-              break;
-            }
+            // no level wait: the fold polls the source cells it reads
+            __syncthreads();
             tr1 = p.trace ? globaltimer() : 0;
           } else {
             __syncthreads();
           }
+          bool bail = false;
           for (int c = my_c; c < C && my_g < G; c += kTileTargets) {
             const int k = c / lp1, l = c % lp1;
             V v = INF;
-            for (int j = my_g; j < nb; j += G) {
-              const int32_t src = f_src[j];
-              if (src < 0) continue;
-              const V* row = dpm + (size_t)src * C;
-              const V acc = f_acc[j];
-              if (k >= 1 && acc != INF) {
-                if (kGeneric && a.repl) {
+            if (kGeneric && a.repl) {
+              for (int j = my_g; j < nb; j += G) {
+                const int32_t src = f_src[j];
+                if (src < 0) continue;
+                const V* row = dpm + (size_t)src * C;
+                const V acc = f_acc[j];
+                if (k >= 1 && acc != INF) {
                   for (int rr = 1; rr <= k; ++rr) {
                     const V load = rr == 1 ? acc : replicated<V>(a, acc, f_mem[j], rr);
-                    v = min(v, vmax(__ldcg(row + c - rr * lp1), load));
+                    v = min(v, vmax(ld_final(p, cv, row + c - rr * lp1, bail), load));
                   }
-                } else {
-                  v = min(v, vmax(__ldcg(row + c - lp1), acc));
+                }
+                if (l >= 1) v = min(v, vmax(ld_final(p, cv, row + c - 1, bail), f_cpu[j]));
+              }
+            } else {
+              // batches of up to 8 sources: every cell load of the batch is in
+              // flight at once (one L2 round trip), PENDING cells polled after
+              constexpr int kB = 8;
+              for (int j0 = my_g; j0 < nb; j0 += kB * G) {
+                V ra[kB], rc[kB];
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                  const int j = j0 + u * G;
+                  const int32_t src = j < nb ? f_src[j] : -1;
+                  const V* row = dpm + (size_t)(src < 0 ? 0 : src) * C;
+                  ra[u] = (src >= 0 && k >= 1 && f_acc[j] != INF) ? __ldcg(row + c - lp1) : INF;
+                  rc[u] = (src >= 0 && l >= 1) ? __ldcg(row + c - 1) : INF;
+                }
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                  const int j = j0 + u * G;
+                  if (j >= nb) break;
+                  const int32_t src = f_src[j];
+                  if (src < 0) continue;
+                  const V* row = dpm + (size_t)src * C;
+                  if (ra[u] == VTraits<V>::PENDING) ra[u] = ld_final(p, cv, row + c - lp1, bail);
+                  if (rc[u] == VTraits<V>::PENDING) rc[u] = ld_final(p, cv, row + c - 1, bail);
+                  if (k >= 1 && f_acc[j] != INF) v = min(v, vmax(ra[u], f_acc[j]));
+                  if (l >= 1) v = min(v, vmax(rc[u], f_cpu[j]));
                 }
               }
-              if (l >= 1) v = min(v, vmax(__ldcg(row + c - 1), f_cpu[j]));
             }
             if (G > 1) f_part[tid] = v;
             else m_val[c] = min(m_val[c], v);
           }
-          __syncthreads();
+          if (__syncthreads_or(bail)) {
+            ok = false;
+            break;
+          }
           if (G > 1) {
             for (int c = tid; c < C; c += kTileTargets) {
               V v = m_val[c];

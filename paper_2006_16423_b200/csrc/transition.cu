@@ -109,6 +109,13 @@ __global__ void fill_inf_kernel(V* p, int64_t n) {
     p[i] = VTraits<V>::INF;
 }
 
+template <typename V>
+__global__ void fill_pending_kernel(V* p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = VTraits<V>::PENDING;
+}
+
 __global__ void read_globaltimer_kernel(uint64_t* out) { *out = globaltimer(); }
 
 __global__ void compare_tables_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
@@ -408,6 +415,13 @@ void launch_init_empty(int value_bits, int K, int L, void* dp, cudaStream_t st) 
   const int C = (K + 1) * (L + 1);
   if (value_bits == 32) init_empty_kernel<int32_t><<<1, 128, 0, st>>>(C, (int32_t*)dp);
   else init_empty_kernel<int64_t><<<1, 128, 0, st>>>(C, (int64_t*)dp);
+  count_launch();
+}
+
+void launch_fill_pending(int value_bits, void* p, int64_t n, cudaStream_t st) {
+  const int blocks = (int)std::min<int64_t>(1024, (n + 255) / 256 + 1);
+  if (value_bits == 32) fill_pending_kernel<int32_t><<<blocks, 256, 0, st>>>((int32_t*)p, n);
+  else fill_pending_kernel<int64_t><<<blocks, 256, 0, st>>>((int64_t*)p, n);
   count_launch();
 }
 
