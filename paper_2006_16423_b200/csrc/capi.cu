@@ -728,6 +728,7 @@ struct Pipeline {
   // virtual shards (dsg_options::shard_count > 1): all `world` ranks run in
   // this process's one cooperative launch, each with its own tables
   bool virt = false;
+  std::vector<std::vector<int4>> run_lists;  // chain-runner items per (virtual) rank
   std::vector<VRank> vranks;  // host copy; [0] aliases the tables above
   VRank* vranks_d = nullptr;
   int* tables_bad = nullptr;  // replica comparison after the solve
@@ -940,6 +941,15 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   if (const char* e = std::getenv("DSG_GRADE1")) grade1 = std::max(0, std::atoi(e));
   int64_t fin_fold_max = 32;  // mode 1: the finisher folds level s-2 up to this size
   if (const char* e = std::getenv("DSG_FIN_FOLD")) fin_fold_max = std::max(0, std::atoi(e));
+  int runner_max_t = 4;  // chain runner: finishers of mode-1 levels with <= this many targets
+  if (const char* e = std::getenv("DSG_RUNNER_T")) runner_max_t = std::max(0, std::atoi(e));
+  int fold_levels = 1;  // measured on C4: folding s-3 too costs the finisher more than it saves
+  if (const char* e = std::getenv("DSG_FOLD_LEVELS")) fold_levels = std::max(0, std::atoi(e));
+  int runners = 16;  // runner CTAs per rank (C4: 16 < 8 < 4 runners in DP ms)
+  if (const char* e = std::getenv("DSG_RUNNERS")) runners = std::max(1, std::atoi(e));
+  // the runners' finishers wait for chunks only the other CTAs claim: keep
+  // the runner off unless most of the grid is left for them
+  if (!pl.persistent || pl.pinfo.blocks < 4 * runners * pl.world) runner_max_t = 0;
   unsigned poll_ns_max = 128;  // measured: 128 ns <= 256 ns (C1 -4 %, C3 -1 %, C4 -1 %, C2 =) and beats 1 us
   if (const char* e = std::getenv("DSG_CHUNK_LEN")) chunk_len0 = std::max(4, std::atoi(e));
   if (const char* e = std::getenv("DSG_CHUNK_LEN1")) chunk_len1 = std::max(4, std::atoi(e));
@@ -989,17 +999,21 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       const int64_t olen = oc ? (Rg + oc - 1) / oc : 1;
       for (int64_t c = 0; c < oc; ++c) chunk_lo.push_back(std::min(Rg, c * olen));
       chunks = oc;
-      // a small level s-2 is folded by the finisher itself (mode 2): no
-      // separate item — and no arrival round trip — between level s-2 and s
-      const bool fold2 = G1 >= 1 && lat.level_off[s - 1] - lat.level_off[s - 2] <= fin_fold_max;
-      if (fold2) pl.mode[s] = 2;
-      for (int j = s - 1 - G1; j <= (fold2 ? s - 3 : s - 2) && G1 > 0; ++j) {
+      // the F most recent old levels s-2 .. s-1-F, when small, are folded by
+      // the finisher itself (mode 1 + F): no separate items — and no arrival
+      // round trips — between those levels and level s
+      int F = 0;
+      while (F < std::min(G1, fold_levels) &&
+             lat.level_off[s - 1] - lat.level_off[s - 2 - F] <= fin_fold_max)
+        ++F;
+      pl.mode[s] = 1 + F;
+      for (int j = s - 1 - G1; j <= s - 2 - F && G1 > 0; ++j) {
         const int64_t lo = lat.level_off[j], n = lat.level_off[j + 1] - lo;
         const int64_t nc = (n + kTileTargets - 1) / kTileTargets, len = (n + nc - 1) / nc;
         for (int64_t c = 0; c < nc; ++c) chunk_lo.push_back(lo + c * len);
         chunks += nc;
       }
-      chunk_lo.push_back(fold2 ? lat.level_off[s - 2] : R);
+      chunk_lo.push_back(lat.level_off[s - 1 - F]);
       chunks += 1;
       pl.chunk_len[s] = 0;
     } else {
@@ -1059,6 +1073,10 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   {
     std::vector<int64_t> pair_off(lat.n_levels + 1, 0);
     for (int l = 1; l < lat.n_levels; ++l) pair_off[l + 1] = pair_off[l] + pl.n_chunks[l];
+    auto runner_level = [&](int l) {
+      return runner_max_t > 0 && pl.mode[l] != 0 &&
+             lat.level_off[l + 1] - lat.level_off[l] <= runner_max_t;
+    };
     auto items_of_rank = [&](int rank) {
       int64_t total = 0;
       for (int l = 1; l < lat.n_levels; ++l) {
@@ -1066,14 +1084,27 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
         const int64_t units = pl.mode[l] == 0 ? (T + 31) / 32 : T;
         const int64_t units_r =
             pl.world > 1 ? (units > rank ? (units - rank + pl.world - 1) / pl.world : 0) : units;
-        total += pl.n_chunks[l] * units_r;
+        total += (pl.n_chunks[l] - (runner_level(l) ? 1 : 0)) * units_r;
       }
       return total;
     };
+    // the chain runner's lists: the finishers of narrow mode-1 levels, in
+    // level order, per rank (units u % world == rank)
+    pl.run_lists.assign(pl.virt ? pl.world : 1, {});
+    for (size_t r = 0; r < pl.run_lists.size(); ++r) {
+      const int rank = pl.virt ? (int)r : pl.rank;
+      for (int l = 1; l < lat.n_levels; ++l) {
+        if (!runner_level(l)) continue;
+        const int64_t T = lat.level_off[l + 1] - lat.level_off[l];
+        for (int64_t u = pl.world > 1 ? rank : 0; u < T; u += pl.world)
+          pl.run_lists[r].push_back(make_int4(l, (int)u, (int)(pl.n_chunks[l] - 1), l - 1));
+      }
+    }
     for (size_t r = 0; r < rank_items.size(); ++r)
       rank_items[r] = items_of_rank(pl.virt ? (int)r : pl.rank);
     pl.total_items = rank_items[0];
     ItemBuild B{};
+    B.runner_max_t = runner_max_t;
     B.lag = 1 << 30;
     if (const char* e = std::getenv("DSG_SCHED_LAG")) B.lag = std::max(1, std::atoi(e));
     // dedicated cover-item CTAs (needs >= 2 CTAs: one of each role; one
@@ -1108,6 +1139,18 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.keys = ctx.get_t<unsigned long long>(pfx + "pp.keys", (size_t)I * C);  // value atomics
   PP.virt = 0;
   PP.vrank = nullptr;
+  PP.runner_max_t = runner_max_t;
+  PP.runners = runners;
+  auto upload_run = [&](const std::string& name, const std::vector<int4>& v) {
+    int4* d = ctx.get_t<int4>(name, v.size() + 1);
+    if (!v.empty()) {
+      CK(cudaMemcpyAsync(d, v.data(), sizeof(int4) * v.size(), cudaMemcpyHostToDevice, st));
+      ctx.h2d_bytes += (int64_t)(sizeof(int4) * v.size());
+    }
+    return d;
+  };
+  PP.run_items = upload_run(pfx + "pp.run_items", pl.run_lists[0]);
+  PP.run_total = (int64_t)pl.run_lists[0].size();
   {
     int32_t* mode_d = ctx.get_t<int32_t>(pfx + "pp.mode", pl.mode.size());
     CK(cudaMemcpyAsync(mode_d, pl.mode.data(), sizeof(int32_t) * pl.mode.size(),
@@ -1117,7 +1160,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     if (pl.virt) {
       // virtual ranks 1..world-1: everything a rank owns on its own GPU
       pl.vranks.assign(pl.world, VRank{});
-      pl.vranks[0] = VRank{PP.items, pl.total_items, pl.ctl, PP.tile_count, PP.keys, LL.dp};
+      pl.vranks[0] = VRank{PP.items, pl.total_items, pl.ctl, PP.tile_count, PP.keys, LL.dp,
+                           PP.run_items, PP.run_total};
       for (int r = 1; r < pl.world; ++r) {
         const std::string vp = pfx + "v" + std::to_string(r) + ".";
         ItemBuild B = pl.item_build;
@@ -1131,6 +1175,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
         v.tile_count = ctx.get_t<unsigned>(vp + "tile_count", (size_t)pl.total_tiles + 1);
         v.keys = ctx.get_t<unsigned long long>(vp + "keys", (size_t)I * C);
         v.dp = ctx.get(vp + "dp", (size_t)I * C * vsz + 64);
+        v.run_items = upload_run(vp + "run_items", pl.run_lists[r]);
+        v.run_total = (int64_t)pl.run_lists[r].size();
       }
       pl.peer_dp.assign(pl.world, nullptr);
       pl.peer_bp.assign(pl.world, nullptr);
@@ -1174,17 +1220,18 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
 
 void write_trace(DeviceCtx& ctx, const Pipeline& pl, const char* path) {
   // debug trace (DSG_TRACE_FILE): header, per-level plan, per-item timestamps
-  std::vector<uint64_t> tr((size_t)pl.total_items * 4);
+  std::vector<uint64_t> tr((size_t)(pl.total_items + pl.PP.run_total) * 4);
   CK(cudaMemcpyAsync(tr.data(), pl.PP.trace, sizeof(uint64_t) * tr.size(), cudaMemcpyDeviceToHost,
                      ctx.stream));
   CK(cudaStreamSynchronize(ctx.stream));
   if (FILE* f = std::fopen(path, "wb")) {
-    int64_t hdr[4] = {pl.lat.n_levels, pl.total_items, pl.pinfo.blocks, pl.rank};
+    int64_t hdr[4] = {pl.lat.n_levels, pl.total_items + pl.PP.run_total, pl.pinfo.blocks, pl.rank};
     std::fwrite(hdr, sizeof hdr, 1, f);
     std::fwrite(pl.lat.level_off.data(), sizeof(int64_t), pl.lat.level_off.size(), f);
     std::fwrite(pl.item_base.data(), sizeof(int64_t), pl.item_base.size(), f);
     std::vector<int4> items((size_t)pl.total_items);
     CK(cudaMemcpy(items.data(), pl.items_d, sizeof(int4) * items.size(), cudaMemcpyDeviceToHost));
+    items.insert(items.end(), pl.run_lists[0].begin(), pl.run_lists[0].end());
     std::fwrite(items.data(), sizeof(int4), items.size(), f);
     std::fwrite(pl.n_chunks.data(), sizeof(int64_t), pl.n_chunks.size(), f);
     std::vector<int64_t> m64(pl.mode.begin(), pl.mode.end());
@@ -1259,8 +1306,9 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
     const char* trace_file = std::getenv("DSG_TRACE_FILE");
     PP.trace = nullptr;
     if (trace_file && *trace_file) {
-      PP.trace = ctx.get_t<uint64_t>(pl.pfx + "pp.trace", (size_t)pl.total_items * 4);
-      CK(cudaMemsetAsync(PP.trace, 0, sizeof(uint64_t) * pl.total_items * 4, st));
+      const size_t n_tr = (size_t)(pl.total_items + PP.run_total) * 4;
+      PP.trace = ctx.get_t<uint64_t>(pl.pfx + "pp.trace", n_tr);
+      CK(cudaMemsetAsync(PP.trace, 0, sizeof(uint64_t) * n_tr, st));
     }
     CK(cudaEventRecord(ev_desc, st));
     launch_persistent(LL, PP, st, &pl.pinfo);

@@ -171,6 +171,8 @@ struct VRank {
   unsigned* tile_count;       // arrival counters of this rank's units
   unsigned long long* keys;   // merge keys of this rank's targets
   void* dp;                   // this rank's replica of the dp table (read by its CTAs)
+  const int4* run_items;      // the rank's chain-runner items (finishers, level order)
+  int64_t run_total;
 };
 
 // One cooperative launch for all levels (transition.cu).
@@ -228,6 +230,16 @@ struct PersistPlan {
   // one GPU); CTA b is rank b % world and takes its tables from vrank[rank]
   int virt;
   const VRank* vrank;          // [world]
+  // Chain runner: one CTA per rank (blockIdx.x == rank, or 0) first runs the
+  // finishers of the narrow mode-1 levels in level order from its own list —
+  // no claims, no queueing behind other items on the level-to-level chain —
+  // then joins the shared queue.  run_items / run_total: this launch's own
+  // rank (virtual ranks: VRank::run_items).
+  int runner_max_t;
+  int runners;               // CTAs per rank sharing the run list round-robin, so each
+                             // prepares its next finisher while the chain advances
+  const int4* run_items;
+  int64_t run_total;
 };
 
 struct PersistInfo {
@@ -242,6 +254,8 @@ struct PersistInfo {
 // = dep + 1) first inside each bucket.
 struct ItemBuild {
   int n_levels;
+  int runner_max_t;          // > 0: finishers of mode-1 levels with <= this many
+                             // targets go to the chain runner, not the list
   int lag;                   // list bucket = max(dep, s - lag)
   int split;                 // cover items in their own queue at the front
   const int64_t* pair_off;   // [n_levels + 1] prefix of chunks over levels

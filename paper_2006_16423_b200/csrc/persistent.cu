@@ -56,6 +56,9 @@ __device__ PairInfo pair_info(const PersistPlan& p, const ItemBuild& b, int64_t 
   // near-term work and the critical items are not queued behind the future
   r.bucket = max(r.dep, lo - b.lag);
   r.n_items = r.units_r;
+  // the chain runner's finishers are not listed (capi.cu builds its list)
+  if (b.runner_max_t > 0 && mode != 0 && r.c == p.n_chunks[lo] - 1 && T <= b.runner_max_t)
+    r.n_items = 0;
   return r;
 }
 

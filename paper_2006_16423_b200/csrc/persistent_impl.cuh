@@ -174,6 +174,9 @@ struct CtaView {
   unsigned* done;
   int* stop;
   int rank;
+  const int4* run_items;  // chain-runner items of this rank: this runner CTA takes
+  int64_t run_total;      //   run_first, run_first + run_step, ... < run_total
+  int run_first, run_step;
 };
 
 // Stop every rank (deadline, watchdog): a peer spinning on a level the
@@ -487,6 +490,12 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       cv.done = vr.ctl + 32;
       cv.stop = reinterpret_cast<int*>(vr.ctl);
       cv.rank = r;
+      cv.run_items = vr.run_items;
+      // CTAs r, r + world, ... (the first `runners`) run rank r's chain
+      const int ri = (int)(blockIdx.x / (unsigned)p.world);
+      cv.run_total = ri < p.runners ? vr.run_total : 0;
+      cv.run_first = ri;
+      cv.run_step = p.runners;
     } else {
       cv.items = p.items;
       cv.total_items = p.total_items;
@@ -497,6 +506,10 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       cv.done = p.done;
       cv.stop = p.stop;
       cv.rank = p.rank;
+      cv.run_items = p.run_items;
+      cv.run_total = (int)blockIdx.x < p.runners ? p.run_total : 0;
+      cv.run_first = (int)blockIdx.x;
+      cv.run_step = p.runners;
     }
   }
   __syncthreads();
@@ -511,8 +524,14 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
   unsigned long long* ctr = crit_role ? p.crit_next : cv.next;
   const int64_t q_lo = crit_role ? 0 : n_crit, q_hi = crit_role ? n_crit : cv.total_items;
   __shared__ long long s_gi;
+  // the chain runner first takes its own items (gi < 0: run item -gi-1)
+  // next run item of this CTA (gi = -(index + 1)); in shared memory, not a
+  // register live across the scan loop
+  __shared__ long long s_run_pos;
   if (tid == 0) {
-    s_gi = q_lo + (long long)atomicAdd(ctr, 1ull);
+    const long long rp = cv.run_first;
+    s_gi = rp < cv.run_total ? -(1 + rp) : q_lo + (long long)atomicAdd(ctr, 1ull);
+    s_run_pos = rp + cv.run_step;
     s_any_last = 0;
   }
   __syncthreads();
@@ -520,10 +539,21 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
   while (true) {
     const int64_t gi = s_gi;
     if (gi >= q_hi) break;
-    const int4 item = __ldg(cv.items + gi);
-    // claim the next item now; its latency hides behind this one
-    unsigned long long next_gi = 0;
-    if (tid == 0) next_gi = q_lo + atomicAdd(ctr, 1ull);
+    const int4 item = gi < 0 ? __ldg(cv.run_items + (-gi - 1)) : __ldg(cv.items + gi);
+    // claim the next item now; its latency hides behind this one (the
+    // runner's own items need no claim)
+    // — but the runner claims its first shared item only after its last own
+    // item: holding a claimed item while blocked on the chain could hold
+    // exactly the chunk that chain waits for
+    // (kept in shared memory: no registers live across the scan)
+    __shared__ long long s_next_gi;
+    if (tid == 0) {
+      const long long rp = s_run_pos;
+      s_next_gi = rp < cv.run_total ? -(1 + rp)
+                  : gi < 0         ? LLONG_MIN
+                                   : (long long)(q_lo + atomicAdd(ctr, 1ull));
+      if (rp < cv.run_total) s_run_pos = rp + cv.run_step;
+    }
     const int s = item.x;
     const int64_t unit = item.y;
     const int64_t chunk = item.z;
@@ -711,9 +741,10 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       } else {
         const int64_t c0 = fin ? __ldg(a.cov_off + t) : s0;
         const int64_t ncov = fin ? __ldg(a.cov_off + t + 1) - c0 : 0;
-        // mode 2: the finisher also folds level s-2 (a short range)
-        const int64_t ex0 = (fin && mode == 2) ? p.level_off[s - 2] : 0;
-        const int64_t ex1 = (fin && mode == 2) ? p.level_off[s - 1] : 0;
+        // mode 1 + F: the finisher also folds the F levels s-2 .. s-1-F
+        // (one short ordinal range)
+        const int64_t ex0 = (fin && mode > 1) ? p.level_off[s - mode] : 0;
+        const int64_t ex1 = (fin && mode > 1) ? p.level_off[s - 1] : 0;
         const int64_t c1 = fin ? c0 + ncov + (ex1 - ex0) : s1;
         __shared__ int32_t f_src[kTileTargets];
         __shared__ V f_acc[kTileTargets], f_cpu[kTileTargets], f_mem[kTileTargets];
@@ -847,15 +878,19 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
     }
     __syncthreads();
     const uint64_t tr2 = p.trace ? globaltimer() : 0;
-    if (p.trace && tid == 0) {
-      uint64_t* tr = p.trace + gi * 4;
+    if (p.trace && tid == 0) {  // runner items after the list's
+      const long long g = s_gi;
+      uint64_t* tr = p.trace + (g >= 0 ? g : cv.total_items + (-g - 1)) * 4;
       tr[0] = tr0;
       tr[1] = tr1;
       tr[2] = tr2;
       tr[3] = globaltimer() | (s_any_last ? (1ull << 63) : 0ull);
     }
     if (tid == 0) s_any_last = 0;
-    if (tid == 0) s_gi = (long long)next_gi;
+    if (tid == 0) {
+      const long long ng = s_next_gi;
+      s_gi = ng == LLONG_MIN ? (long long)(q_lo + atomicAdd(ctr, 1ull)) : ng;
+    }
     __syncthreads();
   }
   for (int off = 16; off > 0; off >>= 1)
