@@ -889,6 +889,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   LL.dp = ctx.get(pfx + "dp.values", (size_t)I * C * vsz + 64);  // + staging slack
   LL.bp = nullptr;  // values only; the traceback re-derives the argmins
   LL.pair_counter = ctx.get_t<unsigned long long>(pfx + "dp.pairs", 1);
+  LL.stats = ctx.get_t<unsigned long long>(pfx + "dp.stats", 8);
 
   // ---- chunk plan
   pl.pinfo = PersistInfo{};
@@ -1246,6 +1247,7 @@ void reset_tables(DeviceCtx& ctx, const Prepared& P, Pipeline& pl) {
   cudaStream_t st = ctx.stream;
   const int vb = P.value_bits;
   CK(cudaMemsetAsync(pl.LL.pair_counter, 0, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(pl.LL.stats, 0, 8 * sizeof(unsigned long long), st));
   // persistent: every row PENDING until final (narrow-level items poll the
   // cells they read instead of a level counter), then the empty ideal's row
   if (pl.persistent) launch_fill_pending(vb, pl.LL.dp, pl.I * P.C, st);
@@ -1381,6 +1383,15 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
   // ---- traceback (rank 0 of a sharded run holds every row)
   unsigned long long pairs = 0;
   D2H(&pairs, LL.pair_counter, sizeof pairs);
+#ifdef DSG_PAIR_STATS
+  {
+    unsigned long long sv[4];
+    CK(cudaMemcpyAsync(sv, LL.stats, sizeof sv, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "DSG_PAIR_STATS {\"count_only\": %llu, \"candidate_test_dropped\": %llu, "
+                 "\"frontier_walks\": %llu, \"minmax_updates\": %llu}\n", sv[0], sv[1], sv[2], sv[3]);
+  }
+#endif
   const bool do_traceback = pl.rank == 0;
   const int maxb = K + Lc + 1;
   TraceState tb{};

@@ -157,6 +157,10 @@ struct LevelLaunch {
   void* part_val;             // V[n_chunks][C][T]
   int32_t* part_arg;
   unsigned long long* pair_counter;
+  // DSG_PAIR_STATS builds only: [0] pairs counted in count-only chunks,
+  // [1] nested pairs dropped by the per-pair candidate test, [2] pairs whose
+  // frontier walk (block cost) ran, [3] pairs whose min-max update ran
+  unsigned long long* stats;
 };
 
 void launch_transition(const LevelLaunch& L, cudaStream_t st);

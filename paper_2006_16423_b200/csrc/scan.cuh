@@ -31,6 +31,13 @@
 namespace dsg {
 namespace scan {
 
+// DSG_PAIR_STATS (a separate diagnostic build): where the nested pairs go
+#ifdef DSG_PAIR_STATS
+#define DSG_STAT(a, k, n) atomicAdd((a).stats + (k), (unsigned long long)(n))
+#else
+#define DSG_STAT(a, k, n) ((void)0)
+#endif
+
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -301,7 +308,10 @@ __device__ __forceinline__ bool pair_cost(const LevelLaunch& a, const Target<V>&
   bool acc_ok = a.K > 0 && (x.un - r.unsup) == 0;
   if (acc_ok && a.memcheck) acc_ok = !(mem_blk > (V)a.mlim);
   const V proc = (V)(x.acc - (V)r.acc);
-  if (acc_ok && need(proc)) acc = acc_block_cost<V, TRAIN, TS>(a, s, r, proc, x, tA, tInt);
+  if (acc_ok && need(proc)) {
+    acc = acc_block_cost<V, TRAIN, TS>(a, s, r, proc, x, tA, tInt);
+    DSG_STAT(a, 2, 1);
+  }
   return true;
 }
 
@@ -466,12 +476,16 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
       if (a.memcheck) cand = cand && !((V)(x.mem - rmem) > (V)a.mlim);
       if (UNIFORM && !__any_sync(0xffffffffu, cand)) {
         nested_cnt += nested ? 1u : 0u;
+        if (nested) DSG_STAT(a, 1, 1);
         continue;
       }
     }
     if (!nested) continue;
     ++nested_cnt;
-    if (!cand) continue;
+    if (!cand) {
+      DSG_STAT(a, 1, 1);
+      continue;
+    }
     bool gated;
     V acc, cpu, mem_blk;
     const V* sdp = STAGED ? sv.dp + (size_t)(s - sv.base) * C : dp + (size_t)s * C;
@@ -496,6 +510,7 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
                                                     AlwaysNeeded(), sv.rec + (s - sv.base));
     }
     if (gated) continue;
+    DSG_STAT(a, 3, 1);
     k4_update<V, LP1, KP1MAX, CS, CX, STAGED>(a, sdp, row, acc, cpu, mem_blk, best, colv);
     if constexpr (kAccOnly) {
       maxbest = NEG;
@@ -576,6 +591,7 @@ __device__ __forceinline__ unsigned count_nested(const LevelLaunch& a, bool acti
       n += stray == 0ull ? 1u : 0u;
     }
   }
+  DSG_STAT(a, 0, n);
   return n;
 }
 
