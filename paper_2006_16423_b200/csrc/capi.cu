@@ -647,12 +647,24 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
       L.table_cap = tc;
     }
     CK(cudaMemsetAsync(st_d, 0, sizeof(EnumStatus), ctx.stream));
+    L.resume = 0;
     launch_enumerate(L, ctx.stream);
     CK(cudaGetLastError());
     debug_sync(ctx, "enumerate");
     EnumStatus st;
     D2H(&st, st_d, sizeof st);
     CK(cudaStreamSynchronize(ctx.stream));
+    if (st.code == 4) {
+      // a level wider than one CTA's frontier: the cluster walk continues
+      // from it (enumerate.cu enumerate_cluster_kernel)
+      CK(cudaMemsetAsync(&st_d->code, 0, sizeof(int32_t), ctx.stream));
+      L.resume = 1;
+      launch_enumerate(L, ctx.stream);
+      CK(cudaGetLastError());
+      debug_sync(ctx, "enumerate (cluster)");
+      D2H(&st, st_d, sizeof st);
+      CK(cudaStreamSynchronize(ctx.stream));
+    }
     if (st.code == 1) throw Fail{DSG_BUDGET, "ideal budget exceeded", budget};
     if (st.code == 2) {
       cap = std::min<int64_t>(budget_eff + 1, std::max(cap * 2, st.needed + st.needed / 2));

@@ -13,10 +13,13 @@ void count_launch();  // kernels launched by this library (bench evidence)
 
 // ---------------------------------------------------------------- K1
 struct EnumStatus {
-  int32_t code;      // 0 ok, 1 budget exceeded, 2 capacity, 3 candidate capacity
+  int32_t code;      // 0 ok, 1 budget exceeded, 2 capacity, 3 candidate capacity,
+                     // 4 a level wider than one CTA's frontier: resume on a cluster
   int32_t n_levels;
   int64_t total;
   int64_t needed;
+  int64_t resume_lo, resume_hi;  // code 4: the level [lo, hi) to expand next
+  int64_t resume_level;
 };
 
 struct EnumLaunch {
@@ -46,6 +49,7 @@ struct EnumLaunch {
   int64_t cand_cap;
   int64_t* table;
   int64_t table_cap;
+  int resume;        // 1: continue from status->resume_* on the cluster kernel
 };
 
 void launch_enumerate(const EnumLaunch& L, cudaStream_t st);

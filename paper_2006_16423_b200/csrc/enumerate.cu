@@ -120,6 +120,8 @@ struct EnumArgs {
   int64_t cand_cap;
   int64_t* table;      // [table_cap] candidate index or -1
   int64_t table_cap;
+  int cluster_ok;      // stop at the first level wider than one CTA's frontier (code 4)
+  int resume;          // cluster kernel: continue from status->resume_*
 };
 
 // Resident modes: the frontier (parents and children, bits / maximal /
@@ -576,6 +578,18 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs
         lo = s_lo;
         hi = s_hi;
         level = s_level;
+      } else if (a.cluster_ok && nP > cta_cap(W)) {
+        // a level wider than the shared frontier: the cluster kernel takes
+        // over from here (launch_enumerate / capi.cu enumerate_device)
+        if (tid == 0) {
+          a.status->code = 4;
+          a.status->resume_lo = lo;
+          a.status->resume_hi = hi;
+          a.status->resume_level = level;
+          s_stop = 1;
+        }
+        __syncthreads();
+        break;
       } else if (a.csr_in_smem && nP <= cta_cap(W)) {
         // every thread runs the same control flow on shared counters, so
         // (lo, hi, level) stay identical across the CTA
@@ -664,6 +678,276 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs
   if (tid == 0 && a.status->code == 0 && !s_stop) {
     a.status->total = hi;
     a.status->n_levels = level;  // levels 0..level-1 are non-empty
+  }
+}
+
+// ---- the level walk spread over a thread-block cluster -----------------
+//
+// Wide levels are where the single-CTA walk is issue-bound (C2: ~3.5 us per
+// level at IPC 1.9 on one SM).  Here a cluster of kClusterCTAs CTAs walks the
+// levels together: CTA r expands parents [lo + r*len, lo + (r+1)*len) of the
+// level, each canonical child is built in full by the thread that found it
+// (no intra-level barrier), the children take contiguous slots after a
+// per-CTA count + block scan + one DSMEM atomicAdd on CTA 0's counter, and
+// ONE cluster barrier (release / acquire: the new rows, written through
+// global memory, are then visible to every CTA) ends the level.  Tiny levels
+// stay with warp 0 of CTA 0 (expand_resident<32>, frontier in its shared
+// memory) while the other CTAs wait at the barrier.
+constexpr int kClusterCTAs = 8;
+
+__device__ __forceinline__ bool canonical_child(const EnumArgs& a, const Adj& g,
+                                                const uint64_t* M, int x, uint64_t mx, int upper,
+                                                int v) {
+  const int above = upper + __popcll(mx & above_mask(v, x));
+  if (!above) return true;
+  int covered = 0;
+  const int p1 = g.pu_off[v + 1];
+  for (int e = g.pu_off[v]; e < p1; ++e) {
+    const int u = g.pu_adj[e];
+    covered += (u > v && bit_of(M, u)) ? 1 : 0;
+  }
+  return covered == above;
+}
+
+// Child J ∪ {v} of parent `par` (all rows in global memory), written to slot.
+__device__ __forceinline__ void build_child(const EnumArgs& a, const Adj& g, int64_t par, int v,
+                                            int64_t slot, int level) {
+  const int W = a.W;
+  const uint64_t* J = a.bits + (size_t)par * W;
+  const uint64_t* PM = a.maxm + (size_t)par * W;
+  const uint64_t* PA = a.addm + (size_t)par * W;
+  const uint64_t* pv = a.pred_u + (size_t)v * W;
+  const int vw = v >> 6;
+  const uint64_t vb = 1ull << (v & 63);
+  for (int x = 0; x < W; ++x) {
+    const uint64_t bx = x == vw ? vb : 0ull;
+    a.bits[(size_t)slot * W + x] = J[x] | bx;
+    a.maxm[(size_t)slot * W + x] = (PM[x] & ~__ldg(pv + x)) | bx;
+  }
+  uint64_t* CA = a.addm + (size_t)slot * W;
+  for (int x = 0; x < W; ++x) CA[x] = PA[x] & ~(x == vw ? vb : 0ull);
+  // successors of v that become addable: all their preds inside J ∪ {v}
+  const int s1 = g.su_off[v + 1];
+  for (int e = g.su_off[v]; e < s1; ++e) {
+    const int y = g.su_adj[e];
+    bool ok = true;
+    const int f1 = g.pu_off[y + 1];
+    for (int f = g.pu_off[y]; f < f1 && ok; ++f) {
+      const int u = g.pu_adj[f];
+      ok = u == v || bit_of(J, u);
+    }
+    if (ok) CA[y >> 6] |= 1ull << (y & 63);
+  }
+  a.level_of[slot] = level + 1;
+}
+
+// One level [lo, hi) across the cluster: returns this CTA's children count
+// base slot (after the DSMEM claim); children are written at base + k.
+__device__ __forceinline__ void expand_slice(const EnumArgs& a, const Adj& g, int64_t plo,
+                                             int64_t phi, int level, int64_t level_end,
+                                             unsigned long long* ctr0, int* s_scan,
+                                             unsigned long long* s_base) {
+  const int W = a.W;
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int64_t nP = phi - plo;
+  // pass 1: count this thread's canonical children over (parent, word) items
+  int mine = 0;
+  for (int64_t it = tid; it < nP * W; it += nt) {
+    const int64_t i = it / W;
+    const int x = (int)(it % W);
+    const size_t row = (size_t)(plo + i) * W;
+    uint64_t cand = a.addm[row + x];
+    if (!cand) continue;
+    const uint64_t* M = a.maxm + row;
+    int upper = 0;
+    for (int y = x + 1; y < W; ++y) upper += __popcll(M[y]);
+    const uint64_t mx = M[x];
+    for (; cand; cand &= cand - 1) {
+      const int v = (x << 6) | (__ffsll((long long)cand) - 1);
+      mine += canonical_child(a, g, M, x, mx, upper, v) ? 1 : 0;
+    }
+  }
+  // block exclusive scan of the counts, one DSMEM claim for the CTA
+  const int lane = tid & 31, warp = tid >> 5;
+  int incl = mine;
+  for (int off = 1; off < 32; off <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += t;
+  }
+  if (lane == 31) s_scan[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (nt >> 5) ? s_scan[lane] : 0;
+    int wi = w;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += t;
+    }
+    s_scan[lane] = wi - w;  // exclusive over warps
+    if (lane == 31) *s_base = atomicAdd(ctr0, (unsigned long long)wi);  // CTA total
+  }
+  __syncthreads();
+  int64_t slot = level_end + (int64_t)*s_base + s_scan[warp] + (incl - mine);
+  // pass 2: the same candidates, now written
+  for (int64_t it = tid; it < nP * W; it += nt) {
+    const int64_t i = it / W;
+    const int x = (int)(it % W);
+    const size_t row = (size_t)(plo + i) * W;
+    uint64_t cand = a.addm[row + x];
+    if (!cand) continue;
+    const uint64_t* M = a.maxm + row;
+    int upper = 0;
+    for (int y = x + 1; y < W; ++y) upper += __popcll(M[y]);
+    const uint64_t mx = M[x];
+    for (; cand; cand &= cand - 1) {
+      const int v = (x << 6) | (__ffsll((long long)cand) - 1);
+      if (!canonical_child(a, g, M, x, mx, upper, v)) continue;
+      if (slot < a.cap) build_child(a, g, plo + i, v, slot, level);
+      ++slot;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kEnumThreads) enumerate_cluster_kernel(EnumArgs a) {
+  namespace cgc = cooperative_groups;
+  cgc::cluster_group cluster = cgc::this_cluster();
+  const unsigned crank = cluster.block_rank();
+  const int W = a.W;
+  extern __shared__ uint64_t s_dyn[];
+  __shared__ unsigned long long s_ctr[3];  // CTA 0's: children of level L in s_ctr[L % 3]
+  __shared__ unsigned long long s_next;
+  __shared__ int s_nc[2];
+  __shared__ int s_scan[32];
+  __shared__ unsigned long long s_base;
+  __shared__ long long s_state[4];  // CTA 0 after a warp-mode run: lo, hi, level, status
+  const int tid = threadIdx.x;
+
+  // adjacency lists in shared memory (each CTA its own copy)
+  int32_t* c = reinterpret_cast<int32_t*>(s_dyn + enum_warp_bytes(W) / sizeof(uint64_t));
+  int32_t* pu_off = c;
+  int32_t* su_off = pu_off + (a.n + 1);
+  int32_t* pu_adj = su_off + (a.n + 1);
+  int32_t* su_adj = pu_adj + a.n_pu;
+  for (int i = tid; i <= a.n; i += blockDim.x) {
+    pu_off[i] = a.pu_off[i];
+    su_off[i] = a.su_off[i];
+  }
+  for (int i = tid; i < a.n_pu; i += blockDim.x) pu_adj[i] = a.pu_adj[i];
+  for (int i = tid; i < a.n_su; i += blockDim.x) su_adj[i] = a.su_adj[i];
+  const Adj adj{pu_off, pu_adj, su_off, su_adj};
+  if (tid < 3) s_ctr[tid] = 0;
+  if (crank == 0 && !a.resume) {
+    // the empty ideal, ideals.cpp:23-24
+    for (int w = tid; w < W; w += blockDim.x) {
+      a.bits[w] = 0;
+      a.maxm[w] = 0;
+      a.addm[w] = 0;
+    }
+    __syncthreads();
+    for (int v = tid; v < a.n; v += blockDim.x) {
+      if (!a.in_universe[v]) continue;
+      bool root = true;
+      for (int w = 0; w < W; ++w) root &= a.pred_u[(size_t)v * W + w] == 0ull;
+      if (root) atomicOr((unsigned long long*)&a.addm[v >> 6], 1ull << (v & 63));
+    }
+    if (tid == 0) {
+      a.level_of[0] = 0;
+      a.level_off[0] = 0;
+      a.level_off[1] = 1;
+    }
+  }
+  cluster.sync();
+  unsigned long long* ctr0 = cluster.map_shared_rank(s_ctr, 0);
+  long long* state0 = cluster.map_shared_rank(s_state, 0);
+
+  int64_t lo = a.resume ? a.status->resume_lo : 0, hi = a.resume ? a.status->resume_hi : 1;
+  int level = a.resume ? (int)a.status->resume_level : 0;
+  int status = 0;  // 1 budget, 2 capacity
+  while (hi > lo) {
+    const int64_t nP = hi - lo;
+    if (nP <= cta_cap(W)) {
+      // CTA 0 alone walks levels up to its shared frontier capacity — tiny
+      // ones with warp 0, the others with the whole CTA — level after level
+      // with the frontier in its shared memory, until a wide level (or the
+      // end); the other CTAs wait at the barrier
+      if (crank == 0) {
+        while (hi > lo && hi - lo <= cta_cap(W)) {
+          const int64_t np = hi - lo;
+          if (tid == 0) s_next = (unsigned long long)hi;
+          __syncthreads();
+          if (np <= small_cap(W) && np * W <= a.warp_items) {
+            if (tid < 32) {
+              expand_resident<32>(a, &lo, &hi, &level, &s_next, s_dyn, s_nc);
+              if (tid == 0) {
+                s_state[0] = lo;
+                s_state[1] = hi;
+                s_state[2] = level;
+              }
+            }
+            __syncthreads();
+            lo = s_state[0];
+            hi = s_state[1];
+            level = (int)s_state[2];
+          } else {
+            expand_resident<kEnumThreads>(a, &lo, &hi, &level, &s_next, s_dyn, s_nc);
+          }
+          __syncthreads();
+          const int64_t new_hi = (int64_t)s_next;
+          if (new_hi > a.budget || new_hi > a.cap) {
+            if (tid == 0) {
+              a.status->code = new_hi > a.budget ? 1 : 2;
+              a.status->needed = new_hi;
+            }
+            status = 1;
+            break;
+          }
+          lo = hi;
+          hi = new_hi;
+          ++level;
+          if (tid == 0 && hi > lo) a.level_off[level + 1] = hi;
+          __syncthreads();
+        }
+        if (tid == 0) {
+          s_state[0] = lo;
+          s_state[1] = hi;
+          s_state[2] = level;
+          s_state[3] = status;
+          s_ctr[level % 3] = 0;  // the counter of the next (wide) level starts at 0
+        }
+      }
+      cluster.sync();
+      lo = state0[0];
+      hi = state0[1];
+      level = (int)state0[2];
+      status = (int)state0[3];
+      cluster.sync();  // everyone has read CTA 0's state before it is rewritten
+      if (status) break;
+      continue;
+    }
+    // a wide level across the cluster
+    if (crank == 0 && tid == 0) s_ctr[(level + 1) % 3] = 0;  // the next level's counter
+    const int64_t len = (nP + kClusterCTAs - 1) / kClusterCTAs;
+    const int64_t plo = min(hi, lo + (int64_t)crank * len), phi = min(hi, plo + len);
+    expand_slice(a, adj, plo, phi, level, hi, ctr0 + (level % 3), s_scan, &s_base);
+    cluster.sync();
+    const int64_t new_hi = hi + (int64_t)ctr0[level % 3];
+    if (new_hi > a.budget || new_hi > a.cap) {
+      if (crank == 0 && tid == 0) {
+        a.status->code = new_hi > a.budget ? 1 : 2;
+        a.status->needed = new_hi;
+      }
+      status = 1;
+      break;
+    }
+    lo = hi;
+    hi = new_hi;
+    ++level;
+    if (crank == 0 && tid == 0 && hi > lo) a.level_off[level + 1] = hi;
+  }
+  cluster.sync();  // no CTA exits while its shared memory may still be read
+  if (crank == 0 && tid == 0 && a.status->code == 0 && !status) {
+    a.status->total = hi;
+    a.status->n_levels = level;
   }
 }
 
@@ -919,6 +1203,32 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(enumerate_levels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+  // canonical dedup: the cluster walk (env DSG_ENUM_CLUSTER=0: one CTA)
+  static const bool cluster_off = [] {
+    const char* e = std::getenv("DSG_ENUM_CLUSTER");
+    return e && std::atoi(e) == 0;
+  }();
+  a.cluster_ok = !a.hash_mode && a.csr_in_smem && !cluster_off;
+  a.resume = L.resume;
+  if (L.resume) {
+    cudaFuncSetAttribute(enumerate_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kClusterCTAs);
+    cfg.blockDim = dim3(kEnumThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kClusterCTAs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, enumerate_cluster_kernel, a);
+    count_launch();
+    return;
+  }
   enumerate_levels_kernel<<<1, kEnumThreads, smem, st>>>(a);
   count_launch();
 }
