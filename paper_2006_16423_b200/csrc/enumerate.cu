@@ -120,7 +120,8 @@ struct EnumArgs {
   int64_t cand_cap;
   int64_t* table;      // [table_cap] candidate index or -1
   int64_t table_cap;
-  int cluster_ok;      // stop at the first level wider than one CTA's frontier (code 4)
+  int cluster_ok;      // stop at the first level wider than wide_min (code 4)
+  int64_t wide_min;    // levels above this go to the cluster (<= cta_cap(W))
   int resume;          // cluster kernel: continue from status->resume_*
 };
 
@@ -487,7 +488,10 @@ __device__ void expand_resident(const EnumArgs& a, int64_t* lo_io, int64_t* hi_i
     // stay while the next level fits this team: warp mode for tiny levels,
     // CTA mode for the rest up to the shared-memory cap
     const bool tiny = (int64_t)nC * W <= a.warp_items && nC <= small_cap(W);
-    const bool fits = TEAM == 32 ? tiny : (nC <= cap && !tiny);
+    // (the CTA stays on while the level fits its frontier — and, when the
+    // cluster walk may take over, is not wider than wide_min)
+    const bool fits = TEAM == 32 ? tiny
+                                 : (nC <= cap && !tiny && (!a.cluster_ok || nC <= a.wide_min));
     if (nC == 0 || !fits || new_hi > a.budget || new_hi > a.cap) break;
     // advance without leaving the team (the CTA step's bookkeeping)
     lo = hi;
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_levels_kernel(EnumArgs
         lo = s_lo;
         hi = s_hi;
         level = s_level;
-      } else if (a.cluster_ok && nP > cta_cap(W)) {
+      } else if (a.cluster_ok && nP > a.wide_min) {
         // a level wider than the shared frontier: the cluster kernel takes
         // over from here (launch_enumerate / capi.cu enumerate_device)
         if (tid == 0) {
@@ -865,13 +869,13 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_cluster_kernel(EnumArg
   int status = 0;  // 1 budget, 2 capacity
   while (hi > lo) {
     const int64_t nP = hi - lo;
-    if (nP <= cta_cap(W)) {
+    if (nP <= a.wide_min) {
       // CTA 0 alone walks levels up to its shared frontier capacity — tiny
       // ones with warp 0, the others with the whole CTA — level after level
       // with the frontier in its shared memory, until a wide level (or the
       // end); the other CTAs wait at the barrier
       if (crank == 0) {
-        while (hi > lo && hi - lo <= cta_cap(W)) {
+        while (hi > lo && hi - lo <= a.wide_min) {
           const int64_t np = hi - lo;
           if (tid == 0) s_next = (unsigned long long)hi;
           __syncthreads();
@@ -1209,6 +1213,9 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
     return e && std::atoi(e) == 0;
   }();
   a.cluster_ok = !a.hash_mode && a.csr_in_smem && !cluster_off;
+  a.wide_min = cta_cap(a.W);
+  if (const char* e = std::getenv("DSG_ENUM_WIDE"))
+    a.wide_min = std::max<int64_t>(1, std::min<int64_t>(a.wide_min, std::atoll(e)));
   a.resume = L.resume;
   if (L.resume) {
     cudaFuncSetAttribute(enumerate_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
