@@ -63,8 +63,8 @@ constexpr int kDescThreads = 128;
 // but no more lanes than about one full wave of threads needs: large
 // lattices keep all lanes busy with fewer lanes per ideal.
 __host__ __device__ __forceinline__ int desc_group(int W, int64_t I) {
-  int G = 1;
-  while (G < W && G < 32) G <<= 1;
+  (void)W;  // the member loops stride over bit positions, so any W uses G lanes
+  int G = 32;
   while (G > 1 && I * G > 148 * 8 * kDescThreads) G >>= 1;
   return G;
 }
@@ -88,6 +88,9 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
   const unsigned gm = G == 32 ? 0xffffffffu : ((1u << G) - 1) << ((threadIdx.x & 31) & ~(G - 1));
   const int64_t o = (int64_t)blockIdx.x * groups + gid;
   if (o >= a.I) return;  // group-uniform
+  // member loops: this lane takes the bit positions ≡ lane (mod G) of every word
+  uint64_t lm = 0;
+  for (int b = lane; b < 64; b += G) lm |= 1ull << b;
   uint64_t* A = d_sh + (size_t)gid * 4 * W;
   uint64_t* F = A + W;
   uint64_t* T = F + W;
@@ -103,8 +106,8 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
   }
   __syncwarp(gm);
   if (a.training) {  // A = J ∪ paired backward nodes (dp_solver.cpp:235-250)
-    for (int w = lane; w < W; w += G) {
-      for (uint64_t x = J[w]; x; x &= x - 1) {
+    for (int w = 0; w < W; ++w) {
+      for (uint64_t x = J[w] & lm; x; x &= x - 1) {
         const int v = (w << 6) | (__ffsll((long long)x) - 1);
         const uint64_t* tw = g.twins + (size_t)v * W;
         for (int y = 0; y < W; ++y) {
@@ -118,9 +121,9 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
   // prefix sums and the frontier F(A) (members with a real successor outside)
   int64_t cpu = 0, acc = 0, mem = 0, fwv = 0;
   int32_t un = 0, fwi = 0, nF = 0;
-  for (int w = lane; w < W; w += G) {
+  for (int w = 0; w < W; ++w) {
     uint64_t fw = 0;
-    for (uint64_t x = A[w]; x; x &= x - 1) {
+    for (uint64_t x = A[w] & lm; x; x &= x - 1) {
       const int b = __ffsll((long long)x) - 1, v = (w << 6) | b;
       cpu += g.cpu[v];
       acc += g.acc[v];
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
         ++nF;
       }
     }
-    F[w] = fw;
+    if (fw) atomicOr((unsigned long long*)&F[w], (unsigned long long)fw);
   }
   cpu = group_sum(cpu, G, gm);
   acc = group_sum(acc, G, gm);
@@ -167,11 +170,13 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
     const int lo = c * 64, hi = min(nF, lo + 64);
     // the chunk's upper neighbours T (successors outside A), weights, ∞ mask
     uint64_t infm = 0;
-    for (int w = lane; w < W; w += G) {
-      int r = rF[w];
-      for (uint64_t x = F[w]; x; x &= x - 1, ++r) {
+    for (int w = 0; w < W; ++w) {
+      if (rF[w] >= hi || rF[w] + __popcll(F[w]) <= lo) continue;
+      for (uint64_t x = F[w] & lm; x; x &= x - 1) {
+        const int b = __ffsll((long long)x) - 1;
+        const int r = rF[w] + __popcll(F[w] & ((1ull << b) - 1));
         if (r < lo || r >= hi) continue;
-        const int u = (w << 6) | (__ffsll((long long)x) - 1);
+        const int u = (w << 6) | b;
         for (int e = g.out_real_off[u]; e < g.out_real_off[u + 1]; ++e) {
           const int y = g.out_real_adj[e];
           if (!bit_of(A, y)) atomicOr((unsigned long long*)&T[y >> 6], 1ull << (y & 63));
@@ -197,10 +202,11 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
       }
       __syncwarp(gm);
       // NItem per upper neighbour y: which chunk producers feed it
-      for (int w = lane; w < W; w += G) {
-        int r = rT[w];
-        for (uint64_t x = T[w]; x; x &= x - 1, ++r) {
-          const int y = (w << 6) | (__ffsll((long long)x) - 1);
+      for (int w = 0; w < W; ++w) {
+        for (uint64_t x = T[w] & lm; x; x &= x - 1) {
+          const int b = __ffsll((long long)x) - 1;
+          const int r = rT[w] + __popcll(T[w] & ((1ull << b) - 1));
+          const int y = (w << 6) | b;
           uint64_t pm = 0;
           for (int fw = 0; fw < W; ++fw) {
             int q = rF[fw];
@@ -236,8 +242,8 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
   int up = 1;
   if (a.training) {
     // P'(A) = L(A) = real predecessors of A outside A
-    for (int w = lane; w < W; w += G) {
-      for (uint64_t x = A[w]; x; x &= x - 1) {
+    for (int w = 0; w < W; ++w) {
+      for (uint64_t x = A[w] & lm; x; x &= x - 1) {
         const int v = (w << 6) | (__ffsll((long long)x) - 1);
         for (int e = g.in_real_off[v]; e < g.in_real_off[v + 1]; ++e) {
           const int u = g.in_real_adj[e];
@@ -247,8 +253,8 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
     }
     __syncwarp(gm);
     // per u: one MaskItem per word where succ(u) meets A
-    for (int w = lane; w < W; w += G) {
-      for (uint64_t x = P[w]; x; x &= x - 1) {
+    for (int w = 0; w < W; ++w) {
+      for (uint64_t x = P[w] & lm; x; x &= x - 1) {
         const int u = (w << 6) | (__ffsll((long long)x) - 1);
         const uint64_t* su = g.succ_real + (size_t)u * W;
         for (int y = 0; y < W; ++y) nLI += (su[y] & A[y]) ? 1 : 0;
@@ -299,8 +305,8 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
     }
     // Φ(J) = A ∩ backward: an up-set of the backward part?
     if (a.has_bw) {
-      for (int w = lane; w < W; w += G) {
-        for (uint64_t x = A[w] & g.bwset[w]; x; x &= x - 1) {
+      for (int w = 0; w < W; ++w) {
+        for (uint64_t x = A[w] & g.bwset[w] & lm; x; x &= x - 1) {
           const int b = (w << 6) | (__ffsll((long long)x) - 1);
           const uint64_t* bs = g.bw_succ + (size_t)b * W;
           for (int y = 0; y < W; ++y)
