@@ -116,10 +116,32 @@ struct DeviceCtx {
         ++it;
       }
     }
+    for (auto it = pinned_named.begin(); it != pinned_named.end();) {
+      if (it->first.compare(0, prefix.size(), prefix) == 0) {
+        if (it->second.first) cudaFreeHost(it->second.first);
+        it = pinned_named.erase(it);
+      } else {
+        ++it;
+      }
+    }
   }
   template <typename T>
   T* get_t(const std::string& name, size_t count) {
     return static_cast<T*>(get(name, count * sizeof(T)));
+  }
+  // pinned device->host landing areas (per pipeline prefix) for a solve's
+  // small results: copies into them stay asynchronous (a D2H into pageable
+  // memory waits for the copy)
+  std::map<std::string, std::pair<void*, size_t>> pinned_named;
+  void* rb(const std::string& name, size_t bytes) {
+    auto& b = pinned_named[name];
+    if (b.second < bytes) {
+      if (b.first) cudaFreeHost(b.first);
+      b.first = nullptr;
+      CK(cudaMallocHost(&b.first, bytes));
+      b.second = bytes;
+    }
+    return b.first;
   }
   void* host(size_t bytes) {
     if (pinned_cap < bytes) {
@@ -562,8 +584,8 @@ DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P, const std::string& p
   char* dev = static_cast<char*>(ctx.get(prefix + "graph", pk.total));
   CK(cudaMemcpyAsync(dev, host, pk.total, cudaMemcpyHostToDevice, ctx.stream));
   ctx.h2d_bytes += (int64_t)pk.total;
-  // the staging buffer is reused by the next solve: the copy must land first
-  CK(cudaStreamSynchronize(ctx.stream));
+  // (the staging buffer is next written by the next solve's upload, after
+  // this solve's final synchronisation)
   DeviceGraph d;
   DevGraph& g = d.g;
   g.n = P.n;
@@ -691,7 +713,6 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
                     perm_a, perm_b, ctx.stream);
     CK(cudaGetLastError());
     debug_sync(ctx, "lex rank");
-    CK(cudaStreamSynchronize(ctx.stream));
     return lat;
   }
   throw Fail{DSG_CUDA_ERROR, "enumeration capacity retries exhausted"};
@@ -710,6 +731,18 @@ cudaEvent_t pl_ev_end(DeviceCtx& ctx) {
 
 struct Pipeline;
 void write_trace(DeviceCtx& ctx, const Pipeline& pl, const char* path);
+
+// One solve's small device->host results, landing in pinned memory (followed
+// by the traceback arrays: kinds [maxb], loads [maxb], block bits [maxb][W]).
+struct Readback {
+  int64_t n_cov;
+  int64_t totals[kNumCounts];
+  int32_t cov_bad;
+  int32_t flags[2];  // stop, watchdog
+  int32_t tables_bad;
+  unsigned long long pairs;
+  TraceState tb;
+};
 
 // ------------------------------------------------------------ solve
 // Phase 1: lattice, descriptors, chunk plan, DP buffers.  Phase 2: reset, all
@@ -751,6 +784,7 @@ struct Pipeline {
   std::vector<unsigned*> peer_done;
   std::vector<void*> ipc_opened;
   double t_enum_ms = 0, t_desc_ms = 0;
+  Readback* rbk = nullptr;  // pinned, this pipeline's
 };
 
 void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_options* opt,
@@ -791,8 +825,14 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   int64_t* cov_off = ctx.get_t<int64_t>(pfx + "lat.cov_off", (size_t)I + 1);
   launch_cover_count(W, I, lat.smax, cov_off, st);
   launch_scan_counts(cov_off, I, 1, st);
-  int64_t n_cov = 0;
-  D2H(&n_cov, cov_off + I, sizeof(int64_t));
+  {
+    const int maxb = K + Lc + 1;
+    pl.rbk = static_cast<Readback*>(ctx.rb(pfx + "rb", sizeof(Readback) + 16 +
+                                                          (size_t)maxb * (4 + 8 + 8 * W)));
+    std::memset(pl.rbk, 0, sizeof(Readback));
+  }
+  Readback& rbk = *pl.rbk;
+  D2H(&rbk.n_cov, cov_off + I, sizeof(int64_t));
 
   // ---- descriptors
   const auto t2 = Clock::now();
@@ -819,11 +859,12 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   CK(cudaMemsetAsync(D.counts, 0, sizeof(int64_t) * kNumCounts * (I + 1), st));
   launch_describe(D, false, st);
   launch_scan_counts(D.counts, I, kNumCounts, st);
-  int64_t totals[kNumCounts];
   for (int k = 0; k < kNumCounts; ++k)
-    D2H(&totals[k], D.counts + (size_t)k * (I + 1) + I, sizeof(int64_t));
-  CK(cudaStreamSynchronize(st));
+    D2H(&rbk.totals[k], D.counts + (size_t)k * (I + 1) + I, sizeof(int64_t));
+  CK(cudaStreamSynchronize(st));  // pool sizes: the one synchronisation after the lattice
   CK(cudaGetLastError());
+  const int64_t* totals = rbk.totals;
+  const int64_t n_cov = rbk.n_cov;
   if (totals[kCntF] > INT32_MAX || totals[kCntN] > INT32_MAX || totals[kCntLItems] > INT32_MAX)
     throw Fail{DSG_UNSUPPORTED, "frontier tables exceed 2^31 entries"};
   D.chunks = ctx.get_t<FChunk>(pfx + "d.chunks", totals[kCntChunks]);
@@ -1206,10 +1247,10 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       PP.vrank = pl.vranks_d;
     }
     CK(cudaGetLastError());
-    int cov_bad = 0;
-    D2H(&cov_bad, cov_err, sizeof(int));
-    CK(cudaStreamSynchronize(st));  // host vectors are temporaries
-    if (cov_bad) throw Fail{DSG_CUDA_ERROR, "lower-cover lookup failed"};
+    // checked after the solve's one final synchronisation (pageable H2D
+    // copies are staged before cudaMemcpyAsync returns, so the host
+    // temporaries above may go)
+    D2H(&pl.rbk->cov_bad, cov_err, sizeof(int));
   }
   // peer tables: this GPU only, until a sharded session attaches its peers
   if (pl.world == 1) {
@@ -1223,7 +1264,6 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   CK(cudaMemcpyAsync(pd, pl.peer_dp.data(), sizeof(void*) * pl.world, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(pb, pl.peer_bp.data(), sizeof(int32_t*) * pl.world, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(pn, pl.peer_done.data(), sizeof(unsigned*) * pl.world, cudaMemcpyHostToDevice, st));
-  CK(cudaStreamSynchronize(st));
   PP.peer_dp = pd;
   PP.peer_bp = pb;
   PP.peer_done = pn;
@@ -1282,7 +1322,6 @@ void reset_tables(DeviceCtx& ctx, const Prepared& P, Pipeline& pl) {
     }
     if (pl.virt) CK(cudaMemsetAsync(pl.tables_bad, 0, sizeof(int), st));
   }
-  CK(cudaStreamSynchronize(st));
 }
 
 void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline& pl,
@@ -1298,6 +1337,11 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
   const int vb = P.value_bits;
   LevelLaunch& LL = pl.LL;
   void* dp = LL.dp;
+  // this pass's readback fields (cov_bad belongs to phase 1, maybe in flight)
+  pl.rbk->tb = TraceState{};
+  pl.rbk->flags[0] = pl.rbk->flags[1] = 0;
+  pl.rbk->tables_bad = 0;
+  pl.rbk->pairs = 0;
 
   cudaEvent_t ev_desc, ev_dp;
   CK(cudaEventCreate(&ev_desc));
@@ -1332,21 +1376,17 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev_dp, st));
     if (PP.trace) write_trace(ctx, pl, trace_file);
-    int flags_h[2] = {0, 0};
-    D2H(flags_h, PP.stop, sizeof flags_h);
-    int bad = 0;
+    D2H(pl.rbk->flags, PP.stop, sizeof pl.rbk->flags);
     if (pl.virt) {
       // every rank's replica must equal rank 0's byte for byte: each row
       // was stored into every table by the rank that finalized it
       const size_t bytes = (size_t)I * C * (vb == 32 ? 4 : 8);
       for (int r = 1; r < pl.world; ++r)
         launch_compare_tables(pl.vranks[0].dp, pl.vranks[r].dp, bytes, pl.tables_bad, st);
-      D2H(&bad, pl.tables_bad, sizeof bad);
+      D2H(&pl.rbk->tables_bad, pl.tables_bad, sizeof(int));
     }
-    CK(cudaStreamSynchronize(st));
-    if (flags_h[1]) throw Fail{DSG_CUDA_ERROR, "dataflow watchdog fired"};
-    if (flags_h[0]) throw Fail{DSG_DEADLINE, "time limit reached"};
-    if (bad) throw Fail{DSG_LOGIC, "virtual shard dp replicas differ"};
+    // stop / watchdog / replica checks wait for the final synchronisation;
+    // the traceback reads the stop flags on the device and stands down
   } else {
     CK(cudaEventRecord(ev_desc, st));
     for (int s = 1; s < lat.n_levels; ++s) {
@@ -1393,8 +1433,8 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
   res->persistent_blocks = pl.persistent ? pl.pinfo.blocks : 0;
 
   // ---- traceback (rank 0 of a sharded run holds every row)
-  unsigned long long pairs = 0;
-  D2H(&pairs, LL.pair_counter, sizeof pairs);
+  Readback& rbk = *pl.rbk;
+  D2H(&rbk.pairs, LL.pair_counter, sizeof rbk.pairs);
 #ifdef DSG_PAIR_STATS
   {
     unsigned long long sv[4];
@@ -1406,10 +1446,10 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
 #endif
   const bool do_traceback = pl.rank == 0;
   const int maxb = K + Lc + 1;
-  TraceState tb{};
-  std::vector<int32_t> cpus(maxb);
-  std::vector<uint64_t> bbits((size_t)maxb * W);
-  std::vector<int64_t> loads(maxb, 0);
+  int32_t* cpus = reinterpret_cast<int32_t*>(pl.rbk + 1);
+  int64_t* loads = reinterpret_cast<int64_t*>(
+      reinterpret_cast<uintptr_t>(cpus + maxb + 1) & ~uintptr_t(7));
+  uint64_t* bbits = reinterpret_cast<uint64_t*>(loads + maxb);
   if (do_traceback) {
     TraceBuffers tbuf;
     tbuf.state = ctx.get_t<TraceState>(pl.pfx + "tb.state", 1);
@@ -1421,11 +1461,12 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
     tbuf.kinds = ctx.get_t<int32_t>(pl.pfx + "tb.kinds", maxb);
     tbuf.block_bits = ctx.get_t<uint64_t>(pl.pfx + "tb.bits", (size_t)maxb * W);
     tbuf.loads = ctx.get_t<int64_t>(pl.pfx + "tb.loads", maxb);
+    tbuf.abort = pl.persistent ? pl.PP.stop : nullptr;
     launch_traceback(LL, pl.level_of_d, pl.level_off_d, I, ctx.sm_count, tbuf, st);
-    D2H(&tb, tbuf.state, sizeof tb);
-    D2H(cpus.data(), tbuf.kinds, sizeof(int32_t) * maxb);
-    D2H(bbits.data(), tbuf.block_bits, sizeof(uint64_t) * maxb * W);
-    D2H(loads.data(), tbuf.loads, sizeof(int64_t) * maxb);
+    D2H(&rbk.tb, tbuf.state, sizeof rbk.tb);
+    D2H(cpus, tbuf.kinds, sizeof(int32_t) * maxb);
+    D2H(bbits, tbuf.block_bits, sizeof(uint64_t) * maxb * W);
+    D2H(loads, tbuf.loads, sizeof(int64_t) * maxb);
   }
   if (flags & DSG_FLAG_KEEP_TABLES) {
     res->words = W;
@@ -1435,8 +1476,16 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
     if (vb == 64) D2H(res->dp_values, dp, sizeof(int64_t) * (size_t)I * C);
   }
   CK(cudaEventRecord(pl_ev_end(ctx), st));
-  CK(cudaStreamSynchronize(st));
+  CK(cudaStreamSynchronize(st));  // the solve's one synchronisation after the lattice
   CK(cudaGetLastError());
+  const TraceState& tb = rbk.tb;
+  const unsigned long long pairs = rbk.pairs;
+  if (rbk.cov_bad) throw Fail{DSG_CUDA_ERROR, "lower-cover lookup failed"};
+  if (pl.persistent) {
+    if (rbk.flags[1]) throw Fail{DSG_CUDA_ERROR, "dataflow watchdog fired"};
+    if (rbk.flags[0]) throw Fail{DSG_DEADLINE, "time limit reached"};
+    if (rbk.tables_bad) throw Fail{DSG_LOGIC, "virtual shard dp replicas differ"};
+  }
   if ((flags & DSG_FLAG_KEEP_TABLES) && vb == 32) {
     std::vector<int32_t> tmp((size_t)I * C);
     ctx.d2h_bytes += (int64_t)(sizeof(int32_t) * tmp.size());
@@ -1809,8 +1858,10 @@ int dsg_enumerate_ideals(const dsg_graph* graph, const uint8_t* within, int64_t 
     out->count = lat.I;
     out->words = P.W;
     out->bits = (uint64_t*)std::malloc(sizeof(uint64_t) * (size_t)lat.I * P.W + 8);
-    CK(cudaMemcpy(out->bits, lat.sbits, sizeof(uint64_t) * (size_t)lat.I * P.W,
-                  cudaMemcpyDeviceToHost));
+    // ctx.stream is non-blocking: a legacy-stream copy would not wait for it
+    CK(cudaMemcpyAsync(out->bits, lat.sbits, sizeof(uint64_t) * (size_t)lat.I * P.W,
+                       cudaMemcpyDeviceToHost, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
     out->n_levels = lat.n_levels;
     out->level_offsets = (int64_t*)std::malloc(sizeof(int64_t) * (lat.n_levels + 1));
     std::memcpy(out->level_offsets, lat.level_off.data(), sizeof(int64_t) * (lat.n_levels + 1));

@@ -310,6 +310,7 @@ struct TraceBuffers {
   int32_t* kinds;        // cpu | repl << 1
   uint64_t* block_bits;  // [K+L+1][W]
   int64_t* loads;        // [K+L+1] per-device load of each block (INT64_MAX = inf)
+  const int* abort;      // [2] persistent stop / watchdog flags, or null: set -> status 3
 };
 
 void launch_traceback(const LevelLaunch& L, const int32_t* level_of, const int64_t* level_off,

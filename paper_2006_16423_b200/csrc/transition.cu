@@ -141,8 +141,15 @@ __global__ void fill_u32_kernel(unsigned* p, int64_t n, unsigned value) {
 
 // Fewest-devices cell (dp_solver.cpp:337-351); one thread.
 template <typename V>
-__global__ void traceback_init_kernel(int64_t I, int K, int L, const V* dp, TraceState* st) {
+__global__ void traceback_init_kernel(int64_t I, int K, int L, const V* dp, TraceState* st,
+                                      const int* abort) {
   constexpr V INF = VTraits<V>::INF;
+  if (abort && (abort[0] | abort[1])) {
+    // the dp pass stopped early (deadline / watchdog): the host raises it
+    st->status = 3;
+    st->n_blocks = 0;
+    return;
+  }
   const int lp1 = L + 1, C = (K + 1) * lp1;
   const V* row = dp + (size_t)(I - 1) * C;
   const V best = row[K * lp1 + L];
@@ -455,7 +462,7 @@ void dispatch_tile(const LevelLaunch& L, dim3 grid, cudaStream_t st) {
 template <typename V>
 void traceback_t(const LevelLaunch& L, const int32_t* level_of, const int64_t* level_off,
                  int64_t I, int sm_count, TraceBuffers& b, cudaStream_t st) {
-  traceback_init_kernel<V><<<1, 1, 0, st>>>(I, L.K, L.L, (const V*)L.dp, b.state);
+  traceback_init_kernel<V><<<1, 1, 0, st>>>(I, L.K, L.L, (const V*)L.dp, b.state, b.abort);
   count_launch();
   const int grid = b.n_parts;
   const size_t smem = (size_t)L.W * sizeof(uint64_t) * 2;
