@@ -995,7 +995,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   if (const char* e = std::getenv("DSG_GRADE1")) grade1 = std::max(0, std::atoi(e));
   int64_t fin_fold_max = 32;  // mode 1: the finisher folds level s-2 up to this size
   if (const char* e = std::getenv("DSG_FIN_FOLD")) fin_fold_max = std::max(0, std::atoi(e));
-  int runner_max_t = 4;  // chain runner: finishers of mode-1 levels with <= this many targets
+  int runner_max_t = 16;  // chain runner: finishers of mode-1 levels with <= this many targets
+                          // (C4 DP: 4 -> 5.21 ms, 8 -> 4.99, 12..64 -> 4.93; C1-C3, C5 flat)
   if (const char* e = std::getenv("DSG_RUNNER_T")) runner_max_t = std::max(0, std::atoi(e));
   int fold_levels = 1;  // measured on C4: folding s-3 too costs the finisher more than it saves
   if (const char* e = std::getenv("DSG_FOLD_LEVELS")) fold_levels = std::max(0, std::atoi(e));
@@ -1119,6 +1120,10 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
 
   PP.grade = grade;
   PP.poll_ns_max = poll_ns_max;
+  // narrow-level cell polls spin (few pollers, each on the level-to-level
+  // chain): C1 DP 0.42 -> 0.37 ms, C4 4.97 -> 4.89 ms, C2/C3/C5 flat
+  PP.fin_poll_ns = 0;
+  if (const char* e = std::getenv("DSG_FIN_POLL_NS")) PP.fin_poll_ns = (unsigned)std::max(0, std::atoi(e));
   // work items in readiness order, built on the device (launch_build_items):
   // buckets by dep = level of the chunk's last source, critical items first;
   // a sharded solve lists only this rank's units (virtual shards: one list

@@ -356,29 +356,78 @@ __global__ void __launch_bounds__(kDescThreads) describe_kernel(DescribeLaunch a
 
 // In-place exclusive scan of one [n + 1] int64 array per block
 // (element n is 0 on entry and receives the total).
+// Exclusive scan of one [n + 1] count array per CTA (the entry n becomes the
+// total).  Tiles of 1024 x 8 entries: each thread scans 8 consecutive
+// entries (coalesced 16-byte loads), warp shuffles and one shared pass over
+// the 32 warp sums give the tile's offsets, and the tile total carries over.
 __global__ void __launch_bounds__(1024) scan_counts_kernel(int64_t* counts, int64_t n) {
+  constexpr int kPer = 8;
   int64_t* x = counts + (size_t)blockIdx.x * (n + 1);
   const int64_t total_n = n + 1;
-  const int T = blockDim.x;
-  const int64_t seg = (total_n + T - 1) / T;
-  const int64_t lo = threadIdx.x * seg;
-  const int64_t hi = min(total_n, lo + seg);
-  int64_t s = 0;
-  for (int64_t i = lo; i < hi; ++i) s += x[i];
-  __shared__ int64_t sh[1024];
-  sh[threadIdx.x] = s;
-  __syncthreads();
-  for (int off = 1; off < T; off <<= 1) {
-    int64_t v = threadIdx.x >= off ? sh[threadIdx.x - off] : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t carry_s;
+  if (threadIdx.x == 0) carry_s = 0;
+  // the array base is 8-byte aligned only: vector loads when 16-aligned
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  for (int64_t base = 0; base < total_n; base += (int64_t)blockDim.x * kPer) {
+    const int64_t lo = base + (int64_t)threadIdx.x * kPer;
+    int64_t v[kPer];
+    if (vec && lo + kPer <= total_n) {
+#pragma unroll
+      for (int j = 0; j < kPer; j += 2) {
+        const longlong2 q = *reinterpret_cast<const longlong2*>(x + lo + j);
+        v[j] = q.x;
+        v[j + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) v[j] = lo + j < total_n ? x[lo + j] : 0;
+    }
+    int64_t s = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) s += v[j];
+    int64_t incl = s;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    sh[threadIdx.x] += v;
+    if (warp == 0) {
+      const int nw = blockDim.x >> 5;
+      int64_t w = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += y;
+      }
+      if (lane < nw) wsum[lane] = w;  // inclusive warp offsets
+    }
     __syncthreads();
-  }
-  int64_t run = sh[threadIdx.x] - s;  // exclusive
-  for (int64_t i = lo; i < hi; ++i) {
-    int64_t v = x[i];
-    x[i] = run;
-    run += v;
+    const int64_t carry = carry_s;
+    int64_t run = carry + (warp ? wsum[warp - 1] : 0) + incl - s;
+    if (vec && lo + kPer <= total_n) {
+#pragma unroll
+      for (int j = 0; j < kPer; j += 2) {
+        longlong2 q;
+        q.x = run;
+        run += v[j];
+        q.y = run;
+        run += v[j + 1];
+        *reinterpret_cast<longlong2*>(x + lo + j) = q;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        if (lo + j < total_n) x[lo + j] = run;
+        run += v[j];
+      }
+    }
+    __syncthreads();  // every thread has read carry_s and wsum
+    if (threadIdx.x == blockDim.x - 1) carry_s = carry + wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
   }
 }
 

@@ -201,6 +201,7 @@ struct PersistPlan {
   int stage;                 // stage old mode-0 chunks in shared memory
   int dead_skip;             // count-only scans of chunks that cannot change a cell
   unsigned poll_ns_max;      // dependency-wait backoff cap
+  unsigned fin_poll_ns;    // narrow-level cell polls: backoff cap (0 = spin)
   const int64_t* chunk_lo;
   const int64_t* chunk_base;
   const int64_t* tile_base;  // [n_levels] prefix of arrival counters over levels

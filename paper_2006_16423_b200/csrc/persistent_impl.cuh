@@ -291,8 +291,10 @@ __device__ __forceinline__ V ld_final(const PersistPlan& p, const CtaView& cv, c
   unsigned ns = 32, polls = 0;
   const uint64_t t0 = globaltimer();
   while (true) {
-    __nanosleep(ns);
-    ns = ns < p.poll_ns_max ? ns * 2 : p.poll_ns_max;
+    if (p.fin_poll_ns) {
+      __nanosleep(ns);
+      ns = ns < p.fin_poll_ns ? ns * 2 : p.fin_poll_ns;
+    }
     v = ld_relaxed_v<V>(q);
     if (v != VTraits<V>::PENDING) return v;
     if ((++polls & 63) != 0) continue;
@@ -575,6 +577,7 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
     if (blockIdx.x == 0 && tid == 0 && p.deadline_ns && globaltimer() > (uint64_t)p.deadline_ns)
       raise_stop(p, cv, false);
     V best[CMAX];
+    uint64_t tr_fold = 0;   // trace: a finisher's fold done (its rows final)
     bool any_last = false;  // trace: some unit of this item finalized
     if (mode == 0) {
       // ------------------------------------ lanes own targets
@@ -858,8 +861,13 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
             const int k = c / lp1;
             V v = tmp[c];
             for (int kk = 1; kk <= k; ++kk) v = min(v, tmp[c - kk * lp1]);
-            for (int r = 0; r < p.world; ++r) ((V*)p.peer_dp[r])[(size_t)t * C + c] = v;
+            // one GPU: the local table (no dependent load of the peer list
+            // on the level-to-level chain)
+            if (p.world == 1) reinterpret_cast<V*>(cv.dp)[(size_t)t * C + c] = v;
+            else
+              for (int r = 0; r < p.world; ++r) ((V*)p.peer_dp[r])[(size_t)t * C + c] = v;
           }
+          if (p.trace) tr_fold = globaltimer();
           __syncthreads();  // every cell stored before the (cumulative) release
           if (tid == 0) {
             release_done(p, s, 1u);
@@ -877,7 +885,7 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       }
     }
     __syncthreads();
-    const uint64_t tr2 = p.trace ? globaltimer() : 0;
+    const uint64_t tr2 = p.trace ? (tr_fold ? tr_fold : globaltimer()) : 0;
     if (p.trace && tid == 0) {  // runner items after the list's
       const long long g = s_gi;
       uint64_t* tr = p.trace + (g >= 0 ? g : cv.total_items + (-g - 1)) * 4;

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "scan.cuh"
 
@@ -466,7 +467,11 @@ void traceback_t(const LevelLaunch& L, const int32_t* level_of, const int64_t* l
   count_launch();
   const int grid = b.n_parts;
   const size_t smem = (size_t)L.W * sizeof(uint64_t) * 2;
-  if (I * L.W <= kTracebackCtaMax) {
+  static const int64_t cta_max = [] {
+    const char* e = std::getenv("DSG_TB_CTA_MAX");
+    return e ? (int64_t)std::atoll(e) : kTracebackCtaMax;
+  }();
+  if (I * L.W <= cta_max) {
     if (L.training)
       traceback_cta_kernel<V, true><<<1, 1024, smem, st>>>(L, b.state, level_of, level_off, b.ords,
                                                            b.prevs, b.kinds, b.block_bits, b.loads);
