@@ -863,7 +863,7 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
             for (int kk = 1; kk <= k; ++kk) v = min(v, tmp[c - kk * lp1]);
             // one GPU: the local table (no dependent load of the peer list
             // on the level-to-level chain)
-            if (p.world == 1) reinterpret_cast<V*>(cv.dp)[(size_t)t * C + c] = v;
+            if (p.world == 1) const_cast<V*>(reinterpret_cast<const V*>(cv.dp))[(size_t)t * C + c] = v;
             else
               for (int r = 0; r < p.world; ++r) ((V*)p.peer_dp[r])[(size_t)t * C + c] = v;
           }

@@ -1,2 +1,1 @@
-DSG_TRACE_FILE=gpurun_out/c4_trace_st2.bin python tools/profile_one.py C4 2
-for w in C4 C1 C2 C3 "C5:16,1,1,300"; do bash tools/knob_bench.sh $w "DSG_FIN_POLL_NS=0"; done
+python -m pytest tests/test_parity_gpu.py tests/test_virtual_shards_gpu.py tests/test_edges_gpu.py tests/test_reference_suites_gpu.py -m gpu -q -x 2>&1 | tail -2
