@@ -189,14 +189,19 @@ struct Q {  // exact rational
 };
 
 int64_t gcd64(int64_t a, int64_t b) {
-  if (a < 0) a = -a;
-  if (b < 0) b = -b;
-  while (b) {
-    int64_t t = a % b;
-    a = b;
-    b = t;
-  }
-  return a;
+  // binary GCD (no divisions); |INT64_MIN| is taken as 2^63 unsigned
+  uint64_t x = a < 0 ? 0ull - (uint64_t)a : (uint64_t)a;
+  uint64_t y = b < 0 ? 0ull - (uint64_t)b : (uint64_t)b;
+  if (!x) return (int64_t)y;
+  if (!y) return (int64_t)x;
+  const int sh = __builtin_ctzll(x | y);
+  x >>= __builtin_ctzll(x);
+  do {
+    y >>= __builtin_ctzll(y);
+    if (x > y) std::swap(x, y);
+    y -= x;
+  } while (y);
+  return (int64_t)(x << sh);
 }
 
 Q to_q(dsg_rat r) {
@@ -206,21 +211,49 @@ Q to_q(dsg_rat r) {
     q.inf = true;
     return q;
   }
-  i128 n = r.num, d = r.den;
+  if (r.num == INT64_MIN || r.den == INT64_MIN) {
+    // the one case whose negation leaves int64: 128-bit path
+    i128 n = r.num, d = r.den;
+    if (d < 0) {
+      n = -n;
+      d = -d;
+    }
+    i128 g = gcd64((int64_t)(n < 0 ? -n : n), (int64_t)d);
+    if (g > 1) {
+      n /= g;
+      d /= g;
+    }
+    if (n > INT64_MAX || n < INT64_MIN || d > INT64_MAX) throw Fail{DSG_OVERFLOW, "rational overflow"};
+    q.num = (int64_t)n;
+    q.den = (int64_t)d;
+    return q;
+  }
+  int64_t n = r.num, d = r.den;
   if (d < 0) {
     n = -n;
     d = -d;
   }
-  i128 g = gcd64((int64_t)(n < 0 ? -n : n), (int64_t)d);
+  const int64_t g = gcd64(n, d);
   if (g > 1) {
     n /= g;
     d /= g;
   }
-  if (n > INT64_MAX || n < INT64_MIN) throw Fail{DSG_OVERFLOW, "rational overflow"};
-  q.num = (int64_t)n;
-  q.den = (int64_t)d;
+  q.num = n;
+  q.den = d;
   return q;
 }
+
+// Adjacency lists in CSR form, filled in edge order (as push_back would).
+struct Adjl {
+  std::vector<int> off, adj;
+  struct Range {
+    const int *b, *e;
+    const int* begin() const { return b; }
+    const int* end() const { return e; }
+    size_t size() const { return (size_t)(e - b); }
+  };
+  Range operator[](int v) const { return {adj.data() + off[v], adj.data() + off[v + 1]}; }
+};
 
 struct Prepared {
   int n = 0, W = 0, K = 0, L = 0, C = 0;
@@ -254,6 +287,16 @@ void set_bit(std::vector<uint64_t>& m, int row, int W, int v) {
 Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint8_t* within,
                  bool enumerate_only, int flags) {
   Prepared P;
+  // DSG_PREP_TRACE=1: host ms per prepare step on stderr (diagnostics)
+  static const bool prep_trace = std::getenv("DSG_PREP_TRACE") != nullptr;
+  auto prep_t = Clock::now();
+#define PREP_MARK(name)                                                      \
+  do {                                                                       \
+    if (prep_trace) {                                                        \
+      std::fprintf(stderr, "prep %-10s %.3f ms\n", name, ms_since(prep_t)); \
+      prep_t = Clock::now();                                                 \
+    }                                                                        \
+  } while (0)
   if (!g || g->n_nodes < 0) throw Fail{DSG_INVALID, "invalid graph"};
   const int n = g->n_nodes;
   if (n > kMaxWords * 64)
@@ -262,28 +305,60 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
   P.W = std::max(1, (n + 63) / 64);
   const int W = P.W;
   P.ids.assign(g->ids, g->ids + n);
+  // external id -> dense index, first wins: a direct table when the ids are
+  // dense enough, else a hash map
+  int32_t id_lo = 0, id_hi = -1;
+  for (int i = 0; i < n; ++i) {
+    id_lo = i ? std::min(id_lo, g->ids[i]) : g->ids[i];
+    id_hi = i ? std::max(id_hi, g->ids[i]) : g->ids[i];
+  }
+  const bool direct = n > 0 && (int64_t)id_hi - id_lo < 4 * (int64_t)n + 64;
+  std::vector<int> table;
   std::unordered_map<int32_t, int> index;
-  index.reserve(n * 2 + 1);
-  for (int i = 0; i < n; ++i) index.emplace(g->ids[i], i);  // first wins
+  if (direct) {
+    table.assign((size_t)((int64_t)id_hi - id_lo + 1), -1);
+    for (int i = 0; i < n; ++i)
+      if (table[g->ids[i] - id_lo] < 0) table[g->ids[i] - id_lo] = i;
+  } else {
+    index.reserve(n * 2 + 1);
+    for (int i = 0; i < n; ++i) index.emplace(g->ids[i], i);
+  }
   auto idx_of = [&](int32_t id) {
+    if (direct) return id < id_lo || id > id_hi ? -1 : table[id - id_lo];
     auto it = index.find(id);
     return it == index.end() ? -1 : it->second;
   };
-  std::vector<std::vector<int>> out_real(n), in_real(n), out_all(n), in_all(n);
+  // resolved edges (dangling ends dropped), then CSR lists by counting
+  std::vector<int> ef, et;
+  ef.reserve(g->n_edges + g->n_artificial);
+  et.reserve(g->n_edges + g->n_artificial);
   for (int e = 0; e < g->n_edges; ++e) {
     int f = idx_of(g->edge_from[e]), t = idx_of(g->edge_to[e]);
     if (f < 0 || t < 0) continue;
-    out_real[f].push_back(t);
-    in_real[t].push_back(f);
-    out_all[f].push_back(t);
-    in_all[t].push_back(f);
+    ef.push_back(f);
+    et.push_back(t);
   }
+  const size_t n_real = ef.size();
   for (int e = 0; e < g->n_artificial; ++e) {
     int f = idx_of(g->art_from[e]), t = idx_of(g->art_to[e]);
     if (f < 0 || t < 0) continue;
-    out_all[f].push_back(t);
-    in_all[t].push_back(f);
+    ef.push_back(f);
+    et.push_back(t);
   }
+  auto build_adj = [&](size_t m, const std::vector<int>& from, const std::vector<int>& to,
+                       Adjl& out) {
+    out.off.assign(n + 1, 0);
+    out.adj.resize(m);
+    for (size_t e = 0; e < m; ++e) ++out.off[from[e] + 1];
+    for (int v = 0; v < n; ++v) out.off[v + 1] += out.off[v];
+    std::vector<int> pos(out.off.begin(), out.off.end() - 1);
+    for (size_t e = 0; e < m; ++e) out.adj[pos[from[e]]++] = to[e];
+  };
+  Adjl out_real, in_real, out_all, in_all;
+  build_adj(n_real, ef, et, out_real);
+  build_adj(n_real, et, ef, in_real);
+  build_adj(ef.size(), ef, et, out_all);
+  build_adj(ef.size(), et, ef, in_all);
   P.bw.assign(n, 0);
   for (int i = 0; i < n; ++i) P.bw[i] = g->is_backward ? (g->is_backward[i] != 0) : 0;
   P.has_bw = std::any_of(P.bw.begin(), P.bw.end(), [](uint8_t b) { return b != 0; });
@@ -297,6 +372,7 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     qmem[i] = to_q(g->mem_size[i]);
   }
 
+  PREP_MARK("weights");
   // acyclicity over real + artificial edges (the reference assumes a
   // validated DAG; a cycle would leave the universe unreachable)
   {
@@ -316,6 +392,7 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     if (seen != n) throw Fail{DSG_INVALID, "graph has a cycle (validate_dag first)"};
   }
 
+  PREP_MARK("acyclic");
   std::vector<std::vector<int>> paired_bw(n);
   P.in_universe.assign(n, 0);
   if (enumerate_only) {
@@ -369,13 +446,15 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
   for (int v = 0; v < n; ++v)
     if (added[v] && (qc[v].inf || qmem[v].inf)) P.inf_cpu_mem = true;
 
+  PREP_MARK("universe");
   // ---- fixed point at the common denominator D (exact)
-  i128 D = 1;
+  int64_t D64 = 1;  // <= 2^62 throughout
   auto lcm_in = [&](const Q& q) {
-    if (q.inf) return;
-    i128 gg = gcd64((int64_t)D, q.den);
-    D = D / gg * q.den;
-    if (D > ((i128)1 << 62)) throw Fail{DSG_OVERFLOW, "common denominator overflow"};
+    if (q.inf || q.den == 1 || D64 % q.den == 0) return;
+    const int64_t gg = gcd64(D64, q.den);
+    const i128 nd = (i128)(D64 / gg) * q.den;
+    if (nd > ((i128)1 << 62)) throw Fail{DSG_OVERFLOW, "common denominator overflow"};
+    D64 = (int64_t)nd;
   };
   for (int v = 0; v < n; ++v) {
     lcm_in(qc[v]);
@@ -400,9 +479,10 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     S = lcmK * P.repl_bn;
     if (S > ((i128)1 << 50)) throw Fail{DSG_OVERFLOW, "replication scale overflow"};
   }
+  const i128 D = D64;
   if (D * S > ((i128)1 << 62)) throw Fail{DSG_OVERFLOW, "common denominator overflow"};
   P.D = (int64_t)(D * S);
-  auto fx = [&](const Q& q) -> i128 { return q.inf ? 0 : (i128)q.num * (D / q.den) * S; };
+  auto fx = [&](const Q& q) -> i128 { return q.inf ? 0 : (i128)q.num * (D64 / q.den) * S; };
   P.cpu.assign(n, 0);
   P.acc.assign(n, 0);
   P.comm.assign(n, 0);
@@ -442,22 +522,22 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     if (P.interleave < 0 || P.interleave > 2) throw Fail{DSG_INVALID, "bad interleaving mode"};
   }
 
+  PREP_MARK("fixedpoint");
   // ---- adjacency bitsets and CSR
   const size_t NW = (size_t)n * W;
+  // [n][W] rows only where a kernel reads them: pred_real never (lists
+  // serve), twins only for training, bw_succ only with backward nodes
   P.succ_real.assign(NW, 0);
-  P.pred_real.assign(NW, 0);
+  P.pred_real.assign(W, 0);
   P.pred_u.assign(NW, 0);
   P.succ_u.assign(NW, 0);
-  P.twins.assign(NW, 0);
-  P.bw_succ.assign(NW, 0);
+  P.twins.assign(P.training ? NW : (size_t)W, 0);
+  P.bw_succ.assign(P.has_bw ? NW : (size_t)W, 0);
   P.bwset.assign(W, 0);
   P.out_off.assign(n + 1, 0);
   P.in_off.assign(n + 1, 0);
   for (int v = 0; v < n; ++v) {
-    for (int w : out_real[v]) {
-      set_bit(P.succ_real, v, W, w);
-      set_bit(P.pred_real, w, W, v);
-    }
+    for (int w : out_real[v]) set_bit(P.succ_real, v, W, w);
     P.out_off[v + 1] = P.out_off[v] + (int)out_real[v].size();
     P.in_off[v + 1] = P.in_off[v] + (int)in_real[v].size();
     if (P.in_universe[v]) {
@@ -473,28 +553,31 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
         if (P.bw[w]) set_bit(P.bw_succ, v, W, w);
     }
   }
-  for (int v = 0; v < n; ++v) {
-    P.out_adj.insert(P.out_adj.end(), out_real[v].begin(), out_real[v].end());
-    P.in_adj.insert(P.in_adj.end(), in_real[v].begin(), in_real[v].end());
-  }
+  PREP_MARK("bitsets");
+  P.out_adj.assign(out_real.adj.begin(), out_real.adj.end());
+  P.in_adj.assign(in_real.adj.begin(), in_real.adj.end());
   if (P.out_adj.empty()) P.out_adj.push_back(0);
   if (P.in_adj.empty()) P.in_adj.push_back(0);
-  // the same universe adjacency as lists (from the bitsets: unique entries)
-  auto to_csr = [&](const std::vector<uint64_t>& bs, std::vector<int32_t>& off,
-                    std::vector<int32_t>& adj) {
+  // the same universe adjacency as lists: sorted, unique (as a bit scan of
+  // pred_u / succ_u would give)
+  auto to_csr = [&](const Adjl& lists, std::vector<int32_t>& off, std::vector<int32_t>& adj) {
     off.assign(n + 1, 0);
     adj.clear();
+    adj.reserve(lists.adj.size());
     for (int v = 0; v < n; ++v) {
-      for (int k = 0; k < W; ++k)
-        for (uint64_t s = bs[(size_t)v * W + k]; s; s &= s - 1)
-          adj.push_back((k << 6) | __builtin_ctzll(s));
+      const size_t b0 = adj.size();
+      if (P.in_universe[v])
+        for (int u : lists[v])
+          if (P.in_universe[u]) adj.push_back(u);
+      std::sort(adj.begin() + b0, adj.end());
+      adj.erase(std::unique(adj.begin() + b0, adj.end()), adj.end());
       off[v + 1] = (int32_t)adj.size();
     }
     if (adj.empty()) adj.push_back(0);
   };
-  to_csr(P.pred_u, P.pu_off, P.pu_adj);
-  to_csr(P.succ_u, P.su_off, P.su_adj);
-
+  to_csr(in_all, P.pu_off, P.pu_adj);
+  to_csr(out_all, P.su_off, P.su_adj);
+  PREP_MARK("csr");
   // reachability_within(g, backward) for the general training gate
   // (graph.cpp:291-345): rows in reverse topological order
   if (P.training && P.has_bw) {
@@ -531,6 +614,7 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     P.bw_from.assign(W, 0);
     P.bw_to.assign(W, 0);
   }
+  PREP_MARK("reach");
   return P;
 }
 
