@@ -80,6 +80,16 @@ double ms_since(Clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
 }
 
+// DSG_PREP_TRACE=1: host timestamps of a solve's steps on stderr (diagnostics)
+void host_mark(const char* what) {
+  static const bool on = std::getenv("DSG_PREP_TRACE") != nullptr;
+  if (!on) return;
+  static Clock::time_point last = Clock::now();
+  const auto now = Clock::now();
+  std::fprintf(stderr, "host %-14s +%.3f ms\n", what, ms_since(last));
+  last = now;
+}
+
 // ------------------------------------------------------------ device arena
 // Named device buffers reused across solves on one device (grow-only), so a
 // repeated solve does no cudaMalloc.  One context per device, one solve at a
@@ -607,8 +617,9 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     }
     for (int u = 0; u < n; ++u) {
       if (!P.bw[u]) continue;
-      for (int w = 0; w < n; ++w)
-        if ((P.bw_from[(size_t)u * W + (w >> 6)] >> (w & 63)) & 1ull) set_bit(P.bw_to, w, W, u);
+      for (int k = 0; k < W; ++k)
+        for (uint64_t x = P.bw_from[(size_t)u * W + k]; x; x &= x - 1)
+          set_bit(P.bw_to, (k << 6) | __builtin_ctzll(x), W, u);
     }
   } else {
     P.bw_from.assign(W, 0);
@@ -759,7 +770,9 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
     debug_sync(ctx, "enumerate");
     EnumStatus st;
     D2H(&st, st_d, sizeof st);
+    host_mark("enum-sync-in");
     CK(cudaStreamSynchronize(ctx.stream));
+    host_mark("enum-sync-out");
     if (st.code == 4) {
       // a level wider than one CTA's frontier: the cluster walk continues
       // from it (enumerate.cu enumerate_cluster_kernel)
@@ -871,6 +884,42 @@ struct Pipeline {
   Readback* rbk = nullptr;  // pinned, this pipeline's
 };
 
+// The persistent plan's host tables (chunk plan, run lists, mode table,
+// virtual-rank records, peer lists) staged in pinned memory and moved with ONE
+// host->device copy into one device buffer (a dozen pageable copies cost
+// ~0.1 ms of host time with the GPU idle).  Each table's device pointer is
+// written through `out` at flush().
+struct PlanStage {
+  struct Ent {
+    const void* src;
+    size_t bytes, off;
+    void** out;
+  };
+  std::vector<Ent> ents;
+  size_t total = 0;
+  template <typename T>
+  void add(const T* src, size_t count, T** out) {
+    const size_t bytes = count * sizeof(T);
+    ents.push_back({src, bytes, total, reinterpret_cast<void**>(out)});
+    total += (std::max<size_t>(bytes, 8) + 15) & ~(size_t)15;
+  }
+  template <typename T>
+  void add(const std::vector<T>& v, T** out) {
+    add(v.data(), v.size(), out);
+  }
+  void flush(DeviceCtx& ctx, const std::string& pfx, cudaStream_t st) {
+    if (!total) return;
+    uint8_t* host = static_cast<uint8_t*>(ctx.rb(pfx + "plan", total));
+    uint8_t* dev = static_cast<uint8_t*>(ctx.get(pfx + "pp.plan", total));
+    for (const Ent& e : ents) {
+      if (e.bytes) std::memcpy(host + e.off, e.src, e.bytes);
+      *e.out = dev + e.off;
+    }
+    CK(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, st));
+    ctx.h2d_bytes += (int64_t)total;
+  }
+};
+
 void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_options* opt,
             Pipeline& pl) {
   const int flags = opt->flags;
@@ -945,7 +994,9 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   launch_scan_counts(D.counts, I, kNumCounts, st);
   for (int k = 0; k < kNumCounts; ++k)
     D2H(&rbk.totals[k], D.counts + (size_t)k * (I + 1) + I, sizeof(int64_t));
+  host_mark("cnt-sync-in");
   CK(cudaStreamSynchronize(st));  // pool sizes: the one synchronisation after the lattice
+  host_mark("cnt-sync-out");
   CK(cudaGetLastError());
   const int64_t* totals = rbk.totals;
   const int64_t n_cov = rbk.n_cov;
@@ -1182,19 +1233,17 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PersistPlan& PP = pl.PP;
   PP = PersistPlan{};
   PP.n_levels = lat.n_levels;
-  auto up64 = [&](const std::string& name, const std::vector<int64_t>& v) {
-    int64_t* d = ctx.get_t<int64_t>(pfx + name, v.size() + 1);
-    CK(cudaMemcpyAsync(d, v.data(), sizeof(int64_t) * v.size(), cudaMemcpyHostToDevice, st));
-    ctx.h2d_bytes += (int64_t)(sizeof(int64_t) * v.size());
-    return (const int64_t*)d;
+  PlanStage stage;
+  auto up64 = [&](const std::vector<int64_t>& v, const int64_t** out) {
+    stage.add(v.data(), v.size(), const_cast<int64_t**>(out));
   };
   PP.level_off = pl.level_off_d;
   PP.level_of = pl.level_of_d;
-  PP.n_chunks = up64("pp.n_chunks", pl.n_chunks);
-  PP.chunk_len = up64("pp.chunk_len", pl.chunk_len);
-  PP.chunk_lo = up64("pp.chunk_lo", chunk_lo);
-  PP.chunk_base = up64("pp.chunk_base", chunk_base);
-  PP.tile_base = up64("pp.tile_base", tile_base);
+  up64(pl.n_chunks, &PP.n_chunks);
+  up64(pl.chunk_len, &PP.chunk_len);
+  up64(chunk_lo, &PP.chunk_lo);
+  up64(chunk_base, &PP.chunk_base);
+  up64(tile_base, &PP.tile_base);
   PP.chunk_len0 = (int)chunk_len0;
   PP.stage = 1;
   if (const char* e = std::getenv("DSG_STAGE")) PP.stage = std::atoi(e) != 0;
@@ -1213,8 +1262,9 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   // a sharded solve lists only this rank's units (virtual shards: one list
   // per rank)
   std::vector<int64_t> rank_items(pl.virt ? pl.world : 1, 0);
+  std::vector<int64_t> pair_off(lat.n_levels + 1, 0);  // staged: lives until the flush
+  const int64_t* pair_off_d = nullptr;
   {
-    std::vector<int64_t> pair_off(lat.n_levels + 1, 0);
     for (int l = 1; l < lat.n_levels; ++l) pair_off[l + 1] = pair_off[l] + pl.n_chunks[l];
     auto runner_level = [&](int l) {
       return runner_max_t > 0 && pl.mode[l] != 0 &&
@@ -1259,7 +1309,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     B.split = crit_ctas > 0 ? 1 : 0;
     PP.crit_ctas = crit_ctas;
     B.n_levels = lat.n_levels;
-    B.pair_off = up64("pp.pair_off", pair_off);
+    up64(pair_off, &pair_off_d);  // into the builds after the flush
     B.n_pairs = pair_off[lat.n_levels];
     B.cnt = ctx.get_t<unsigned long long>(pfx + "pp.item_cnt", 4 * (size_t)lat.n_levels + 1);
     B.items = ctx.get_t<int4>(pfx + "pp.items", (size_t)pl.total_items + 1);
@@ -1269,7 +1319,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
     PP.total_items = pl.total_items;
     PP.crit_end = B.cnt + 2 * (size_t)lat.n_levels - 1;  // end of the last cover key
     pl.items_d = B.items;
-    pl.item_build = B;  // launched after the mode table is on the device
+    pl.item_build = B;  // launched after the plan is on the device
   }
   PP.tile_count = ctx.get_t<unsigned>(pfx + "pp.tile_count", (size_t)pl.total_tiles + 1);
   pl.ctl_words = (size_t)lat.n_levels + 64;
@@ -1284,78 +1334,70 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   PP.vrank = nullptr;
   PP.runner_max_t = runner_max_t;
   PP.runners = runners;
-  auto upload_run = [&](const std::string& name, const std::vector<int4>& v) {
-    int4* d = ctx.get_t<int4>(name, v.size() + 1);
-    if (!v.empty()) {
-      CK(cudaMemcpyAsync(d, v.data(), sizeof(int4) * v.size(), cudaMemcpyHostToDevice, st));
-      ctx.h2d_bytes += (int64_t)(sizeof(int4) * v.size());
-    }
-    return d;
-  };
-  PP.run_items = upload_run(pfx + "pp.run_items", pl.run_lists[0]);
   PP.run_total = (int64_t)pl.run_lists[0].size();
-  {
-    int32_t* mode_d = ctx.get_t<int32_t>(pfx + "pp.mode", pl.mode.size());
-    CK(cudaMemcpyAsync(mode_d, pl.mode.data(), sizeof(int32_t) * pl.mode.size(),
-                       cudaMemcpyHostToDevice, st));
-    PP.mode = mode_d;
-    launch_build_items(PP, pl.item_build, st);
-    if (pl.virt) {
-      // virtual ranks 1..world-1: everything a rank owns on its own GPU
-      pl.vranks.assign(pl.world, VRank{});
-      pl.vranks[0] = VRank{PP.items, pl.total_items, pl.ctl, PP.tile_count, PP.keys, LL.dp,
-                           PP.run_items, PP.run_total};
-      for (int r = 1; r < pl.world; ++r) {
-        const std::string vp = pfx + "v" + std::to_string(r) + ".";
-        ItemBuild B = pl.item_build;
-        B.rank = r;
-        B.items = ctx.get_t<int4>(vp + "items", (size_t)rank_items[r] + 1);
-        launch_build_items(PP, B, st);
-        VRank& v = pl.vranks[r];
-        v.items = B.items;
-        v.total_items = rank_items[r];
-        v.ctl = ctx.get_t<unsigned>(vp + "ctl", pl.ctl_words);
-        v.tile_count = ctx.get_t<unsigned>(vp + "tile_count", (size_t)pl.total_tiles + 1);
-        v.keys = ctx.get_t<unsigned long long>(vp + "keys", (size_t)I * C);
-        v.dp = ctx.get(vp + "dp", (size_t)I * C * vsz + 64);
-        v.run_items = upload_run(vp + "run_items", pl.run_lists[r]);
-        v.run_total = (int64_t)pl.run_lists[r].size();
-      }
-      pl.peer_dp.assign(pl.world, nullptr);
-      pl.peer_bp.assign(pl.world, nullptr);
-      pl.peer_done.assign(pl.world, nullptr);
-      for (int r = 0; r < pl.world; ++r) {
-        pl.peer_dp[r] = pl.vranks[r].dp;
-        pl.peer_done[r] = pl.vranks[r].ctl + 32;
-      }
-      pl.vranks_d = ctx.get_t<VRank>(pfx + "pp.vranks", pl.world);
-      CK(cudaMemcpyAsync(pl.vranks_d, pl.vranks.data(), sizeof(VRank) * pl.world,
-                         cudaMemcpyHostToDevice, st));
-      pl.tables_bad = ctx.get_t<int>(pfx + "pp.tables_bad", 1);
-      PP.virt = 1;
-      PP.vrank = pl.vranks_d;
+  stage.add(pl.run_lists[0], const_cast<int4**>(&PP.run_items));
+  stage.add(pl.mode, const_cast<int32_t**>(&PP.mode));
+  std::vector<ItemBuild> rank_builds;
+  if (pl.virt) {
+    // virtual ranks 1..world-1: everything a rank owns on its own GPU
+    pl.vranks.assign(pl.world, VRank{});
+    rank_builds.assign(pl.world, pl.item_build);
+    for (int r = 1; r < pl.world; ++r) {
+      const std::string vp = pfx + "v" + std::to_string(r) + ".";
+      ItemBuild& B = rank_builds[r];
+      B.rank = r;
+      B.items = ctx.get_t<int4>(vp + "items", (size_t)rank_items[r] + 1);
+      VRank& v = pl.vranks[r];
+      v.items = B.items;
+      v.total_items = rank_items[r];
+      v.ctl = ctx.get_t<unsigned>(vp + "ctl", pl.ctl_words);
+      v.tile_count = ctx.get_t<unsigned>(vp + "tile_count", (size_t)pl.total_tiles + 1);
+      v.keys = ctx.get_t<unsigned long long>(vp + "keys", (size_t)I * C);
+      v.dp = ctx.get(vp + "dp", (size_t)I * C * vsz + 64);
+      v.run_total = (int64_t)pl.run_lists[r].size();
+      stage.add(pl.run_lists[r], const_cast<int4**>(&v.run_items));
     }
-    CK(cudaGetLastError());
-    // checked after the solve's one final synchronisation (pageable H2D
-    // copies are staged before cudaMemcpyAsync returns, so the host
-    // temporaries above may go)
-    D2H(&pl.rbk->cov_bad, cov_err, sizeof(int));
+    pl.tables_bad = ctx.get_t<int>(pfx + "pp.tables_bad", 1);
   }
   // peer tables: this GPU only, until a sharded session attaches its peers
-  if (pl.world == 1) {
+  // (virtual shards: every rank's replica in this process)
+  if (pl.virt) {
+    pl.peer_dp.assign(pl.world, nullptr);
+    pl.peer_bp.assign(pl.world, nullptr);
+    pl.peer_done.assign(pl.world, nullptr);
+    for (int r = 1; r < pl.world; ++r) {
+      pl.peer_dp[r] = pl.vranks[r].dp;
+      pl.peer_done[r] = pl.vranks[r].ctl + 32;
+    }
+    pl.peer_dp[0] = LL.dp;
+    pl.peer_done[0] = PP.done;
+  } else if (pl.world == 1) {
     pl.peer_dp.assign(1, LL.dp);
     pl.peer_bp.assign(1, LL.bp);
     pl.peer_done.assign(1, PP.done);
   }
-  void** pd = ctx.get_t<void*>(pfx + "pp.peer_dp", pl.world);
-  int32_t** pb = ctx.get_t<int32_t*>(pfx + "pp.peer_bp", pl.world);
-  unsigned** pn = ctx.get_t<unsigned*>(pfx + "pp.peer_done", pl.world);
-  CK(cudaMemcpyAsync(pd, pl.peer_dp.data(), sizeof(void*) * pl.world, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(pb, pl.peer_bp.data(), sizeof(int32_t*) * pl.world, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(pn, pl.peer_done.data(), sizeof(unsigned*) * pl.world, cudaMemcpyHostToDevice, st));
-  PP.peer_dp = pd;
-  PP.peer_bp = pb;
-  PP.peer_done = pn;
+  stage.add(pl.peer_dp, const_cast<void***>(&PP.peer_dp));
+  stage.add(pl.peer_bp, const_cast<int32_t***>(&PP.peer_bp));
+  stage.add(pl.peer_done, const_cast<unsigned***>(&PP.peer_done));
+  stage.flush(ctx, pfx, st);  // every table above, one copy
+  // the virtual-rank records hold the (now known) run-list pointers
+  if (pl.virt) {
+    pl.vranks[0] = VRank{PP.items, pl.total_items, pl.ctl, PP.tile_count, PP.keys, LL.dp,
+                         PP.run_items, PP.run_total};
+    pl.vranks_d = ctx.get_t<VRank>(pfx + "pp.vranks", pl.world);
+    VRank* vh = static_cast<VRank*>(ctx.rb(pfx + "vranks", sizeof(VRank) * pl.world));
+    std::memcpy(vh, pl.vranks.data(), sizeof(VRank) * pl.world);
+    CK(cudaMemcpyAsync(pl.vranks_d, vh, sizeof(VRank) * pl.world, cudaMemcpyHostToDevice, st));
+    PP.virt = 1;
+    PP.vrank = pl.vranks_d;
+  }
+  pl.item_build.pair_off = pair_off_d;
+  for (ItemBuild& B : rank_builds) B.pair_off = pair_off_d;
+  launch_build_items(PP, pl.item_build, st);
+  for (int r = 1; pl.virt && r < pl.world; ++r) launch_build_items(PP, rank_builds[r], st);
+  CK(cudaGetLastError());
+  // checked after the solve's one final synchronisation
+  D2H(&pl.rbk->cov_bad, cov_err, sizeof(int));
   PP.rank = pl.rank;
   PP.world = pl.world;
 }
@@ -1458,6 +1500,7 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
       CK(cudaMemsetAsync(PP.trace, 0, sizeof(uint64_t) * n_tr, st));
     }
     CK(cudaEventRecord(ev_desc, st));
+    host_mark("dp-launch");
     launch_persistent(LL, PP, st, &pl.pinfo);
     if (pl.pinfo.launch_error != 0)
       throw Fail{DSG_CUDA_ERROR, std::string("cooperative launch failed: ") +
@@ -1565,7 +1608,9 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
     if (vb == 64) D2H(res->dp_values, dp, sizeof(int64_t) * (size_t)I * C);
   }
   CK(cudaEventRecord(pl_ev_end(ctx), st));
+  host_mark("fin-sync-in");
   CK(cudaStreamSynchronize(st));  // the solve's one synchronisation after the lattice
+  host_mark("fin-sync-out");
   CK(cudaGetLastError());
   const TraceState& tb = rbk.tb;
   const unsigned long long pairs = rbk.pairs;
@@ -1664,13 +1709,16 @@ void solve(int mode, const dsg_graph* graph, const dsg_config* config, const dsg
   dsg_options defaults;
   dsg_default_options(&defaults);
   if (!opt) opt = &defaults;
+  host_mark("solve-start");
   Prepared P = prepare(mode, graph, config, nullptr, false, opt->flags);
+  host_mark("prepared");
   DeviceCtx& ctx = context(opt->device);
   std::lock_guard<std::mutex> lk(ctx.mu);
   CK(cudaSetDevice(ctx.device));
   ctx.h2d_bytes = 0;
   DeviceGraph dg = upload_graph(ctx, P, "g.");
   res->t_prepare_ms = ms_since(t0);
+  host_mark("uploaded");
   Pipeline pl;
   run_device(ctx, P, dg, opt, pl, res, t0, true);
 }
