@@ -1140,6 +1140,33 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   // the runners' finishers wait for chunks only the other CTAs claim: keep
   // the runner off unless most of the grid is left for them
   if (!pl.persistent || pl.pinfo.blocks < 4 * runners * pl.world) runner_max_t = 0;
+  // chain blocks (persistent_impl.cuh): runs of single-target levels whose
+  // predecessor level is single-target too, folded by one runner CTA with the
+  // recent rows in shared memory; the staging area must hold the block state
+  // off by default: measured on C4 (DP 4.86 ms without; 8.6 / 7.2 / 6.5 / 6.7 ms with F = 16 / 8 /
+  // 4 / 2) and C1 (0.33 vs 0.44-0.51 ms) — a chain level costs ~2 us of CTA-wide barriers and
+  // dependent shared-memory steps on an SM shared with six scanning CTAs, more than the L2 hand-off
+  // between runner CTAs it removes
+  int chain_fmax = 0;  // levels folded by a chain level (its old chunks end before them)
+  if (const char* e = std::getenv("DSG_CHAIN_F")) chain_fmax = std::max(0, std::atoi(e));
+  bool chain_on = runner_max_t > 0 && chain_fmax > 0 && !P.repl && C <= kTileTargets;
+  {
+    const int n_stage = (int)std::max(chunk_len0, chunk_len1);
+    const size_t staging = std::getenv("DSG_STAGE") && std::atoi(std::getenv("DSG_STAGE")) == 0
+                               ? 0
+                               : 16 + (size_t)n_stage * (LL.AW * 8 + sizeof(SrcRec) + (size_t)C * vsz) + 32;
+    if (chain_smem_need(C, LL.AW, W, vsz) > staging) chain_on = false;
+  }
+  std::vector<int> chain_f(lat.n_levels, -1);  // F of a chain level, -1: not one
+  for (int s = 3; chain_on && s < lat.n_levels; ++s) {
+    if (lat.level_off[s + 1] - lat.level_off[s] != 1 || lat.level_off[s] - lat.level_off[s - 1] != 1)
+      continue;
+    int F = 0;
+    while (F < std::min(chain_fmax, s - 2) &&
+           lat.level_off[s - 1] - lat.level_off[s - 2 - F] <= kChainSrcMax - 1)
+      ++F;
+    chain_f[s] = F;
+  }
   unsigned poll_ns_max = 128;  // measured: 128 ns <= 256 ns (C1 -4 %, C3 -1 %, C4 -1 %, C2 =) and beats 1 us
   if (const char* e = std::getenv("DSG_CHUNK_LEN")) chunk_len0 = std::max(4, std::atoi(e));
   if (const char* e = std::getenv("DSG_CHUNK_LEN1")) chunk_len1 = std::max(4, std::atoi(e));
@@ -1181,7 +1208,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       // s-2 in chunks of its own, so the item that waits for level s-2 (on
       // the level-to-level chain of a narrow lattice) holds only that
       // level's few sources; then the cover chunk (the finisher)
-      const int G1 = std::max(0, std::min(grade1, s - 2));
+      const int G1 = chain_f[s] >= 0 ? chain_f[s] : std::max(0, std::min(grade1, s - 2));
       const int64_t R = s >= 2 ? lat.level_off[s - 1] : 0;
       const int64_t Rg = s >= 2 ? lat.level_off[s - 1 - G1] : 0;
       chunk_base[s] = (int64_t)chunk_lo.size();
@@ -1196,6 +1223,7 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       while (F < std::min(G1, fold_levels) &&
              lat.level_off[s - 1] - lat.level_off[s - 2 - F] <= fin_fold_max)
         ++F;
+      if (chain_f[s] >= 0) F = chain_f[s];
       pl.mode[s] = 1 + F;
       for (int j = s - 1 - G1; j <= s - 2 - F && G1 > 0; ++j) {
         const int64_t lo = lat.level_off[j], n = lat.level_off[j + 1] - lo;
@@ -1281,18 +1309,48 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
       }
       return total;
     };
-    // the chain runner's lists: the finishers of narrow mode-1 levels, in
-    // level order, per rank (units u % world == rank)
+    // the chain runners' lists, per rank (units u % world == rank): the
+    // finishers of narrow mode-1 levels, and the chain blocks (a chain level
+    // run: up to kChainBlk levels per block, a block's levels' old chunks all
+    // reading levels before the block), in level order; runner i takes
+    // segment i (header: run_items[i].y = start of segment i, i <= runners),
+    // a whole chain in one segment, the rest round-robin
     pl.run_lists.assign(pl.virt ? pl.world : 1, {});
+    int chain_blk = 8;  // levels per chain block (<= persistent_impl.cuh kChainBlk)
+    if (const char* e = std::getenv("DSG_CHAIN_BLK")) chain_blk = std::max(1, std::min(8, std::atoi(e)));
     for (size_t r = 0; r < pl.run_lists.size(); ++r) {
       const int rank = pl.virt ? (int)r : pl.rank;
+      std::vector<std::vector<int4>> seg(runners);
+      int rr = 0;
       for (int l = 1; l < lat.n_levels; ++l) {
         if (!runner_level(l)) continue;
         const int64_t T = lat.level_off[l + 1] - lat.level_off[l];
+        if (chain_f[l] >= 0) {
+          if (rank != 0) continue;  // single-target levels: unit 0, rank 0
+          int b = l;
+          while (b + 1 < lat.n_levels && chain_f[b + 1] >= 0) ++b;
+          auto& sg = seg[rr++ % runners];
+          for (int blk = l; blk <= b;) {
+            int e = blk;
+            while (e + 1 <= b && e + 1 - blk < chain_blk && (e + 1) - 2 - chain_f[e + 1] < blk) ++e;
+            sg.push_back(make_int4(blk, -(e - blk + 1), (int)(pl.n_chunks[blk] - 1), blk - 1));
+            blk = e + 1;
+          }
+          l = b;
+          continue;
+        }
         for (int64_t u = pl.world > 1 ? rank : 0; u < T; u += pl.world)
-          pl.run_lists[r].push_back(make_int4(l, (int)u, (int)(pl.n_chunks[l] - 1), l - 1));
+          seg[rr++ % runners].push_back(make_int4(l, (int)u, (int)(pl.n_chunks[l] - 1), l - 1));
       }
+      std::vector<int4>& out = pl.run_lists[r];
+      out.assign(runners + 1, make_int4(-1, 0, 0, 0));
+      for (int i = 0; i < runners; ++i) {
+        out[i].y = (int)out.size();
+        out.insert(out.end(), seg[i].begin(), seg[i].end());
+      }
+      out[runners].y = (int)out.size();
     }
+    PP.chain = chain_on ? (std::getenv("DSG_CHAIN_DEBUG") ? 2 : 1) : 0;
     for (size_t r = 0; r < rank_items.size(); ++r)
       rank_items[r] = items_of_rank(pl.virt ? (int)r : pl.rank);
     pl.total_items = rank_items[0];

@@ -202,6 +202,7 @@ struct PersistPlan {
   int dead_skip;             // count-only scans of chunks that cannot change a cell
   unsigned poll_ns_max;      // dependency-wait backoff cap
   unsigned fin_poll_ns;    // narrow-level cell polls: backoff cap (0 = spin)
+  int chain;               // runner lists hold chain blocks (persistent_impl.cuh)
   const int64_t* chunk_lo;
   const int64_t* chunk_base;
   const int64_t* tile_base;  // [n_levels] prefix of arrival counters over levels
@@ -273,6 +274,11 @@ struct ItemBuild {
   int4* items;               // [total_items] out
   int rank, world;
 };
+// chain blocks (persistent_impl.cuh): fold sources per chain level, and the
+// shared memory a chain block needs (inside the old-chunk staging area)
+constexpr int kChainSrcMax = 32;
+size_t chain_smem_need(int C, int AW, int W, size_t vsz);
+
 void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t st);
 
 void query_persistent(const LevelLaunch& L, const PersistPlan& P, PersistInfo* info);

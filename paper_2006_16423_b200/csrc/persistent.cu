@@ -134,6 +134,8 @@ __global__ void item_fill_kernel(const PersistPlan p, const ItemBuild b) {
 
 }  // namespace
 
+size_t chain_smem_need(int C, int AW, int W, size_t vsz) { return chain_smem_bytes(C, AW, W, vsz); }
+
 void launch_build_items(const PersistPlan& P, const ItemBuild& B, cudaStream_t st) {
   const int n = 4 * B.n_levels;
   cudaMemsetAsync(B.cnt, 0, sizeof(unsigned long long) * (n + 1), st);

@@ -35,6 +35,7 @@
 // aborts (flag) instead of hanging.
 #include <climits>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "scan.cuh"
@@ -283,6 +284,20 @@ __device__ __forceinline__ int64_t ld_relaxed_v<int64_t>(const int64_t* p) {
 // waiting for the level counter — each cell is one aligned store, so a
 // non-PENDING value is final, and the producer's fence + counter release
 // are off the level-to-level chain.  On stop / watchdog: bail (INF).
+// A poll loop's periodic check (every 64 rounds): a stop raised elsewhere,
+// or this wait past the watchdog (raises the stop).  t0 starts at the first
+// check.
+__device__ __forceinline__ bool poll_abort(const PersistPlan& p, const CtaView& cv, uint64_t& t0) {
+  if (ld_relaxed_sys((const unsigned*)cv.stop) != 0) return true;
+  const uint64_t now = globaltimer();
+  if (!t0) t0 = now;
+  if (now - t0 > kWatchdogNs) {
+    raise_stop(p, cv, true);
+    return true;
+  }
+  return false;
+}
+
 template <typename V>
 __device__ __forceinline__ V ld_final(const PersistPlan& p, const CtaView& cv, const V* q,
                                       bool& bail) {
@@ -445,6 +460,240 @@ __device__ __forceinline__ SrcView<V> stage_sources(const LevelLaunch& a, const 
   return v;
 }
 
+// ---------------------------------------------------------------- chain blocks
+// A run of single-target levels (the long chains of C4 / C1) is one runner
+// CTA's: a chain block item holds up to kChainBlk consecutive levels.  The
+// block's static work is done for all its levels at once — targets, the
+// fold sources (covers + the F most recent levels, F set by the plan) with
+// their block costs, the old chunks' arrivals and merged keys — then the
+// levels run back to back, each folding its sources with the rows of the
+// recent chain levels taken from a shared-memory ring (no L2 round trip on
+// the level-to-level chain), applying monotone_pass (dp_solver.cpp:180-193)
+// and storing its row; the block's levels are released together.  The plan
+// guarantees every old chunk of a block level reads only levels before the
+// block, all released before the block waits for its chunks.
+constexpr int kChainBlk = 8;   // levels per chain block
+constexpr int kChainSrc = kChainSrcMax;  // fold sources per chain level (covers + window)
+constexpr int kChainRing = 32; // rows kept (> any level's fold window)
+
+template <typename V>
+struct ChainSmem {
+  V* ring;           // [kChainRing][C]
+  int64_t* ring_ord; // [kChainRing]
+  int64_t* hdr;      // [kChainBlk][8]: t, chunks, tile, c0, ncov, ex0, n_src, -
+  uint64_t* tgt;     // [kChainBlk][AW]
+  uint64_t* tint;    // [kChainBlk][W] (training)
+  V* keys;           // [kChainBlk][C]
+  int32_t* src;      // [kChainBlk][kChainSrc]
+  V* acc;            // [kChainBlk][kChainSrc]
+  V* cpu;
+  V* mem;
+  V* part;           // [kTileTargets]
+  V* row;            // [2][C] monotone scratch
+};
+
+__host__ __device__ inline size_t chain_smem_bytes(int C, int AW, int W, size_t vsz) {
+  size_t b = 0;
+  auto al = [&](size_t x) { b = (b + 15) & ~(size_t)15; b += x; };
+  al((size_t)kChainRing * C * vsz);
+  al(kChainRing * 8);
+  al(kChainBlk * 8 * 8);
+  al((size_t)kChainBlk * AW * 8);
+  al((size_t)kChainBlk * W * 8);
+  al((size_t)kChainBlk * C * vsz);
+  al(kChainBlk * kChainSrc * 4);
+  al(3 * (size_t)kChainBlk * kChainSrc * vsz);
+  al((size_t)kTileTargets * vsz);
+  al(2 * (size_t)C * vsz);
+  return b + 16;
+}
+
+template <typename V>
+__device__ __forceinline__ ChainSmem<V> chain_smem(unsigned char* base, int C, int AW, int W) {
+  ChainSmem<V> m;
+  size_t b = 0;
+  auto al = [&](size_t x) {
+    b = (b + 15) & ~(size_t)15;
+    unsigned char* r = base + b;
+    b += x;
+    return r;
+  };
+  m.ring = reinterpret_cast<V*>(al((size_t)kChainRing * C * sizeof(V)));
+  m.ring_ord = reinterpret_cast<int64_t*>(al(kChainRing * 8));
+  m.hdr = reinterpret_cast<int64_t*>(al(kChainBlk * 8 * 8));
+  m.tgt = reinterpret_cast<uint64_t*>(al((size_t)kChainBlk * AW * 8));
+  m.tint = reinterpret_cast<uint64_t*>(al((size_t)kChainBlk * W * 8));
+  m.keys = reinterpret_cast<V*>(al((size_t)kChainBlk * C * sizeof(V)));
+  m.src = reinterpret_cast<int32_t*>(al(kChainBlk * kChainSrc * 4));
+  m.acc = reinterpret_cast<V*>(al(3 * (size_t)kChainBlk * kChainSrc * sizeof(V)));  // acc | cpu | mem
+  m.cpu = m.acc + kChainBlk * kChainSrc;
+  m.mem = m.cpu + kChainBlk * kChainSrc;
+  m.part = reinterpret_cast<V*>(al((size_t)kTileTargets * sizeof(V)));
+  m.row = reinterpret_cast<V*>(al(2 * (size_t)C * sizeof(V)));
+  return m;
+}
+
+// One chain block: levels [sb, sb + nl).  Returns false when the solve
+// stopped (deadline / watchdog / another rank).
+template <typename V, bool TRAIN>
+__device__ __forceinline__ bool chain_block(const LevelLaunch& a, const PersistPlan& p, const CtaView& cv,
+                                         int sb, int nl, unsigned char* area, unsigned& nested,
+                                         uint64_t* tr_mid) {
+  constexpr V INF = VTraits<V>::INF;
+  const int tid = threadIdx.x;
+  const int C = a.C, AW = a.AW, W = a.W, lp1 = a.L + 1;
+  const ChainSmem<V> m = chain_smem<V>(area, C, AW, W);
+  // level headers
+  if (tid < nl) {
+    const int s = sb + tid;
+    const int64_t t = p.level_off[s];
+    const int mode = p.mode[s];
+    const int64_t c0 = __ldg(a.cov_off + t);
+    const int64_t ncov = __ldg(a.cov_off + t + 1) - c0;
+    const int64_t ex0 = p.level_off[s - mode], ex1 = p.level_off[s - 1];
+    int64_t* h = m.hdr + tid * 8;
+    h[0] = t;
+    h[1] = p.n_chunks[s];
+    h[2] = p.tile_base[s];
+    h[3] = c0;
+    h[4] = ncov;
+    h[5] = ex0;
+    h[6] = min((int64_t)kChainSrc, ncov + (ex1 - ex0));
+    if (ncov + (ex1 - ex0) > kChainSrc) raise_stop(p, cv, true);  // the plan keeps it <= kChainSrc
+  }
+  __syncthreads();
+  // target bitsets
+  for (int i = tid; i < nl * AW; i += kTileTargets) {
+    const int lv = i / AW, w = i % AW;
+    m.tgt[i] = __ldg(a.abits + (size_t)m.hdr[lv * 8] * AW + w);
+  }
+  if (TRAIN)
+    for (int i = tid; i < nl * W; i += kTileTargets) {
+      const int lv = i / W, w = i % W;
+      m.tint[i] = __ldg(a.intbits + (size_t)m.hdr[lv * 8] * W + w);
+    }
+  __syncthreads();
+  // fold sources of every level: subset test and block costs (K2 + K3)
+  for (int i = tid; i < nl * kChainSrc; i += kTileTargets) {
+    const int lv = i / kChainSrc, j = i % kChainSrc;
+    const int64_t* h = m.hdr + lv * 8;
+    if (j >= h[6]) continue;
+    const int64_t src = j < h[4] ? (int64_t)__ldg(a.cov + h[3] + j) : h[5] + (j - h[4]);
+    const Target<V> x = target_scalars<V, TRAIN>(a, h[0], 0, true);
+    const PrePair<V> q = pre_pair<V, TRAIN, 1>(a, x, src, m.tgt + lv * AW, m.tint + lv * W);
+    m.src[i] = q.ok ? (int32_t)src : -1;
+    m.acc[i] = q.acc;
+    m.cpu[i] = q.cpu;
+    m.mem[i] = q.mem_blk;
+    nested += q.nested ? 1u : 0u;
+  }
+  if (p.trace) tr_mid[0] = globaltimer();
+  // the old chunks' merges (their sources all precede the block, released)
+  __shared__ int s_cok;
+  if (tid == 0) s_cok = 1;
+  __syncthreads();
+  if (tid < nl) {
+    const int64_t* h = m.hdr + tid * 8;
+    const unsigned need = (unsigned)(h[1] - 1);
+    const unsigned* c = cv.tile_count + h[2];
+    if (need > 0 && ld_relaxed(c) < need) {
+      uint64_t t0 = 0;
+      for (unsigned polls = 0; ld_relaxed(c) < need; ++polls) {
+        __nanosleep(64);
+        if ((polls & 63) == 63 && poll_abort(p, cv, t0)) {
+          s_cok = 0;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (!s_cok) return false;
+  for (int i = tid; i < nl * C; i += kTileTargets) {
+    const int lv = i / C, c = i % C;
+    m.keys[i] = __ldcg(reinterpret_cast<const V*>(cv.keys) + (size_t)m.hdr[lv * 8] * C + c);
+  }
+  __syncthreads();
+  if (p.trace) tr_mid[1] = globaltimer();
+  const V* dpm = reinterpret_cast<const V*>(cv.dp);
+  const int G = max(1, kTileTargets / C);
+  const int my_g = tid / C, my_c = tid % C;
+  for (int lv = 0; lv < nl; ++lv) {
+    const int64_t* h = m.hdr + lv * 8;
+    const int64_t t = h[0];
+    const int nsrc = (int)h[6];
+    const int32_t* fs = m.src + lv * kChainSrc;
+    const V* fa = m.acc + lv * kChainSrc;
+    const V* fc = m.cpu + lv * kChainSrc;
+    // fold: threads over (cell, source group)
+    bool bail = false;
+    if (my_g < G && tid < G * C) {
+      const int c = my_c, k = c / lp1, l = c % lp1;
+      V v = INF;
+      for (int j = my_g; j < nsrc; j += G) {
+        const int32_t src = fs[j];
+        if (src < 0) continue;
+        const int slot = (int)(src % kChainRing);
+        V ra, rc;
+        if (m.ring_ord[slot] == src) {
+          const V* row = m.ring + (size_t)slot * C;
+          ra = k >= 1 ? row[c - lp1] : INF;
+          rc = l >= 1 ? row[c - 1] : INF;
+        } else {
+          const V* row = dpm + (size_t)src * C;
+          ra = k >= 1 && fa[j] != INF ? ld_final(p, cv, row + c - lp1, bail) : INF;
+          rc = l >= 1 ? ld_final(p, cv, row + c - 1, bail) : INF;
+        }
+        if (k >= 1 && fa[j] != INF) v = min(v, vmax(ra, fa[j]));
+        if (l >= 1) v = min(v, vmax(rc, fc[j]));
+      }
+      m.part[tid] = v;
+    }
+    if (__syncthreads_or(bail)) return false;
+    // merge the groups with the keys, then monotone_pass: row pass (over l),
+    // column pass (over k)
+    V* r0 = m.row;
+    V* r1 = m.row + C;
+    for (int c = tid; c < C; c += kTileTargets) {
+      V v = m.keys[lv * C + c];
+      for (int g = 0; g < G; ++g) v = min(v, m.part[g * C + c]);
+      r0[c] = v;
+    }
+    __syncthreads();
+    for (int c = tid; c < C; c += kTileTargets) {
+      const int l = c % lp1;
+      V v = r0[c];
+      for (int ll = 1; ll <= l; ++ll) v = min(v, r0[c - ll]);
+      r1[c] = v;
+    }
+    __syncthreads();
+    const int slot = (int)(t % kChainRing);
+    for (int c = tid; c < C; c += kTileTargets) {
+      const int k = c / lp1;
+      V v = r1[c];
+      for (int kk = 1; kk <= k; ++kk) v = min(v, r1[c - kk * lp1]);
+      m.ring[(size_t)slot * C + c] = v;
+      if (p.world == 1) const_cast<V*>(dpm)[(size_t)t * C + c] = v;
+      else
+        for (int r = 0; r < p.world; ++r) ((V*)p.peer_dp[r])[(size_t)t * C + c] = v;
+    }
+    if (tid == 0) m.ring_ord[slot] = t;
+    __syncthreads();
+  }
+  // release the block's levels (one fence for all)
+  if (tid == 0) {
+    if (p.world == 1) {
+      __threadfence();
+      for (int lv = 0; lv < nl; ++lv) atomicAdd(p.peer_done[0] + sb + lv, 1u);
+    } else {
+      __threadfence_system();
+      for (int lv = 0; lv < nl; ++lv)
+        for (int r = 0; r < p.world; ++r) atomicAdd_system(p.peer_done[r] + sb + lv, 1u);
+    }
+  }
+  return true;
+}
+
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
 __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const PersistPlan& p) {
   constexpr V INF = VTraits<V>::INF;
@@ -493,11 +742,12 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       cv.stop = reinterpret_cast<int*>(vr.ctl);
       cv.rank = r;
       cv.run_items = vr.run_items;
-      // CTAs r, r + world, ... (the first `runners`) run rank r's chain
+      // CTAs r, r + world, ... (the first `runners`) run rank r's runner
+      // segments (header: run_items[i].y = start of segment i)
       const int ri = (int)(blockIdx.x / (unsigned)p.world);
-      cv.run_total = ri < p.runners ? vr.run_total : 0;
-      cv.run_first = ri;
-      cv.run_step = p.runners;
+      cv.run_first = ri < p.runners && vr.run_total > 0 ? __ldg(vr.run_items + ri).y : 0;
+      cv.run_total = ri < p.runners && vr.run_total > 0 ? __ldg(vr.run_items + ri + 1).y : 0;
+      cv.run_step = 1;
     } else {
       cv.items = p.items;
       cv.total_items = p.total_items;
@@ -509,12 +759,19 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       cv.stop = p.stop;
       cv.rank = p.rank;
       cv.run_items = p.run_items;
-      cv.run_total = (int)blockIdx.x < p.runners ? p.run_total : 0;
-      cv.run_first = (int)blockIdx.x;
-      cv.run_step = p.runners;
+      const int ri = (int)blockIdx.x;
+      cv.run_first = ri < p.runners && p.run_total > 0 ? __ldg(p.run_items + ri).y : 0;
+      cv.run_total = ri < p.runners && p.run_total > 0 ? __ldg(p.run_items + ri + 1).y : 0;
+      cv.run_step = 1;
     }
   }
   __syncthreads();
+  // chain blocks: an empty row ring (shared memory is not cleared at launch)
+  if (p.chain && cv.run_total > cv.run_first) {
+    int64_t* ro = chain_smem<V>(st_area, a.C, a.AW, W).ring_ord;  // chain_block's layout (a.C)
+    for (int i = tid; i < kChainRing; i += kTileTargets) ro[i] = -1;
+    __syncthreads();
+  }
   // Roles: with crit_ctas > 0 the list starts with the cover items (they gate
   // the levels) and the first crit_ctas CTAs claim only those, so a level's
   // critical work never queues behind ready background work; the other CTAs
@@ -555,6 +812,27 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
                   : gi < 0         ? LLONG_MIN
                                    : (long long)(q_lo + atomicAdd(ctr, 1ull));
       if (rp < cv.run_total) s_run_pos = rp + cv.run_step;
+    }
+    if (item.y < 0) {
+      // a chain block (runner lists only)
+      const uint64_t tc0 = p.trace ? globaltimer() : 0;
+      uint64_t tmid[2] = {0, 0};
+      if (!chain_block<V, TRAIN>(a, p, cv, item.x, -item.y, st_area, nested_total, tmid)) break;
+      __syncthreads();
+      if (p.trace && tid == 0) {
+        // start, static part done, chunk merges read, end
+        uint64_t* tr = p.trace + (cv.total_items + (-gi - 1)) * 4;
+        tr[0] = tc0;
+        tr[1] = tmid[0];
+        tr[2] = tmid[1];
+        tr[3] = globaltimer() | (1ull << 63);
+      }
+      if (tid == 0) {
+        const long long ng = s_next_gi;
+        s_gi = ng == LLONG_MIN ? (long long)(q_lo + atomicAdd(ctr, 1ull)) : ng;
+      }
+      __syncthreads();
+      continue;
     }
     const int s = item.x;
     const int64_t unit = item.y;
