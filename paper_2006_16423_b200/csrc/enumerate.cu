@@ -386,6 +386,74 @@ __device__ void expand_resident(const EnumArgs& a, int64_t* lo_io, int64_t* hi_i
     team_sync<TEAM>();
   }
   while (true) {
+    if (TEAM == 32 && hi - lo == 1 && W <= 32) {
+      // A level holding ONE ideal: each of its children is canonical (the
+      // child's canonical parent has this level's size, so it is this
+      // ideal).  While the ideal has exactly one addable node the next level
+      // is that single child: walk such chains with one lane per bitset word
+      // (registers, no phase barriers), then continue generically.
+      const int w = r;
+      uint64_t J = 0, M = 0, A = 0;
+      if (w < W) {
+        J = par[w];
+        M = par[W + w];
+        A = par[2 * W + w];
+      }
+      bool moved = false;
+      while (true) {
+        const unsigned cnt = __reduce_add_sync(0xffffffffu, (unsigned)__popcll(A));
+        if (cnt != 1u || hi + 1 > a.budget || hi + 1 > a.cap) break;
+        const unsigned has = __ballot_sync(0xffffffffu, A != 0ull);
+        const int lw = __ffs((int)has) - 1;
+        const uint64_t aw = __shfl_sync(0xffffffffu, A, lw);
+        const int v = (lw << 6) | (__ffsll((long long)aw) - 1);
+        const uint64_t bx = w == (v >> 6) ? 1ull << (v & 63) : 0ull;
+        // max(J ∪ v) = (max(J) \ pred(v)) ∪ {v}; add = (add(J) \ {v}) ∪
+        // {y ∈ succ(v) : pred(y) ⊆ J ∪ {v}}
+        J |= bx;
+        for (int e = pu_off[v], e1 = pu_off[v + 1]; e < e1; ++e) {
+          const int u = pu_adj[e];
+          if ((u >> 6) == w) M &= ~(1ull << (u & 63));
+        }
+        M |= bx;
+        A &= ~bx;
+        for (int e = su_off[v], e1 = su_off[v + 1]; e < e1; ++e) {
+          const int y = su_adj[e];
+          bool miss = false;
+          for (int f = pu_off[y], f1 = pu_off[y + 1]; f < f1; ++f) {
+            const int u = pu_adj[f];
+            miss |= (u >> 6) == w && !((J >> (u & 63)) & 1ull);
+          }
+          if (!__any_sync(0xffffffffu, miss) && (y >> 6) == w) A |= 1ull << (y & 63);
+        }
+        const int64_t slot = hi;
+        if (w < W) {
+          a.bits[slot * W + w] = J;
+          a.maxm[slot * W + w] = M;
+          a.addm[slot * W + w] = A;
+        }
+        if (w == 0) {
+          a.level_of[slot] = level + 1;
+          a.level_off[level + 2] = hi + 1;
+        }
+        lo = hi;
+        hi = hi + 1;
+        ++level;
+        moved = true;
+      }
+      if (moved) {
+        // the generic step continues from this single ideal
+        if (w < W) {
+          par[w] = J;
+          par[W + w] = M;
+          par[2 * W + w] = A;
+        }
+        const int tb = M ? (w << 6) | (63 - __clzll((long long)M)) : -1;
+        const int top = __reduce_max_sync(0xffffffffu, tb);
+        if (w == 0) top_p[0] = top;
+        __syncwarp();
+      }
+    }
     const int nP = (int)(hi - lo);
     int* nc = s_nc + par_nc;
     // phase A: canonical candidates
