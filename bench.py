@@ -72,8 +72,10 @@ def sample_workload(name: str):
 
 def full_size_reference(name: str):
     """The unmodified reference's full-size solve of this workload on the
-    bench host (tools/cpu_ref_host.sh, committed under profiles/), if any."""
+    bench host (tools/cpu_ref_host.sh, committed under profiles/), if any
+    (the @int64 tag changes the device value width only)."""
     import glob
+    name = name.replace("@int64", "")
     for path in glob.glob(os.path.join(HOST_REF_DIR, "*.json")):
         try:
             for r in json.load(open(path)):
@@ -289,7 +291,7 @@ def run_ours(args, world, rank, local):
     w = workload(args.workload)
     mode = 1 if w.training else 0
     nv, n_ideals, pairs_cf = w.counts
-    flags = _abi.DSG_FLAG_TIME_KERNELS
+    flags = _abi.DSG_FLAG_TIME_KERNELS | w.flags
     opt = solver.SolveOptions(flags=flags, device=local)
     sharded = world > 1
     if sharded:
@@ -342,7 +344,7 @@ def run_ours(args, world, rank, local):
     _abi.pod_graph(w.graph)
     python_flatten_ms = 1e3 * (time.perf_counter() - t)
     if not sharded:
-        solver.run_dp(lib, "dsg", mode, w.graph, w.config, solver.SolveOptions(device=local))
+        solver.run_dp(lib, "dsg", mode, w.graph, w.config, solver.SolveOptions(device=local, flags=w.flags))
     for i in range(max(1, args.steps)):
         barrier_sync(world)
         t = time.perf_counter()
@@ -351,7 +353,7 @@ def run_ours(args, world, rank, local):
             raw = sess.run()
             h2d.append(up["h2d_bytes"])
         else:
-            raw = solver.run_dp(lib, "dsg", mode, w.graph, w.config, solver.SolveOptions(device=local))
+            raw = solver.run_dp(lib, "dsg", mode, w.graph, w.config, solver.SolveOptions(device=local, flags=w.flags))
             h2d.append(raw.stats["h2d_bytes"])
             parts["host_prepare_ms"].append(raw.stats["t_prepare_ms"])
         t_call = time.perf_counter()

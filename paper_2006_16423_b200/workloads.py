@@ -11,6 +11,7 @@
 """
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 from fractions import Fraction
 from typing import List, Optional, Sequence, Tuple
@@ -233,6 +234,7 @@ class Workload:
     training: bool
     spec: ChainSpec
     description: str
+    flags: int = 0  # extra dsg_options flags (the @int64 tag: DSG_FLAG_FORCE_INT64)
 
     @property
     def counts(self):
@@ -289,14 +291,18 @@ def standin(name: str, seed: int = 1, decimals: int = 1) -> Workload:
 
 def by_name(name: str) -> Workload:
     """Workload names used by bench.py and the tools: C1..C4, optionally
-    suffixed @seedN / @D1000 (weight draw), or C5:w,c,M,stem (sweep point)."""
+    suffixed @seedN / @D1000 (weight draw) / @int64 (64-bit values forced),
+    or C5:w,c,M,stem (sweep point)."""
     if name.startswith("C5"):
         pt = tuple(int(x) for x in name[3:].split(","))
         return sweep(*pt)
     base, *tags = name.split("@")
-    seed, decimals = 1, 1
+    seed, decimals, flags = 1, 1, 0
     for t in tags:
-        if t.startswith("seed"):
+        if t == "int64":
+            from . import _abi
+            flags |= _abi.DSG_FLAG_FORCE_INT64
+        elif t.startswith("seed"):
             seed = int(t[4:])
         elif t.startswith("D"):
             d = int(t[1:])
@@ -305,7 +311,10 @@ def by_name(name: str) -> Workload:
                 raise ValueError(f"weight denominator must be a power of 10: {name}")
         else:
             raise ValueError(f"unknown workload tag {t!r} in {name!r}")
-    return standin(base, seed=seed, decimals=decimals)
+    w = standin(base, seed=seed, decimals=decimals)
+    if flags:
+        w = dataclasses.replace(w, name=name, flags=flags)
+    return w
 
 
 def sweep(width: int, chain: int, modules: int, stem: int, k: int = 8, l: int = 0,
