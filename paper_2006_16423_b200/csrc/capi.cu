@@ -1685,8 +1685,11 @@ void phase2(DeviceCtx& ctx, const Prepared& P, const dsg_options* opt, Pipeline&
     for (size_t i = 0; i < tmp.size(); ++i)
       res->dp_values[i] = tmp[i] == VTraits<int32_t>::INF ? INT64_MAX : (int64_t)tmp[i];
   }
-  float dp_ms = 0;
+  float dp_ms = 0, tb_ms = 0;
   cudaEventElapsedTime(&dp_ms, ev_desc, ev_dp);
+  // traceback + result copies: the dp pass's end to the pipeline's end event
+  cudaEventElapsedTime(&tb_ms, ev_dp, pl_ev_end(ctx));
+  res->t_traceback_ms = tb_ms;
   double kern_ms = 0;
   for (size_t i = 0; i + 1 < kev.size(); i += 2) {
     float x = 0;

@@ -80,3 +80,37 @@ def test_above_maximum_size_is_unsupported(gpu):
     g, *_ = random_path(4097, 1)
     with pytest.raises(Unsupported):
         solver.solve_maxload_inference(g, DeviceConfig(2, 0, 10 ** 6))
+
+
+def _coprime_chain(dens):
+    from fractions import Fraction as F
+    from paper_2006_16423_b200.graph import Edge, Node
+    nodes = [Node(i + 1, F(1, d), F(1, d), F(1, d), F(1, d)) for i, d in enumerate(dens)]
+    return Graph(nodes, [Edge(i + 1, i + 2) for i in range(len(dens) - 1)])
+
+
+@pytest.mark.parametrize("dens", [[2097143, 2097091], [2 ** 20, 3 ** 12, 5 ** 8]])
+def test_large_denominators_match_oracle(gpu, dens):
+    """Weights whose common denominator is large but <= 2^62: exact, on the
+    int64 path, equal to the reference (rational.cpp arithmetic)."""
+    from fractions import Fraction as F
+    g = _coprime_chain(dens)
+    cfg = DeviceConfig(accelerators=2, memory_limit=F(10))
+    split = solver.solve_maxload_inference(g, cfg)
+    assert split.stats["value_bits"] == 64
+    assert split.objective_value == ob.dp("port", 0, g, cfg).objective
+    assert not verify_split(g, cfg, split)
+
+
+def test_common_denominator_above_2_62_is_overflow(gpu):
+    """The documented boundary of the fixed-point design: three
+    ~2^21 primes as weight denominators give a common denominator ~2^63.  The
+    reference still solves this instance (its Rat reduces pairwise sums), the
+    B200 path reports std::overflow_error (DSG_OVERFLOW) instead of a wrong
+    value."""
+    from fractions import Fraction as F
+    g = _coprime_chain([2097143, 2097091, 2097083])
+    cfg = DeviceConfig(accelerators=2, memory_limit=F(10))
+    assert ob.dp("port", 0, g, cfg).objective == F(6291377, 4397899711013)
+    with pytest.raises(OverflowError):
+        solver.solve_maxload_inference(g, cfg)
