@@ -309,8 +309,10 @@ def _replicated(load: Num, mem: Num, r: int, config: DeviceConfig) -> Num:
 def make_canonical_split(g: Graph, config: DeviceConfig, blocks: List[SplitBlock],
                          objective: Num) -> Split:
     """graph.cpp:573-621: accelerators first, each kind by smallest external id."""
+    ids = [n.id for n in g.nodes()]
+
     def smallest_id(b: SplitBlock) -> int:
-        return min((g.id_of(v) for v in b.members), default=2 ** 31 - 1)
+        return min(map(ids.__getitem__, b.members), default=2 ** 31 - 1)
 
     blocks = sorted(blocks, key=lambda b: (b.cpu, smallest_id(b)))  # stable
     split = Split(objective_value=objective)
@@ -319,8 +321,7 @@ def make_canonical_split(g: Graph, config: DeviceConfig, blocks: List[SplitBlock
         if not b.members:
             continue
         pl = Placement.cpu(next_cpu) if b.cpu else Placement.acc(next_acc)
-        for v in b.members:
-            split.assignment[g.id_of(v)] = pl
+        split.assignment.update(dict.fromkeys(map(ids.__getitem__, b.members), pl))
         if b.load is not None:
             load = b.load  # recomputed on the device (dsg_block::load_num)
         else:

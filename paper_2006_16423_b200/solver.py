@@ -99,9 +99,14 @@ STAT_FIELDS = ("t_prepare_ms", "t_enumerate_ms", "t_describe_ms", "t_dp_ms", "t_
 
 def _raw_from(res, config: DeviceConfig) -> RawResult:
     blocks = []
+    n_mem = 0
+    for b in range(res.n_blocks):
+        n_mem = max(n_mem, res.blocks[b].offset + res.blocks[b].n_members)
+    # one view of the member array (per-element ctypes indexing costs ~0.1 us each)
+    mem = np.ctypeslib.as_array(res.members, shape=(n_mem,)).tolist() if n_mem else []
     for b in range(res.n_blocks):
         blk = res.blocks[b]
-        members = [res.members[blk.offset + i] for i in range(blk.n_members)]
+        members = mem[blk.offset:blk.offset + blk.n_members]
         load = None
         if res.block_loads:
             load = INF if blk.load_num == _I64_MAX else Fraction(blk.load_num, res.denominator)

@@ -12,7 +12,8 @@ from paper_2006_16423_b200 import solver, workloads as wl  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 15
 w = wl.by_name(name)
-s = solver.Session(1 if w.training else 0, w.graph, w.config, solver.SolveOptions())
+s = solver.Session(1 if w.training else 0, w.graph, w.config,
+                   solver.SolveOptions(max_blocks=int(os.environ.get("DSG_KNOB_BLOCKS", "0")), flags=w.flags))
 dp, dev = [], []
 for i in range(reps + 3):
     r = s.run()
