@@ -89,6 +89,7 @@ def _coprime_chain(dens):
     return Graph(nodes, [Edge(i + 1, i + 2) for i in range(len(dens) - 1)])
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("dens", [[2097143, 2097091], [2 ** 20, 3 ** 12, 5 ** 8]])
 def test_large_denominators_match_oracle(gpu, dens):
     """Weights whose common denominator is large but <= 2^62: exact, on the
@@ -102,6 +103,7 @@ def test_large_denominators_match_oracle(gpu, dens):
     assert not verify_split(g, cfg, split)
 
 
+@pytest.mark.gpu
 def test_common_denominator_above_2_62_is_overflow(gpu):
     """The documented boundary of the fixed-point design: three
     ~2^21 primes as weight denominators give a common denominator ~2^63.  The
