@@ -1333,7 +1333,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
           for (int blk = l; blk <= b;) {
             int e = blk;
             while (e + 1 <= b && e + 1 - blk < chain_blk && (e + 1) - 2 - chain_f[e + 1] < blk) ++e;
-            sg.push_back(make_int4(blk, -(e - blk + 1), (int)(pl.n_chunks[blk] - 1), blk - 1));
+            // .w: the run's first level (its rows onwards sit in the runner's ring)
+            sg.push_back(make_int4(blk, -(e - blk + 1), (int)(pl.n_chunks[blk] - 1), l));
             blk = e + 1;
           }
           l = b;

@@ -485,6 +485,7 @@ struct ChainSmem {
   uint64_t* tint;    // [kChainBlk][W] (training)
   V* keys;           // [kChainBlk][C]
   int32_t* src;      // [kChainBlk][kChainSrc]
+  int32_t* slot;     // [kChainBlk][kChainSrc] ring row of the source, -1: global
   V* acc;            // [kChainBlk][kChainSrc]
   V* cpu;
   V* mem;
@@ -501,6 +502,7 @@ __host__ __device__ inline size_t chain_smem_bytes(int C, int AW, int W, size_t 
   al((size_t)kChainBlk * AW * 8);
   al((size_t)kChainBlk * W * 8);
   al((size_t)kChainBlk * C * vsz);
+  al(kChainBlk * kChainSrc * 4);
   al(kChainBlk * kChainSrc * 4);
   al(3 * (size_t)kChainBlk * kChainSrc * vsz);
   al((size_t)kTileTargets * vsz);
@@ -525,6 +527,7 @@ __device__ __forceinline__ ChainSmem<V> chain_smem(unsigned char* base, int C, i
   m.tint = reinterpret_cast<uint64_t*>(al((size_t)kChainBlk * W * 8));
   m.keys = reinterpret_cast<V*>(al((size_t)kChainBlk * C * sizeof(V)));
   m.src = reinterpret_cast<int32_t*>(al(kChainBlk * kChainSrc * 4));
+  m.slot = reinterpret_cast<int32_t*>(al(kChainBlk * kChainSrc * 4));
   m.acc = reinterpret_cast<V*>(al(3 * (size_t)kChainBlk * kChainSrc * sizeof(V)));  // acc | cpu | mem
   m.cpu = m.acc + kChainBlk * kChainSrc;
   m.mem = m.cpu + kChainBlk * kChainSrc;
@@ -537,8 +540,8 @@ __device__ __forceinline__ ChainSmem<V> chain_smem(unsigned char* base, int C, i
 // stopped (deadline / watchdog / another rank).
 template <typename V, bool TRAIN>
 __device__ __forceinline__ bool chain_block(const LevelLaunch& a, const PersistPlan& p, const CtaView& cv,
-                                         int sb, int nl, unsigned char* area, unsigned& nested,
-                                         uint64_t* tr_mid) {
+                                         int sb, int nl, int run_lvl, unsigned char* area,
+                                         unsigned& nested, uint64_t* tr_mid) {
   constexpr V INF = VTraits<V>::INF;
   const int tid = threadIdx.x;
   const int C = a.C, AW = a.AW, W = a.W, lp1 = a.L + 1;
@@ -574,6 +577,7 @@ __device__ __forceinline__ bool chain_block(const LevelLaunch& a, const PersistP
     }
   __syncthreads();
   // fold sources of every level: subset test and block costs (K2 + K3)
+  const int64_t ring_lo = p.level_off[run_lvl];
   for (int i = tid; i < nl * kChainSrc; i += kTileTargets) {
     const int lv = i / kChainSrc, j = i % kChainSrc;
     const int64_t* h = m.hdr + lv * 8;
@@ -582,6 +586,9 @@ __device__ __forceinline__ bool chain_block(const LevelLaunch& a, const PersistP
     const Target<V> x = target_scalars<V, TRAIN>(a, h[0], 0, true);
     const PrePair<V> q = pre_pair<V, TRAIN, 1>(a, x, src, m.tgt + lv * AW, m.tint + lv * W);
     m.src[i] = q.ok ? (int32_t)src : -1;
+    // rows of this run's earlier levels are in the ring (this CTA computed
+    // them, in order); older rows come from the global table
+    m.slot[i] = src >= ring_lo && src < h[0] ? (int32_t)(src % kChainRing) : -1;
     m.acc[i] = q.acc;
     m.cpu[i] = q.cpu;
     m.mem[i] = q.mem_blk;
@@ -618,66 +625,80 @@ __device__ __forceinline__ bool chain_block(const LevelLaunch& a, const PersistP
   const V* dpm = reinterpret_cast<const V*>(cv.dp);
   const int G = max(1, kTileTargets / C);
   const int my_g = tid / C, my_c = tid % C;
+  const bool folder = my_g < G;  // a (cell, source group) of the fold
+  const int ck = my_c / lp1, cl = my_c % lp1;
+  const int offa = ck >= 1 ? my_c - lp1 : 0, offc = cl >= 1 ? my_c - 1 : 0;
   for (int lv = 0; lv < nl; ++lv) {
-    const int64_t* h = m.hdr + lv * 8;
-    const int64_t t = h[0];
-    const int nsrc = (int)h[6];
+    const int64_t t = m.hdr[lv * 8];
+    const int nsrc = (int)m.hdr[lv * 8 + 6];
     const int32_t* fs = m.src + lv * kChainSrc;
+    const int32_t* fsl = m.slot + lv * kChainSrc;
     const V* fa = m.acc + lv * kChainSrc;
     const V* fc = m.cpu + lv * kChainSrc;
-    // fold: threads over (cell, source group)
     bool bail = false;
-    if (my_g < G && tid < G * C) {
-      const int c = my_c, k = c / lp1, l = c % lp1;
+    if (folder) {
       V v = INF;
+      // ring rows first: 4 sources per round, every shared load of the round
+      // issued before any is used (no per-source branch) ...
+      for (int j0 = my_g; j0 < nsrc; j0 += 4 * G) {
+        int sl[4];
+        V xa[4], xc[4], ra[4], rc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * G;
+          const bool in = j < nsrc;
+          sl[u] = in ? fsl[j] : -1;
+          xa[u] = in ? fa[j] : INF;
+          xc[u] = in ? fc[j] : INF;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const V* row = m.ring + (size_t)(sl[u] < 0 ? 0 : sl[u]) * C;
+          ra[u] = row[offa];
+          rc[u] = row[offc];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (sl[u] < 0) continue;
+          if (ck >= 1 && xa[u] != INF) v = min(v, vmax(ra[u], xa[u]));
+          if (cl >= 1) v = min(v, vmax(rc[u], xc[u]));
+        }
+      }
+      // ... then the rows from before the run (global, final or polled)
       for (int j = my_g; j < nsrc; j += G) {
         const int32_t src = fs[j];
-        if (src < 0) continue;
-        const int slot = (int)(src % kChainRing);
-        V ra, rc;
-        if (m.ring_ord[slot] == src) {
-          const V* row = m.ring + (size_t)slot * C;
-          ra = k >= 1 ? row[c - lp1] : INF;
-          rc = l >= 1 ? row[c - 1] : INF;
-        } else {
-          const V* row = dpm + (size_t)src * C;
-          ra = k >= 1 && fa[j] != INF ? ld_final(p, cv, row + c - lp1, bail) : INF;
-          rc = l >= 1 ? ld_final(p, cv, row + c - 1, bail) : INF;
-        }
-        if (k >= 1 && fa[j] != INF) v = min(v, vmax(ra, fa[j]));
-        if (l >= 1) v = min(v, vmax(rc, fc[j]));
+        if (src < 0 || fsl[j] >= 0) continue;
+        const V* row = dpm + (size_t)src * C;
+        if (ck >= 1 && fa[j] != INF) v = min(v, vmax(ld_final(p, cv, row + offa, bail), fa[j]));
+        if (cl >= 1) v = min(v, vmax(ld_final(p, cv, row + offc, bail), fc[j]));
       }
       m.part[tid] = v;
     }
     if (__syncthreads_or(bail)) return false;
     // merge the groups with the keys, then monotone_pass: row pass (over l),
-    // column pass (over k)
+    // column pass (over k); thread c < C keeps cell c
     V* r0 = m.row;
     V* r1 = m.row + C;
-    for (int c = tid; c < C; c += kTileTargets) {
-      V v = m.keys[lv * C + c];
-      for (int g = 0; g < G; ++g) v = min(v, m.part[g * C + c]);
-      r0[c] = v;
+    if (tid < C) {
+      V v = m.keys[lv * C + tid];
+      for (int g = 0; g < G; ++g) v = min(v, m.part[g * C + tid]);
+      r0[tid] = v;
     }
     __syncthreads();
-    for (int c = tid; c < C; c += kTileTargets) {
-      const int l = c % lp1;
-      V v = r0[c];
-      for (int ll = 1; ll <= l; ++ll) v = min(v, r0[c - ll]);
-      r1[c] = v;
+    if (tid < C) {
+      V v = r0[tid];
+      for (int ll = 1; ll <= cl; ++ll) v = min(v, r0[tid - ll]);
+      r1[tid] = v;
     }
     __syncthreads();
-    const int slot = (int)(t % kChainRing);
-    for (int c = tid; c < C; c += kTileTargets) {
-      const int k = c / lp1;
-      V v = r1[c];
-      for (int kk = 1; kk <= k; ++kk) v = min(v, r1[c - kk * lp1]);
-      m.ring[(size_t)slot * C + c] = v;
-      if (p.world == 1) const_cast<V*>(dpm)[(size_t)t * C + c] = v;
+    if (tid < C) {
+      V v = r1[tid];
+      for (int kk = 1; kk <= ck; ++kk) v = min(v, r1[tid - kk * lp1]);
+      m.ring[(size_t)(t % kChainRing) * C + tid] = v;
+      if (p.world == 1) const_cast<V*>(dpm)[(size_t)t * C + tid] = v;
       else
-        for (int r = 0; r < p.world; ++r) ((V*)p.peer_dp[r])[(size_t)t * C + c] = v;
+        for (int r = 0; r < p.world; ++r) ((V*)p.peer_dp[r])[(size_t)t * C + tid] = v;
     }
-    if (tid == 0) m.ring_ord[slot] = t;
     __syncthreads();
   }
   // release the block's levels (one fence for all)
@@ -817,7 +838,7 @@ __device__ __forceinline__ void persistent_body(const LevelLaunch& a, const Pers
       // a chain block (runner lists only)
       const uint64_t tc0 = p.trace ? globaltimer() : 0;
       uint64_t tmid[2] = {0, 0};
-      if (!chain_block<V, TRAIN>(a, p, cv, item.x, -item.y, st_area, nested_total, tmid)) break;
+      if (!chain_block<V, TRAIN>(a, p, cv, item.x, -item.y, item.w, st_area, nested_total, tmid)) break;
       __syncthreads();
       if (p.trace && tid == 0) {
         // start, static part done, chunk merges read, end
