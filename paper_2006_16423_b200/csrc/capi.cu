@@ -61,7 +61,8 @@ struct Fail {
   do {                                                                                 \
     cudaError_t e_ = (x);                                                              \
     if (e_ != cudaSuccess)                                                             \
-      throw Fail{DSG_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)};     \
+      throw Fail{DSG_CUDA_ERROR, std::string(#x) + " (capi.cu:" + std::to_string(__LINE__) + \
+                                     "): " + cudaGetErrorString(e_)};                  \
   } while (0)
 
 // DSG_DEBUG_SYNC=1: synchronise after a launch group and name it in the
@@ -806,8 +807,9 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
       max_level = std::max(max_level, lat.level_off[s + 1] - lat.level_off[s]);
     int64_t* perm_a = ctx.get_t<int64_t>("enum.perm_a", (size_t)lat.I);
     int64_t* perm_b = ctx.get_t<int64_t>("enum.perm_b", (size_t)lat.I);
+    int* lvl_pre = ctx.get_t<int>("enum.lvl_pre", (size_t)lat.n_levels + 1);
     launch_lex_rank(W, lat.I, L.bits, L.maxm, L.level_of, lvl_d, lat.sbits, lat.smax, max_level,
-                    perm_a, perm_b, ctx.stream);
+                    perm_a, perm_b, lvl_pre, lat.n_levels, ctx.stream);
     CK(cudaGetLastError());
     debug_sync(ctx, "lex rank");
     return lat;

@@ -62,17 +62,25 @@ constexpr int kDescThreads = 128;
 // (one thread per ideal was 0.5 ms on C1's 242 ideals of ~350 members) —
 // but no more lanes than about one full wave of threads needs: large
 // lattices keep all lanes busy with fewer lanes per ideal.
+__host__ __device__ __forceinline__ size_t desc_group_bytes(int W) {
+  return 4 * W * sizeof(uint64_t) + 2 * (W + 1) * sizeof(int32_t);
+}
+
+// G lanes per ideal: about one wave of threads in flight, and the groups'
+// shared rows within kDescSmemMax (wide bitsets on large lattices: W = 24 at
+// 47K ideals needs 62 KB at G = 2)
+constexpr size_t kDescSmemMax = 96 * 1024;
 __host__ __device__ __forceinline__ int desc_group(int W, int64_t I) {
-  (void)W;  // the member loops stride over bit positions, so any W uses G lanes
-  int G = 32;
+  int G = 32;  // the member loops stride over bit positions, so any W uses G lanes
   while (G > 1 && I * G > 148 * 8 * kDescThreads) G >>= 1;
+  while (G < 32 && (size_t)(kDescThreads / G) * desc_group_bytes(W) > kDescSmemMax) G <<= 1;
   return G;
 }
 
 // shared words per group: A, F, T (chunk neighbours), P; then two rank arrays
 __host__ __device__ __forceinline__ size_t desc_smem(int W, int64_t I) {
   const int groups = kDescThreads / desc_group(W, I);
-  return (size_t)groups * (4 * W * sizeof(uint64_t) + 2 * (W + 1) * sizeof(int32_t));
+  return (size_t)groups * desc_group_bytes(W);
 }
 
 template <typename V, bool FILL>
@@ -474,6 +482,13 @@ void launch_describe(const DescribeLaunch& L, bool fill, cudaStream_t st) {
   const unsigned blocks = (unsigned)((L.I + groups - 1) / groups);
   const size_t smem = desc_smem(L.g.W, L.I);
   if (blocks == 0) return;
+  // above the 48 KB default: opt in (per device context, so on every launch)
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(describe_kernel<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(describe_kernel<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(describe_kernel<int64_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(describe_kernel<int64_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
   if (L.value_bits == 32) {
     if (fill) describe_kernel<int32_t, true><<<blocks, threads, smem, st>>>(L);
     else describe_kernel<int32_t, false><<<blocks, threads, smem, st>>>(L);

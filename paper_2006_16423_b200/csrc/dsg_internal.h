@@ -58,7 +58,7 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st);
 void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
                      const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,
                      uint64_t* out_maxm, int64_t max_level, int64_t* perm_a, int64_t* perm_b,
-                     cudaStream_t st);
+                     int* lvl_d, int n_levels, cudaStream_t st);
 // lower covers of every ideal (ordinals one level down), CSR over ordinals
 void launch_cover_count(int W, int64_t I, const uint64_t* smax, int64_t* cnt, cudaStream_t st);
 void launch_cover_fill(int W, int64_t I, const uint64_t* sbits, const uint64_t* smax,

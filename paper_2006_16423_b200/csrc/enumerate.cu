@@ -1025,8 +1025,8 @@ __global__ void __launch_bounds__(kEnumThreads) enumerate_cluster_kernel(EnumArg
 
 // Lexicographic rank within a level (graph.cpp:62-72): the set holding the
 // smallest differing index comes first.  rank(i) = #{j in level : j < i}.
-__device__ __forceinline__ bool lex_less(const uint64_t* a, const uint64_t* b, int W) {
-  for (int w = 0; w < W; ++w) {
+__device__ __forceinline__ bool lex_less(const uint64_t* a, const uint64_t* b, int w0, int W) {
+  for (int w = w0; w < W; ++w) {
     uint64_t d = a[w] ^ b[w];
     if (d) return (a[w] & (d & (~d + 1))) != 0ull;
   }
@@ -1048,17 +1048,40 @@ constexpr int64_t kRankChunk = 256;  // chunk-local ranks, then merges from this
 // a before b in the level order (NodeSet::lex_less, graph.cpp:62-72): the
 // set holding the smallest differing index comes first = the larger
 // bit-reversed word at the first difference
-__device__ __forceinline__ bool lex_before(const uint64_t* a, const uint64_t* b, int W) {
-  for (int w = 0; w < W; ++w) {
+__device__ __forceinline__ bool lex_before(const uint64_t* a, const uint64_t* b, int w0, int W) {
+  for (int w = w0; w < W; ++w) {
     const uint64_t x = __brevll(__ldg(a + w)), y = __brevll(__ldg(b + w));
     if (x != y) return x > y;
   }
   return false;
 }
 
+__global__ void fill_i32_kernel(int* p, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// The words every ideal of a level shares with the level's first ideal
+// (lvl_d[s] = the first word where any differs): comparisons inside the level
+// start there.  A long common stem leaves a wide lattice's ideals equal in
+// all but their last words (a 2,000-node sweep point: 30 of 32).
+__global__ void level_prefix_kernel(int W, int64_t total, const uint64_t* __restrict__ bits,
+                                    const int32_t* __restrict__ level_of,
+                                    const int64_t* __restrict__ level_off, int* __restrict__ lvl_d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int s = level_of[i];
+  const int64_t lo = level_off[s];
+  if (i == lo) return;
+  int w = 0;
+  while (w < W && bits[(size_t)i * W + w] == bits[(size_t)lo * W + w]) ++w;
+  atomicMin(lvl_d + s, w);
+}
+
 __global__ void rank_chunk_kernel(int W, int64_t total, const uint64_t* __restrict__ bits,
                                   const int32_t* __restrict__ level_of,
-                                  const int64_t* __restrict__ level_off, int64_t* __restrict__ perm) {
+                                  const int64_t* __restrict__ level_off, const int* __restrict__ lvl_d,
+                                  int64_t* __restrict__ perm) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   const int s = level_of[i];
@@ -1067,14 +1090,15 @@ __global__ void rank_chunk_kernel(int W, int64_t total, const uint64_t* __restri
   const int64_t c0 = lo + (i - lo) / kRankChunk * kRankChunk, c1 = min(hi, c0 + kRankChunk);
   const uint64_t* bi = bits + (size_t)i * W;
   int64_t r = 0;
-  for (int64_t j = c0; j < c1; ++j) r += lex_before(bits + (size_t)j * W, bi, W) ? 1 : 0;
+  const int d0 = lvl_d[s];
+  for (int64_t j = c0; j < c1; ++j) r += lex_before(bits + (size_t)j * W, bi, d0, W) ? 1 : 0;
   perm[c0 + r] = i;
 }
 
 __global__ void merge_pass_kernel(int W, int64_t total, int64_t width,
                                   const uint64_t* __restrict__ bits,
                                   const int32_t* __restrict__ level_of,
-                                  const int64_t* __restrict__ level_off,
+                                  const int64_t* __restrict__ level_off, const int* __restrict__ lvl_d,
                                   const int64_t* __restrict__ in, int64_t* __restrict__ out) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= total) return;
@@ -1089,10 +1113,11 @@ __global__ void merge_pass_kernel(int W, int64_t total, int64_t width,
     return;
   }
   const uint64_t* be = bits + (size_t)e * W;
+  const int d0 = lvl_d[s];
   int64_t a = q0, b = q1;  // partner elements before e
   while (a < b) {
     const int64_t m = (a + b) >> 1;
-    if (lex_before(bits + (size_t)in[m] * W, be, W)) a = m + 1;
+    if (lex_before(bits + (size_t)in[m] * W, be, d0, W)) a = m + 1;
     else b = m;
   }
   out[min(r0, q0) + (p - r0) + (a - q0)] = e;
@@ -1118,8 +1143,8 @@ __global__ void scatter_perm_kernel(int W, int64_t total, const uint64_t* __rest
 __global__ void __launch_bounds__(kRankRows* kRankParts)
     lex_rank_scatter_kernel(int W, int64_t total, const uint64_t* __restrict__ bits,
                             const uint64_t* __restrict__ maxm, const int32_t* __restrict__ level_of,
-                            const int64_t* __restrict__ level_off, uint64_t* __restrict__ out_bits,
-                            uint64_t* __restrict__ out_maxm) {
+                            const int64_t* __restrict__ level_off, const int* __restrict__ lvl_d,
+                            uint64_t* __restrict__ out_bits, uint64_t* __restrict__ out_maxm) {
   extern __shared__ uint64_t s_tile[];  // [tile rows][W], bit-reversed
   __shared__ int s_part[kRankParts][kRankRows];
   const int row = threadIdx.x % kRankRows, part = threadIdx.x / kRankRows;
@@ -1168,8 +1193,9 @@ __global__ void __launch_bounds__(kRankRows* kRankParts)
       }
     }
   } else if (act) {
+    const int d0 = lvl_d[s];
     for (int64_t j = lo + part; j < hi; j += kRankParts)
-      rank += lex_less(bits + (size_t)j * W, bi, W) ? 1 : 0;
+      rank += lex_less(bits + (size_t)j * W, bi, d0, W) ? 1 : 0;
   }
   s_part[part][row] = rank;
   __syncthreads();
@@ -1222,7 +1248,7 @@ __global__ void cover_fill_kernel(int W, int64_t I, const uint64_t* __restrict__
       int64_t lo = lo0, hi = hi0;  // first j with !(bits_j < key)
       while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
-        if (lex_less(sbits + (size_t)mid * W, key, W)) lo = mid + 1;
+        if (lex_less(sbits + (size_t)mid * W, key, 0, W)) lo = mid + 1;
         else hi = mid;
       }
       bool eq = lo < hi0;
@@ -1311,18 +1337,27 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
 void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
                      const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,
                      uint64_t* out_maxm, int64_t max_level, int64_t* perm_a, int64_t* perm_b,
-                     cudaStream_t st) {
+                     int* lvl_d, int n_levels, cudaStream_t st) {
   const int64_t blocks = (total + kRankRows - 1) / kRankRows;
   const size_t smem = W <= 8 ? (size_t)kRankRows * kRankParts * W * sizeof(uint64_t) : 0;
+  if (W > 8 || max_level > kRankDirect) {
+    // the per-level common prefix (the word-by-word comparisons start there)
+    fill_i32_kernel<<<(unsigned)((n_levels + 255) / 256), 256, 0, st>>>(lvl_d, n_levels, W);
+    count_launch();
+    level_prefix_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(W, total, bits, level_of,
+                                                                          level_off, lvl_d);
+    count_launch();
+  }
   lex_rank_scatter_kernel<<<(unsigned)blocks, kRankRows * kRankParts, smem, st>>>(
-      W, total, bits, maxm, level_of, level_off, out_bits, out_maxm);
+      W, total, bits, maxm, level_of, level_off, lvl_d, out_bits, out_maxm);
   count_launch();
   if (max_level <= kRankDirect) return;
   const unsigned g = (unsigned)((total + 255) / 256);
-  rank_chunk_kernel<<<g, 256, 0, st>>>(W, total, bits, level_of, level_off, perm_a);
+  rank_chunk_kernel<<<g, 256, 0, st>>>(W, total, bits, level_of, level_off, lvl_d, perm_a);
   count_launch();
   for (int64_t width = kRankChunk; width < max_level; width *= 2) {
-    merge_pass_kernel<<<g, 256, 0, st>>>(W, total, width, bits, level_of, level_off, perm_a, perm_b);
+    merge_pass_kernel<<<g, 256, 0, st>>>(W, total, width, bits, level_of, level_off, lvl_d, perm_a,
+                                         perm_b);
     count_launch();
     std::swap(perm_a, perm_b);
   }

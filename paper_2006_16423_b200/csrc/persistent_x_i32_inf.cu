@@ -13,11 +13,19 @@ bool dispatch_exact_i32_inf(const LevelLaunch& L, const PersistPlan* P, cudaStre
   // replication and unprunable weights: generic cells (no pruning)
   if (L.repl || L.no_prune) return false;
   if (lp1 == 1 && kp1 == 9) {
-    // exact words and cells: no predicates in the hot loop (C2: K=8, L=0)
+    // exact words and cells: no predicates in the hot loop (C2: K=8, L=0;
+    // the sweep up to 2,048 nodes: C5 top, AW = 12, DP 13.5 -> 9.8 ms)
     if (L.AW == 2) return run_variant<V, 1, 9, TRAIN, 2, true>(L, P, st, info), true;
     if (L.AW == 4) return run_variant<V, 1, 9, TRAIN, 4, true>(L, P, st, info), true;
     if (L.AW == 6) return run_variant<V, 1, 9, TRAIN, 6, true>(L, P, st, info), true;
     if (L.AW == 8) return run_variant<V, 1, 9, TRAIN, 8, true>(L, P, st, info), true;
+#ifndef DSG_NO_WIDE_EXACT  // (A/B builds)
+    if (L.AW == 10) return run_variant<V, 1, 9, TRAIN, 10, true>(L, P, st, info), true;
+    if (L.AW == 12) return run_variant<V, 1, 9, TRAIN, 12, true>(L, P, st, info), true;
+    if (L.AW == 16) return run_variant<V, 1, 9, TRAIN, 16, true>(L, P, st, info), true;
+    if (L.AW == 24) return run_variant<V, 1, 9, TRAIN, 24, true>(L, P, st, info), true;
+    if (L.AW == 32) return run_variant<V, 1, 9, TRAIN, 32, true>(L, P, st, info), true;
+#endif
   }
   if (lp1 == 3 && kp1 == 7) {  // C3: K=6, L=2
     if (L.AW == 2) return run_variant<V, 3, 7, TRAIN, 2, true>(L, P, st, info), true;

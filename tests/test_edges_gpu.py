@@ -115,3 +115,18 @@ def test_common_denominator_above_2_62_is_overflow(gpu):
     assert ob.dp("port", 0, g, cfg).objective == F(6291377, 4397899711013)
     with pytest.raises(OverflowError):
         solver.solve_maxload_inference(g, cfg)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [600, 700, 1000, 1500, 2000])
+def test_exact_word_variants_wide(gpu, n):
+    """K = 8, L = 0 inference on 600 to 2,000 nodes: the exact-word
+    kernels for AW = 10, 12, 16, 24 and 32 (persistent_x_i32_inf.cu) against the
+    oracle port; one module keeps the lattice small."""
+    stem = n - 9
+    g = wl.module_chain(wl.ChainSpec(stem, [[3, 2]], 2))
+    assert g.size() == n
+    cfg = DeviceConfig(8, 0, 10 ** 6)
+    split = solver.solve_maxload_inference(g, cfg)
+    assert split.objective_value == ob.dp("port", 0, g, cfg).objective
+    assert not verify_split(g, cfg, split, training=False)

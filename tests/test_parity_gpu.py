@@ -368,7 +368,8 @@ def test_full_size_objectives_match_reference(gpu):
     """Objectives of the unmodified reference on full workloads, solved on the
     bench host (tools/cpu_ref_host.sh): the C5 top point (943.5M transitions),
     the 3 %-dense sweep point (16,1,1,300), a second weight seed and D = 1000
-    weights for C2, and C1-C4."""
+    weights for C2, C1-C4, and a wide-bitset sweep point (16,1,1,1300: W = 21,
+    66,838 ideals; solved by the reference in the build container)."""
     for row in json.load(open(HOST_REF)):
         w = wl.by_name(row["workload"])
         split = device_solve(1 if w.training else 0, w.graph, w.config)
