@@ -5,7 +5,7 @@
 TAG=${1:-r2}
 OUT=gpurun_out/final_${TAG}
 mkdir -p $OUT
-for w in C2 C1 C3 C4 "C5:8,2,7,600" "C5:16,1,1,300" C2@seed2 C2@D1000 C2@int64; do
+for w in C2 C1 C3 C4 "C5:8,2,7,600" "C5:16,1,1,300" "C5:8,2,7,1900" "C5:16,1,1,1300" C2@seed2 C2@D1000 C2@int64; do
   f=${w//[:,@]/_}
   timeout 600 python bench.py --workload "$w" > $OUT/bench_$f.json 2> $OUT/bench_$f.err
   echo "$w rc=$? $(tail -c 300 $OUT/bench_$f.json | head -c 0)"
