@@ -146,15 +146,20 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def dist_setup():
+def dist_setup(cpu_only: bool = False):
+    """One process per GPU (torchrun); the reference arm is CPU work on rank 0
+    only, so it joins a gloo group and never touches CUDA."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
+        if cpu_only:
+            dist.init_process_group("gloo", init_method="env://")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", init_method="env://")
     return world, rank, local
 
 
@@ -493,7 +498,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(cpu_only=args.impl == "reference")
     if args.impl == "reference":
         run_reference_arm(args, world, rank)
     else:
