@@ -720,6 +720,7 @@ struct Lattice {
   std::vector<int64_t> level_off;  // host copy, n_levels + 1
   uint64_t* sbits = nullptr;       // sorted, device
   uint64_t* smax = nullptr;        // maximal elements of each ideal, same order
+  const int* lvl_pre = nullptr;    // each level's common word prefix (null: not computed)
 };
 
 Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, int64_t budget,
@@ -807,9 +808,11 @@ Lattice enumerate_device(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& d
       max_level = std::max(max_level, lat.level_off[s + 1] - lat.level_off[s]);
     int64_t* perm_a = ctx.get_t<int64_t>("enum.perm_a", (size_t)lat.I);
     int64_t* perm_b = ctx.get_t<int64_t>("enum.perm_b", (size_t)lat.I);
-    int* lvl_pre = ctx.get_t<int>("enum.lvl_pre", (size_t)lat.n_levels + 1);
-    launch_lex_rank(W, lat.I, L.bits, L.maxm, L.level_of, lvl_d, lat.sbits, lat.smax, max_level,
-                    perm_a, perm_b, lvl_pre, lat.n_levels, ctx.stream);
+    int* lvl_pre = ctx.get_t<int>(pfx + "lat.lvl_pre", (size_t)lat.n_levels + 1);
+    lat.lvl_pre = launch_lex_rank(W, lat.I, L.bits, L.maxm, L.level_of, lvl_d, lat.sbits, lat.smax,
+                                  max_level, perm_a, perm_b, lvl_pre, lat.n_levels, ctx.stream)
+                      ? lvl_pre
+                      : nullptr;
     CK(cudaGetLastError());
     debug_sync(ctx, "lex rank");
     return lat;
@@ -1016,8 +1019,8 @@ void phase1(DeviceCtx& ctx, const Prepared& P, const DeviceGraph& dg, const dsg_
   int32_t* cov = ctx.get_t<int32_t>(pfx + "lat.cov", (size_t)n_cov + 1);
   int* cov_err = ctx.get_t<int>(pfx + "lat.cov_err", 1);
   CK(cudaMemsetAsync(cov_err, 0, sizeof(int), st));
-  launch_cover_fill(W, I, lat.sbits, lat.smax, pl.level_of_d, pl.level_off_d, cov_off, cov, cov_err,
-                    st);
+  launch_cover_fill(W, I, lat.sbits, lat.smax, pl.level_of_d, pl.level_off_d, cov_off, cov,
+                    lat.lvl_pre, cov_err, st);
   pl.t_desc_ms = ms_since(t2);
 
   // ---- DP tables and launch parameters

@@ -72,7 +72,9 @@ __host__ __device__ __forceinline__ size_t desc_group_bytes(int W) {
 constexpr size_t kDescSmemMax = 96 * 1024;
 __host__ __device__ __forceinline__ int desc_group(int W, int64_t I) {
   int G = 32;  // the member loops stride over bit positions, so any W uses G lanes
-  while (G > 1 && I * G > 148 * 8 * kDescThreads) G >>= 1;
+  // (wider bitsets give each lane more words per member loop: a larger budget)
+  const int64_t budget = (int64_t)148 * 8 * kDescThreads * (W > 8 ? W / 8 : 1);
+  while (G > 1 && I * G > budget) G >>= 1;
   while (G < 32 && (size_t)(kDescThreads / G) * desc_group_bytes(W) > kDescSmemMax) G <<= 1;
   return G;
 }

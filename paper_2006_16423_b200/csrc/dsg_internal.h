@@ -55,7 +55,8 @@ struct EnumLaunch {
 void launch_enumerate(const EnumLaunch& L, cudaStream_t st);
 // level order (size-major, NodeSet::lex_less within a level); max_level =
 // the largest level size, perm_a / perm_b: [total] scratch for large levels
-void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
+// returns whether lvl_d (each level's common word prefix) was filled
+bool launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
                      const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,
                      uint64_t* out_maxm, int64_t max_level, int64_t* perm_a, int64_t* perm_b,
                      int* lvl_d, int n_levels, cudaStream_t st);
@@ -63,7 +64,7 @@ void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t*
 void launch_cover_count(int W, int64_t I, const uint64_t* smax, int64_t* cnt, cudaStream_t st);
 void launch_cover_fill(int W, int64_t I, const uint64_t* sbits, const uint64_t* smax,
                        const int32_t* level_of, const int64_t* level_off, const int64_t* cov_off,
-                       int32_t* cov, int* err, cudaStream_t st);
+                       int32_t* cov, const int* lvl_pre, int* err, cudaStream_t st);
 
 // ------------------------------------------------------- descriptors
 // Per-ideal table sizes (pass 1) -> exclusive offsets (scan) -> fill (pass 2).

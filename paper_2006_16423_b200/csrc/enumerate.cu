@@ -1229,12 +1229,14 @@ __global__ void cover_fill_kernel(int W, int64_t I, const uint64_t* __restrict__
                                   const int32_t* __restrict__ level_of,
                                   const int64_t* __restrict__ level_off,
                                   const int64_t* __restrict__ cov_off, int32_t* __restrict__ cov,
-                                  int* __restrict__ err) {
+                                  const int* __restrict__ lvl_pre, int* __restrict__ err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= I) return;
   const int s = level_of[i];
   if (s == 0) return;
   const int64_t lo0 = level_off[s - 1], hi0 = level_off[s];
+  // I \ {v} is an ideal of level s-1: it shares that level's common prefix
+  const int w0 = lvl_pre ? lvl_pre[s - 1] : 0;
   const uint64_t* bi = sbits + (size_t)i * W;
   int64_t out = cov_off[i];
   uint64_t key[kMaxWords];
@@ -1248,7 +1250,7 @@ __global__ void cover_fill_kernel(int W, int64_t I, const uint64_t* __restrict__
       int64_t lo = lo0, hi = hi0;  // first j with !(bits_j < key)
       while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
-        if (lex_less(sbits + (size_t)mid * W, key, 0, W)) lo = mid + 1;
+        if (lex_less(sbits + (size_t)mid * W, key, w0, W)) lo = mid + 1;
         else hi = mid;
       }
       bool eq = lo < hi0;
@@ -1334,13 +1336,14 @@ void launch_enumerate(const EnumLaunch& L, cudaStream_t st) {
   count_launch();
 }
 
-void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
+bool launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
                      const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,
                      uint64_t* out_maxm, int64_t max_level, int64_t* perm_a, int64_t* perm_b,
                      int* lvl_d, int n_levels, cudaStream_t st) {
+  const bool prefix = W > 8 || max_level > kRankDirect;
   const int64_t blocks = (total + kRankRows - 1) / kRankRows;
   const size_t smem = W <= 8 ? (size_t)kRankRows * kRankParts * W * sizeof(uint64_t) : 0;
-  if (W > 8 || max_level > kRankDirect) {
+  if (prefix) {
     // the per-level common prefix (the word-by-word comparisons start there)
     fill_i32_kernel<<<(unsigned)((n_levels + 255) / 256), 256, 0, st>>>(lvl_d, n_levels, W);
     count_launch();
@@ -1351,7 +1354,7 @@ void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t*
   lex_rank_scatter_kernel<<<(unsigned)blocks, kRankRows * kRankParts, smem, st>>>(
       W, total, bits, maxm, level_of, level_off, lvl_d, out_bits, out_maxm);
   count_launch();
-  if (max_level <= kRankDirect) return;
+  if (max_level <= kRankDirect) return prefix;
   const unsigned g = (unsigned)((total + 255) / 256);
   rank_chunk_kernel<<<g, 256, 0, st>>>(W, total, bits, level_of, level_off, lvl_d, perm_a);
   count_launch();
@@ -1364,6 +1367,7 @@ void launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t*
   scatter_perm_kernel<<<g, 256, 0, st>>>(W, total, bits, maxm, level_of, level_off, perm_a,
                                          out_bits, out_maxm);
   count_launch();
+  return prefix;
 }
 
 void launch_cover_count(int W, int64_t I, const uint64_t* smax, int64_t* cnt, cudaStream_t st) {
@@ -1375,10 +1379,10 @@ void launch_cover_count(int W, int64_t I, const uint64_t* smax, int64_t* cnt, cu
 
 void launch_cover_fill(int W, int64_t I, const uint64_t* sbits, const uint64_t* smax,
                        const int32_t* level_of, const int64_t* level_off, const int64_t* cov_off,
-                       int32_t* cov, int* err, cudaStream_t st) {
+                       int32_t* cov, const int* lvl_pre, int* err, cudaStream_t st) {
   const int threads = 128;
   cover_fill_kernel<<<(unsigned)((I + threads - 1) / threads), threads, 0, st>>>(
-      W, I, sbits, smax, level_of, level_off, cov_off, cov, err);
+      W, I, sbits, smax, level_of, level_off, cov_off, cov, lvl_pre, err);
   count_launch();
 }
 
