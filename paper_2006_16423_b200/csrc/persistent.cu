@@ -20,7 +20,7 @@ void dispatch(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st, Persi
     }
   } else {
     if (L.training) dispatch_general_i64_train(L, P, st, info);
-    else dispatch_general_i64_inf(L, P, st, info);
+    else if (!dispatch_exact_i64_inf(L, P, st, info)) dispatch_general_i64_inf(L, P, st, info);
   }
 }
 

@@ -5,8 +5,18 @@
 
 namespace dsg {
 
-bool dispatch_exact_i64_inf(const LevelLaunch&, const PersistPlan*, cudaStream_t, PersistInfo*) {
-  return false;  // exact variants are int32-only
+bool dispatch_exact_i64_inf(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st,
+                            PersistInfo* info) {
+  // exact words and cells for K = 8, L = 0 on the 64-bit path (graphs whose
+  // proven bound passes 2^30, e.g. many-decimal weights)
+  using V = int64_t;
+  constexpr bool TRAIN = false;
+  if (L.repl || L.no_prune || L.L != 0 || L.K != 8) return false;
+  if (L.AW == 2) return run_variant<V, 1, 9, TRAIN, 2, true>(L, P, st, info), true;
+  if (L.AW == 4) return run_variant<V, 1, 9, TRAIN, 4, true>(L, P, st, info), true;
+  if (L.AW == 6) return run_variant<V, 1, 9, TRAIN, 6, true>(L, P, st, info), true;
+  if (L.AW == 8) return run_variant<V, 1, 9, TRAIN, 8, true>(L, P, st, info), true;
+  return false;
 }
 
 void dispatch_general_i64_inf(const LevelLaunch& L, const PersistPlan* P, cudaStream_t st,

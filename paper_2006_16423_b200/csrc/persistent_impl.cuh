@@ -1214,7 +1214,8 @@ __global__ void __launch_bounds__(kTileTargets) persistent_levels_kernel(const L
 // exact variants: register budget for kMinBlocksExact resident CTAs per SM
 template <typename V, int LP1, int KP1MAX, bool TRAIN, int WT, bool CX>
 __global__ void __launch_bounds__(kTileTargets,
-                                  LP1 * KP1MAX <= 9 ? kMinBlocksExact : kMinBlocksExactBig)
+                                  LP1 * KP1MAX <= 9 && sizeof(V) == 4 ? kMinBlocksExact
+                                                                      : kMinBlocksExactBig)
     persistent_levels_kernel_x(const LevelLaunch a, const PersistPlan p) {
   persistent_body<V, LP1, KP1MAX, TRAIN, WT, CX>(a, p);
 }

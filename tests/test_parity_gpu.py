@@ -377,3 +377,18 @@ def test_full_size_objectives_match_reference(gpu):
         assert split.stats["n_ideals"] == row["ideals"]
         assert split.stats["n_pairs"] == row["pairs_closed_form"]
         assert not verify_split(w.graph, w.config, split, training=w.training)
+
+
+@pytest.mark.parametrize("name", ["C2", "C5:16,1,1,300", "C5:4,4,8,1400"])
+def test_int64_exact_variants(gpu, name):
+    """The 64-bit exact-word kernels (K = 8, L = 0, AW = 6 / 6 / 26->generic):
+    the same objective and transition count as the 32-bit path, which the
+    host-reference objectives pin for the first two."""
+    w = wl.by_name(name)
+    base = solver.solve_maxload_inference(w.graph, w.config)
+    s = solver.solve_maxload_inference(w.graph, w.config,
+                                       solver.SolveOptions(flags=_abi.DSG_FLAG_FORCE_INT64))
+    assert s.stats["value_bits"] == 64 and base.stats["value_bits"] == 32
+    assert s.objective_value == base.objective_value
+    assert s.stats["n_pairs"] == base.stats["n_pairs"]
+    assert not verify_split(w.graph, w.config, s, training=False)
