@@ -538,25 +538,17 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
   const size_t NW = (size_t)n * W;
   // [n][W] rows only where a kernel reads them: pred_real never (lists
   // serve), twins only for training, bw_succ only with backward nodes
-  P.succ_real.assign(NW, 0);
+  // (succ_real, pred_u and succ_u rows are built on the device from the
+  // lists: launch_adj_bits in upload_graph)
   P.pred_real.assign(W, 0);
-  P.pred_u.assign(NW, 0);
-  P.succ_u.assign(NW, 0);
   P.twins.assign(P.training ? NW : (size_t)W, 0);
   P.bw_succ.assign(P.has_bw ? NW : (size_t)W, 0);
   P.bwset.assign(W, 0);
   P.out_off.assign(n + 1, 0);
   P.in_off.assign(n + 1, 0);
   for (int v = 0; v < n; ++v) {
-    for (int w : out_real[v]) set_bit(P.succ_real, v, W, w);
     P.out_off[v + 1] = P.out_off[v] + (int)out_real[v].size();
     P.in_off[v + 1] = P.in_off[v] + (int)in_real[v].size();
-    if (P.in_universe[v]) {
-      for (int u : in_all[v])
-        if (P.in_universe[u]) set_bit(P.pred_u, v, W, u);
-      for (int w : out_all[v])
-        if (P.in_universe[w]) set_bit(P.succ_u, v, W, w);
-    }
     for (int b : paired_bw[v]) set_bit(P.twins, v, W, b);
     if (P.bw[v]) {
       P.bwset[v >> 6] |= 1ull << (v & 63);
@@ -668,8 +660,7 @@ DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P, const std::string& p
   Packer pk;
   const size_t o_cpu = pk.add(P.cpu), o_acc = pk.add(P.acc), o_comm = pk.add(P.comm),
                o_mem = pk.add(P.mem), o_unsup = pk.add(P.unsup), o_comminf = pk.add(P.comminf),
-               o_sr = pk.add(P.succ_real), o_pr = pk.add(P.pred_real), o_pu = pk.add(P.pred_u),
-               o_su = pk.add(P.succ_u), o_tw = pk.add(P.twins), o_bws = pk.add(P.bw_succ),
+               o_pr = pk.add(P.pred_real), o_tw = pk.add(P.twins), o_bws = pk.add(P.bw_succ),
                o_bwf = pk.add(P.bw_from), o_bwt = pk.add(P.bw_to), o_bwset = pk.add(P.bwset),
                o_oo = pk.add(P.out_off), o_oa = pk.add(P.out_adj), o_io = pk.add(P.in_off),
                o_ia = pk.add(P.in_adj), o_univ = pk.add(P.in_universe), o_puo = pk.add(P.pu_off),
@@ -692,10 +683,7 @@ DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P, const std::string& p
   g.mem = reinterpret_cast<const int64_t*>(dev + o_mem);
   g.unsup = reinterpret_cast<const uint8_t*>(dev + o_unsup);
   g.comminf = reinterpret_cast<const uint8_t*>(dev + o_comminf);
-  g.succ_real = reinterpret_cast<const uint64_t*>(dev + o_sr);
   g.pred_real = reinterpret_cast<const uint64_t*>(dev + o_pr);
-  g.pred_u = reinterpret_cast<const uint64_t*>(dev + o_pu);
-  g.succ_u = reinterpret_cast<const uint64_t*>(dev + o_su);
   g.twins = reinterpret_cast<const uint64_t*>(dev + o_tw);
   g.bw_succ = reinterpret_cast<const uint64_t*>(dev + o_bws);
   g.bw_from = reinterpret_cast<const uint64_t*>(dev + o_bwf);
@@ -710,6 +698,16 @@ DeviceGraph upload_graph(DeviceCtx& ctx, const Prepared& P, const std::string& p
   d.pu_adj = reinterpret_cast<int32_t*>(dev + o_pua);
   d.su_off = reinterpret_cast<int32_t*>(dev + o_suo);
   d.su_adj = reinterpret_cast<int32_t*>(dev + o_sua);
+  // [n][W] adjacency rows from the lists, on the device (C4: 0.9 MB of host
+  // bit setting and H2D per solve before)
+  const size_t NW = (size_t)std::max(1, P.n) * P.W;
+  uint64_t* rows = ctx.get_t<uint64_t>(prefix + "adj.rows", 3 * NW);
+  CK(cudaMemsetAsync(rows, 0, 3 * NW * sizeof(uint64_t), ctx.stream));
+  launch_adj_bits(P.n, P.W, d.pu_off, d.pu_adj, d.su_off, d.su_adj, g.out_real_off, g.out_real_adj,
+                  rows, rows + NW, rows + 2 * NW, ctx.stream);
+  g.pred_u = rows;
+  g.succ_u = rows + NW;
+  g.succ_real = rows + 2 * NW;
   return d;
 }
 

@@ -55,6 +55,12 @@ struct EnumLaunch {
 void launch_enumerate(const EnumLaunch& L, cudaStream_t st);
 // level order (size-major, NodeSet::lex_less within a level); max_level =
 // the largest level size, perm_a / perm_b: [total] scratch for large levels
+// [n][W] bitset rows of the universe predecessors / successors and the real
+// successors, from their CSR lists (rows zeroed by the caller)
+void launch_adj_bits(int n, int W, const int32_t* pu_off, const int32_t* pu_adj, const int32_t* su_off,
+                     const int32_t* su_adj, const int32_t* out_off, const int32_t* out_adj,
+                     uint64_t* pred_u, uint64_t* succ_u, uint64_t* succ_real, cudaStream_t st);
+
 // returns whether lvl_d (each level's common word prefix) was filled
 bool launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t* maxm,
                      const int32_t* level_of, const int64_t* level_off, uint64_t* out_bits,

@@ -1370,6 +1370,33 @@ bool launch_lex_rank(int W, int64_t total, const uint64_t* bits, const uint64_t*
   return prefix;
 }
 
+namespace {
+__global__ void adj_bits_kernel(int n, int W, const int32_t* __restrict__ pu_off,
+                                const int32_t* __restrict__ pu_adj, const int32_t* __restrict__ su_off,
+                                const int32_t* __restrict__ su_adj, const int32_t* __restrict__ out_off,
+                                const int32_t* __restrict__ out_adj, uint64_t* __restrict__ pred_u,
+                                uint64_t* __restrict__ succ_u, uint64_t* __restrict__ succ_real) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;  // row v is this thread's alone
+  uint64_t* p = pred_u + (size_t)v * W;
+  uint64_t* q = succ_u + (size_t)v * W;
+  uint64_t* r = succ_real + (size_t)v * W;
+  for (int e = pu_off[v]; e < pu_off[v + 1]; ++e) p[pu_adj[e] >> 6] |= 1ull << (pu_adj[e] & 63);
+  for (int e = su_off[v]; e < su_off[v + 1]; ++e) q[su_adj[e] >> 6] |= 1ull << (su_adj[e] & 63);
+  for (int e = out_off[v]; e < out_off[v + 1]; ++e) r[out_adj[e] >> 6] |= 1ull << (out_adj[e] & 63);
+}
+}  // namespace
+
+void launch_adj_bits(int n, int W, const int32_t* pu_off, const int32_t* pu_adj, const int32_t* su_off,
+                     const int32_t* su_adj, const int32_t* out_off, const int32_t* out_adj,
+                     uint64_t* pred_u, uint64_t* succ_u, uint64_t* succ_real, cudaStream_t st) {
+  if (n <= 0) return;
+  adj_bits_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, W, pu_off, pu_adj, su_off, su_adj,
+                                                               out_off, out_adj, pred_u, succ_u,
+                                                               succ_real);
+  count_launch();
+}
+
 void launch_cover_count(int W, int64_t I, const uint64_t* smax, int64_t* cnt, cudaStream_t st) {
   const int threads = 256;
   cover_count_kernel<<<(unsigned)((I + 1 + threads - 1) / threads), threads, 0, st>>>(W, I, smax,
