@@ -119,6 +119,11 @@ class Graph:
                 self._out_all[f].append(t)
                 self._in_all[t].append(f)
         self._pod_cache = None
+        self._ids: List[int] = [nd.id for nd in self._nodes]
+
+    def ids(self) -> List[int]:
+        """External id of every dense index (the Graph is immutable)."""
+        return self._ids
 
     # --- reference accessors (graph.hpp:157-185) ---
     def size(self) -> int:
@@ -309,7 +314,7 @@ def _replicated(load: Num, mem: Num, r: int, config: DeviceConfig) -> Num:
 def make_canonical_split(g: Graph, config: DeviceConfig, blocks: List[SplitBlock],
                          objective: Num) -> Split:
     """graph.cpp:573-621: accelerators first, each kind by smallest external id."""
-    ids = [n.id for n in g.nodes()]
+    ids = g.ids()
 
     def smallest_id(b: SplitBlock) -> int:
         return min(map(ids.__getitem__, b.members), default=2 ** 31 - 1)
