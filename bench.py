@@ -70,6 +70,30 @@ def sample_workload(name: str):
     return g, cfg, spec, w.training
 
 
+def pair_fates(name: str, transitions: int):
+    """What the dataflow kernel did with each transition of this workload:
+    counted only (a chunk no pair of which can change a cell), dropped by the
+    per-pair candidate test, frontier walks, min-max updates (mode-0 items).
+    Device counters of the DSG_PAIR_STATS diagnostic build
+    (tools/pair_stats.sh -> profiles/r2_pair_stats.txt); the timed build
+    carries no counters."""
+    path = os.path.join(ROOT, "profiles", "r2_pair_stats.txt")
+    if not os.path.exists(path):
+        return None
+    cur = None
+    for line in open(path):
+        line = line.strip()
+        if line.startswith("== "):
+            cur = line[3:]
+        elif cur == name and line.startswith("DSG_PAIR_STATS "):
+            d = json.loads(line[len("DSG_PAIR_STATS "):])
+            d["fraction_count_only"] = d["count_only"] / transitions if transitions else None
+            d["fraction_minmax"] = d["minmax_updates"] / transitions if transitions else None
+            d["source"] = "profiles/r2_pair_stats.txt (DSG_PAIR_STATS diagnostic build)"
+            return d
+    return None
+
+
 def full_size_reference(name: str):
     """The unmodified reference's full-size solve of this workload on the
     bench host (tools/cpu_ref_host.sh, committed under profiles/), if any
@@ -460,6 +484,7 @@ def run_ours(args, world, rank, local):
                 "call": "dsg_dp_solve (C-ABI, host POD buffers) + canonical split"},
         "gpu_launches": int(launches),
         "roofline": roofline,
+        "pair_fates": pair_fates(args.workload, pairs_cf),
         "wall_s": wall,
     }
     line["clocks"] = clk
