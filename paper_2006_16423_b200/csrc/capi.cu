@@ -619,6 +619,7 @@ Prepared prepare(int mode, const dsg_graph* g, const dsg_config* cfg, const uint
     P.bw_to.assign(W, 0);
   }
   PREP_MARK("reach");
+#undef PREP_MARK
   return P;
 }
 
