@@ -230,7 +230,7 @@ __device__ __forceinline__ Target<V> load_target(const LevelLaunch& a, int64_t t
 template <typename V, bool TRAIN, int TS>
 __device__ __forceinline__ V acc_block_cost(const LevelLaunch& a, int64_t s, const SrcRec& r,
                                             V proc, const Target<V>& x, const uint64_t* tA,
-                                            const uint64_t* tInt) {
+                                            const uint64_t* tInt, const uint64_t* sAs = nullptr) {
   constexpr V INF = VTraits<V>::INF;
   V cin = 0, csub = 0;
   bool cin_inf = false;
@@ -253,13 +253,14 @@ __device__ __forceinline__ V acc_block_cost(const LevelLaunch& a, int64_t s, con
       cout += in ? (V)__ldg(&pi->weight) : (V)0;
       cout_inf += (in && __ldg(&pi->inf)) ? 1 : 0;
     }
-    const uint64_t* sA = a.abits + (size_t)s * a.AW;
+    // the source's bitset row: staged in shared memory when the chunk is
+    const uint64_t* sA = sAs ? sAs : a.abits + (size_t)s * a.AW;
     for (int64_t e = x.l_lo; e < x.l_hi; ++e) {
       const LEntry le = a.lentries[e];
       bool charged = false;
       for (int i = 0; i < le.n_items; ++i) {
         const MaskItem mi = a.litems[le.off_items + i];
-        charged |= (mi.mask & ~__ldg(sA + mi.word)) != 0ull;
+        charged |= (mi.mask & ~(sAs ? sA[mi.word] : __ldg(sA + mi.word))) != 0ull;
       }
       cin += charged ? (V)le.weight : (V)0;
       cin_inf |= charged && le.inf;
@@ -291,12 +292,13 @@ template <typename V, bool TRAIN, int TS, class Need = AlwaysNeeded, bool STAGED
 __device__ __forceinline__ bool pair_cost(const LevelLaunch& a, const Target<V>& x, int64_t s,
                                           const uint64_t* tA, const uint64_t* tInt, bool& gated,
                                           V& acc, V& cpu, V& mem_blk, Need need = Need(),
-                                          const SrcRec* rs = nullptr) {
+                                          const SrcRec* rs = nullptr,
+                                          const uint64_t* sAs = nullptr) {
   constexpr V INF = VTraits<V>::INF;
   const SrcRec r = STAGED ? load_rec_s(rs) : load_rec(a.srec + s);
   gated = false;
   if (TRAIN && a.has_bw) {
-    const uint64_t* sA = a.abits + (size_t)s * a.AW;
+    const uint64_t* sA = sAs ? sAs : a.abits + (size_t)s * a.AW;
     if (!(a.fastgate && x.up && __ldg(a.upset + s)) && !bw_contiguous<TS>(a, tA, sA)) {
       gated = true;
       return true;
@@ -309,7 +311,7 @@ __device__ __forceinline__ bool pair_cost(const LevelLaunch& a, const Target<V>&
   if (acc_ok && a.memcheck) acc_ok = !(mem_blk > (V)a.mlim);
   const V proc = (V)(x.acc - (V)r.acc);
   if (acc_ok && need(proc)) {
-    acc = acc_block_cost<V, TRAIN, TS>(a, s, r, proc, x, tA, tInt);
+    acc = acc_block_cost<V, TRAIN, TS>(a, s, r, proc, x, tA, tInt, sAs);
     DSG_STAT(a, 2, 1);
   }
   return true;
@@ -503,11 +505,13 @@ __device__ __forceinline__ unsigned scan_sources(const LevelLaunch& a, const Tar
           if (c < C) thr = vmax(thr, row[c - LP1] < best[c] ? best[c] : NEG);
         return proc < thr;
       };
-      pair_cost<V, TRAIN, TS, decltype(need), STAGED>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk,
-                                                      need, sv.rec + (s - sv.base));
+      pair_cost<V, TRAIN, TS, decltype(need), STAGED>(
+          a, x, s, tA, tInt, gated, acc, cpu, mem_blk, need, sv.rec + (s - sv.base),
+          STAGED && TRAIN ? sv.bits + (size_t)(s - sv.base) * AWp : nullptr);
     } else {
-      pair_cost<V, TRAIN, TS, AlwaysNeeded, STAGED>(a, x, s, tA, tInt, gated, acc, cpu, mem_blk,
-                                                    AlwaysNeeded(), sv.rec + (s - sv.base));
+      pair_cost<V, TRAIN, TS, AlwaysNeeded, STAGED>(
+          a, x, s, tA, tInt, gated, acc, cpu, mem_blk, AlwaysNeeded(), sv.rec + (s - sv.base),
+          STAGED && TRAIN ? sv.bits + (size_t)(s - sv.base) * AWp : nullptr);
     }
     if (gated) continue;
     DSG_STAT(a, 3, 1);
