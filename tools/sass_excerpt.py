@@ -28,8 +28,18 @@ for f in re.split(r"\n\s*Function : ", txt)[1:]:
     for i, l in enumerate(lines):
         if "UBLKCP" in l or "SYNCS" in l:
             print("  " + l)
-    first_vote = next(i for i, l in enumerate(lines) if "VOTE.ANY" in l)
+    # the staged subset test: LDS.128 source rows against the target words
+    # (LOP3), then the warp vote on 'any lane nested'
+    hot = None
+    for i, l in enumerate(lines):
+        if "LDS.128" in l:
+            v = next((j for j in range(i, min(len(lines), i + 40)) if "VOTE" in lines[j]), None)
+            if v is not None:
+                hot = (i, v)
+                break
+    if hot is None:
+        hot = (next(i for i, l in enumerate(lines) if "VOTE.ANY" in l),) * 2
     print("\n-- staged scan loop (subset test on LDS.128 rows, warp vote):")
-    for l in lines[max(0, first_vote - 40):first_vote + 4]:
+    for l in lines[max(0, hot[0] - 12):hot[1] + 8]:
         print("  " + l)
     break
